@@ -1,0 +1,134 @@
+/*
+ * cpsjoin_b200.h -- C ABI of the B200 CPSJoin self-join path.
+ *
+ * The reference (simjoin, pure Python) exposes this path as a Python API,
+ * not an FFI; each entry point below names the reference function it
+ * replaces.  Conventions:
+ *   - plain pointers and sizes only; "d_" = device pointer (caller-owned,
+ *     e.g. torch tensors' data_ptr()), "h_" = host pointer;
+ *   - every call takes the CUDA stream to run on (cudaStream_t as void*,
+ *     NULL = legacy default stream) and is stream-ordered;
+ *   - return 0 on success, a negative CPSJ_E* code on failure; the message
+ *     is available from cpsj_last_error(ctx) (thread-local to the context);
+ *   - no host threads are spawned; one context per device.
+ */
+#ifndef CPSJOIN_B200_H
+#define CPSJOIN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPSJ_OK 0
+#define CPSJ_E_ARG -1      /* invalid argument (reference: ValueError)      */
+#define CPSJ_E_CUDA -2     /* CUDA runtime error                            */
+#define CPSJ_E_OOM -3      /* device allocation failed                      */
+#define CPSJ_E_PICK -4     /* node-sketch pick index == m (reference raises
+                              IndexError at cpsjoin.py:193; p ~ 2^-54)      */
+
+typedef struct cpsj_ctx cpsj_ctx;
+typedef struct cpsj_family cpsj_family;
+
+/* library version, (major << 16) | minor */
+int cpsj_version(void);
+
+/* context: device selection + stream-ordered memory pool + result arena */
+int cpsj_ctx_create(int device, cpsj_ctx **out);
+int cpsj_ctx_destroy(cpsj_ctx *ctx);
+const char *cpsj_last_error(const cpsj_ctx *ctx);
+
+/*
+ * A family of F tabulation-hash MinHash functions made device-resident.
+ * h_minhash_tables: (F, 4, 256) u64, the reference's table layout
+ *   (EmbeddingParams.tables, embed.py:44-45; SketchFamily.minhash_tables,
+ *   hashing.py:175-176).
+ * h_bit_tables: (F, 4, 256) u64 or NULL (SketchFamily.bit_tables,
+ *   hashing.py:177-178); required to produce sketches.
+ */
+int cpsj_family_create(cpsj_ctx *ctx, const uint64_t *h_minhash_tables,
+                       const uint64_t *h_bit_tables, int32_t n_functions,
+                       cpsj_family **out);
+int cpsj_family_destroy(cpsj_family *fam);
+
+/*
+ * K1: MinHash values and/or 1-bit minwise sketches of n_sets CSR sets.
+ * Replaces: minhash_segments (hashing.py:129-146) as looped by
+ *   embed_dataset (embed.py:117-128) -> d_values_out (n_sets, F) u32; and
+ *   build_sketch_matrix (hashing.py:197-211) -> d_sketch_out
+ *   (n_sets, F/64) u64 (F must be a multiple of 64 for sketches).
+ * d_tokens: u32 column indices sorted ascending per set (core.py:29,74);
+ * d_offsets: int64, n_sets + 1; every set non-empty.
+ * max_token: an upper bound on every token (selects the key-byte count).
+ * Either output may be NULL.
+ */
+int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam,
+                        const uint32_t *d_tokens, const int64_t *d_offsets,
+                        int64_t n_sets, uint32_t max_token,
+                        uint32_t *d_values_out, uint64_t *d_sketch_out,
+                        void *stream);
+
+/* device inputs of a self-join: the EmbeddedDataset fields the engine reads
+ * (cpsjoin.py:95-108) */
+typedef struct {
+    const uint32_t *d_tokens;   /* verify_csr.indices  (nnz)            */
+    const int64_t *d_offsets;   /* verify_csr.indptr   (n + 1)          */
+    const int32_t *d_sizes;     /* emb.sizes           (n)              */
+    int64_t n;
+    const uint32_t *d_values;   /* emb.values          (n, t) row-major */
+    int32_t t;
+    const uint64_t *d_sketch;   /* emb.sketches(ell, seed)  (n, ell)    */
+    int32_t ell;
+} cpsj_inputs;
+
+/* host-derived plan; every float rule is pre-reduced to an integer
+ * threshold by the host with numpy semantics */
+typedef struct {
+    double lambda_;          /* verification threshold J >= lambda_           */
+    int32_t limit;           /* brute-force size limit (cpsjoin.py:259)        */
+    int32_t depth_cap;       /* cpsjoin.py:294                                 */
+    int32_t accept_dist;     /* sketch filter: popcount(xor) <= accept_dist
+                                (== 64*ell - k*, cpsjoin.py:150-152)          */
+    int32_t flag_dist;       /* flag rule: dist <= flag_dist (-1: never)
+                                (cpsjoin.py:268 with _sketch_estimates)        */
+    double split_p;          /* 1.0 / (lambda_ * t) (cpsjoin.py:234)           */
+    const uint64_t *h_rep_seeds;  /* repetition tree seeds (cpsjoin.py:346) */
+    int32_t n_reps;
+} cpsj_plan;
+
+typedef struct {
+    int64_t n_pairs;          /* unique verified pairs                        */
+    int64_t pre_candidates;   /* core.py Counters                             */
+    int64_t candidates;
+    int64_t results;
+    int64_t max_depth;
+    int64_t peak_live_members;/* DFS stack peak, reproduced exactly            */
+    int64_t n_depth_cap_events;
+    int64_t n_levels;         /* frontier levels processed                    */
+    int64_t gpu_launches;     /* kernels launched by this call                */
+} cpsj_join_stats;
+
+/*
+ * K2..K6: cpsjoin_self (cpsjoin.py:331-351) over all repetitions as one
+ * level-synchronous frontier.  The sorted-unique result keys
+ * ((min_row << 32) | max_row) and similarities stay in a ctx-owned arena
+ * until the next join call; fetch them with cpsj_join_copy_result.
+ */
+int cpsj_self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
+                   cpsj_join_stats *stats, void *stream);
+
+/* copy the last join's pairs (and optionally the survivor counts of
+ * depth-capped nodes, one per reference warning, cpsjoin.py:295-296) */
+int cpsj_join_copy_result(cpsj_ctx *ctx, uint64_t *h_keys, double *h_sims,
+                          int64_t capacity, int64_t *h_depth_cap_sizes,
+                          int64_t depth_cap_capacity, void *stream);
+
+/* device pointers to the last join's arena (valid until the next call) */
+int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys,
+                            const double **d_sims, int64_t *n_pairs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

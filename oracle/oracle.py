@@ -1,0 +1,208 @@
+"""ctypes front-end of the C oracle (cpsj_oracle.c) -- TEST INFRASTRUCTURE ONLY.
+
+Restates the reference's host-side parameter derivation with the same
+numpy/scipy calls (hashing.py:43-46 seed plumbing, :168-178 table draw
+order, embed.py:39-45, cpsjoin.py:346-347 repetition seeds,
+hashing.py:234-247 k*), and drives the C restatement of the hot path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_build", "libcpsj_oracle.so")
+_lib = None
+
+KIND_EMBED, KIND_SKETCH, KIND_CPS_TREE = 1, 2, 3
+
+
+def build() -> str:
+    src = os.path.join(_HERE, "cpsj_oracle.c")
+    if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            build()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        i64, i32, u64, dbl = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
+        L.orc_mix64.restype = u64
+        L.orc_mix64.argtypes = [u64]
+        L.orc_word_stream.argtypes = [u64, i64, u64, P]
+        L.orc_minhash.argtypes = [P, P, i64, P, i32, P, ctypes.c_int]
+        L.orc_sketch.argtypes = [P, P, i64, P, P, i32, P, ctypes.c_int]
+        L.orc_self_join.restype = ctypes.c_int
+        L.orc_self_join.argtypes = [P, P, P, i64, P, i32, P, i32, dbl, dbl, i32, i32, i32,
+                                    P, i32, ctypes.c_int,
+                                    ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64),
+                                    P, ctypes.POINTER(P), ctypes.POINTER(i64)]
+        L.orc_exact_join.restype = ctypes.c_int
+        L.orc_exact_join.argtypes = [P, P, i64, ctypes.c_uint32, dbl, ctypes.c_int,
+                                     ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)]
+        L.orc_free.argtypes = [P]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ---------------------------------------------------------------- host params
+
+def derive_rng(master_seed: int, *path: int) -> np.random.Generator:
+    # hashing.py:43-46
+    return np.random.default_rng(np.random.SeedSequence(master_seed, spawn_key=tuple(path)))
+
+
+def embedding_tables(t: int, seed: int) -> np.ndarray:
+    # embed.py:44-45
+    return derive_rng(seed, KIND_EMBED).integers(0, 2**64, size=(t, 4, 256), dtype=np.uint64)
+
+
+def sketch_tables(ell: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    # hashing.py:174-178: minhash tables first, then bit tables, one stream
+    rng = derive_rng(seed, KIND_SKETCH)
+    bits = 64 * ell
+    mh = rng.integers(0, 2**64, size=(bits, 4, 256), dtype=np.uint64)
+    bt = rng.integers(0, 2**64, size=(bits, 4, 256), dtype=np.uint64)
+    return mh, bt
+
+
+def rep_seeds(seed: int, reps: int) -> np.ndarray:
+    # cpsjoin.py:346-347
+    return derive_rng(seed, KIND_CPS_TREE).integers(0, 2**64, size=reps, dtype=np.uint64)
+
+
+def kstar(lam: float, delta: float, mbits: int) -> int:
+    # hashing.py:246-247
+    from scipy.stats import binom
+    return int(binom.ppf(delta, mbits, (1.0 + lam) / 2.0))
+
+
+# ---------------------------------------------------------------- kernels
+
+def mix64(x: int) -> int:
+    return int(lib().orc_mix64(x))
+
+
+def word_stream(seed: int, n: int, offset: int = 0) -> np.ndarray:
+    out = np.empty(n, dtype=np.uint64)
+    lib().orc_word_stream(seed, n, offset, _p(out))
+    return out
+
+
+def _csr(tokens, offsets):
+    return (np.ascontiguousarray(tokens, dtype=np.uint32),
+            np.ascontiguousarray(offsets, dtype=np.int64))
+
+
+def minhash(tokens, offsets, tables, threads: int = 0) -> np.ndarray:
+    tok, off = _csr(tokens, offsets)
+    tables = np.ascontiguousarray(tables, dtype=np.uint64)
+    n, F = len(off) - 1, tables.shape[0]
+    out = np.zeros((n, F), dtype=np.uint32)
+    lib().orc_minhash(_p(tok), _p(off), n, _p(tables), F, _p(out), threads)
+    return out
+
+
+def sketch(tokens, offsets, mh_tables, bit_tables, threads: int = 0) -> np.ndarray:
+    tok, off = _csr(tokens, offsets)
+    mh = np.ascontiguousarray(mh_tables, dtype=np.uint64)
+    bt = np.ascontiguousarray(bit_tables, dtype=np.uint64)
+    n, ell = len(off) - 1, mh.shape[0] // 64
+    out = np.zeros((n, ell), dtype=np.uint64)
+    lib().orc_sketch(_p(tok), _p(off), n, _p(mh), _p(bt), ell, _p(out), threads)
+    return out
+
+
+@dataclass
+class JoinOut:
+    keys: np.ndarray      # u64 (lo << 32) | hi, ascending, unique
+    sims: np.ndarray      # f64
+    pre_candidates: int
+    candidates: int
+    results: int
+    max_depth: int
+    peak_live_members: int
+    cap_events: np.ndarray
+    error: int
+
+    @property
+    def a(self):
+        return (self.keys >> np.uint64(32)).astype(np.int64)
+
+    @property
+    def b(self):
+        return (self.keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
+
+
+def _take(ptr, n, dtype):
+    L = lib()
+    if n:
+        buf = (ctypes.c_char * (n * np.dtype(dtype).itemsize)).from_address(ptr.value)
+        arr = np.frombuffer(bytes(buf), dtype=dtype).copy()
+    else:
+        arr = np.zeros(0, dtype=dtype)
+    L.orc_free(ptr)
+    return arr
+
+
+def self_join(tokens, offsets, sizes, values, sketches, lam: float, *, epsilon=0.1, limit=250,
+              delta=0.05, repetitions=10, seed=0, depth_cap=64, threads: int = 0) -> JoinOut:
+    """cpsjoin.py:331-351 on explicit arrays (self-join, source_ids = arange)."""
+    tok, off = _csr(tokens, offsets)
+    sizes = np.ascontiguousarray(sizes, dtype=np.int64)
+    values = np.ascontiguousarray(values, dtype=np.uint32)
+    sk = np.ascontiguousarray(sketches, dtype=np.uint64)
+    n, t = values.shape
+    ell = sk.shape[1]
+    ks = kstar(lam, delta, 64 * ell)
+    seeds = rep_seeds(seed, repetitions)
+    kp, sp, cp = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    nk, nc = ctypes.c_int64(), ctypes.c_int64()
+    counters = np.zeros(5, dtype=np.int64)
+    err = lib().orc_self_join(_p(tok), _p(off), _p(sizes), n, _p(values), t, _p(sk), ell,
+                              float(lam), float(epsilon), int(limit), ks, int(depth_cap),
+                              _p(seeds), int(repetitions), threads,
+                              ctypes.byref(kp), ctypes.byref(sp), ctypes.byref(nk),
+                              _p(counters), ctypes.byref(cp), ctypes.byref(nc))
+    keys = _take(kp, nk.value, np.uint64)
+    sims = _take(sp, nk.value, np.float64)
+    ev = _take(cp, nc.value, np.int64)
+    return JoinOut(keys, sims, int(counters[0]), int(counters[1]), int(counters[2]),
+                   int(counters[3]), int(counters[4]), ev, int(err))
+
+
+def exact_join(tokens, offsets, d: int, lam: float, threads: int = 0):
+    """All pairs with J >= lam (recall ground truth).  Returns (keys, sims)."""
+    tok, off = _csr(tokens, offsets)
+    n = len(off) - 1
+    kp, sp = ctypes.c_void_p(), ctypes.c_void_p()
+    nk = ctypes.c_int64()
+    lib().orc_exact_join(_p(tok), _p(off), n, int(d), float(lam), threads,
+                         ctypes.byref(kp), ctypes.byref(sp), ctypes.byref(nk))
+    return _take(kp, nk.value, np.uint64), _take(sp, nk.value, np.float64)
+
+
+def full_pipeline(tokens, offsets, sizes, *, lam, t=128, emb_seed=0, ell=8, seed=0,
+                  repetitions=10, epsilon=0.1, limit=250, delta=0.05, depth_cap=64,
+                  threads: int = 0):
+    """embed_dataset + sketches + cpsjoin_self, as the reference runs them."""
+    values = minhash(tokens, offsets, embedding_tables(t, emb_seed), threads)
+    mh, bt = sketch_tables(ell, seed)
+    sk = sketch(tokens, offsets, mh, bt, threads)
+    out = self_join(tokens, offsets, sizes, values, sk, lam, epsilon=epsilon, limit=limit,
+                    delta=delta, repetitions=repetitions, seed=seed, depth_cap=depth_cap,
+                    threads=threads)
+    return values, sk, out

@@ -1,0 +1,146 @@
+// Shared device helpers and the context object of the B200 CPSJoin library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/cpsjoin_b200.h"
+
+namespace cpsj {
+
+// ---------------------------------------------------------------- errors
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+#define CPSJ_CUDA(call)                                                                 \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw ::cpsj::Error{e_ == cudaErrorMemoryAllocation ? CPSJ_E_OOM : CPSJ_E_CUDA, \
+                                std::string(#call) + ": " + cudaGetErrorString(e_)};     \
+    } while (0)
+
+#define CPSJ_LAUNCH_CHECK() CPSJ_CUDA(cudaGetLastError())
+
+inline void require(bool ok, const std::string &msg) {
+    if (!ok) throw Error{CPSJ_E_ARG, msg};
+}
+
+// ------------------------------------------------- stream-ordered buffers
+
+template <typename T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DevBuf &operator=(DevBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count, cudaStream_t stream) {
+        release();
+        s = stream;
+        n = count;
+        if (count) CPSJ_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), stream));
+    }
+    // grow to at least `count` elements, keeping the first `keep` elements
+    void grow(size_t count, size_t keep, cudaStream_t stream) {
+        if (count <= n) return;
+        T *q = nullptr;
+        CPSJ_CUDA(cudaMallocAsync((void **)&q, count * sizeof(T), stream));
+        if (keep && p) CPSJ_CUDA(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, stream));
+        release();
+        p = q;
+        n = count;
+        s = stream;
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    T *get() const { return p; }
+};
+
+// ---------------------------------------------------------------- hashing
+
+// SplitMix64 finaliser (reference hashing.py:49-56)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// word k of a node's counter stream (hashing.py:59-63)
+__host__ __device__ __forceinline__ uint64_t stream_word(uint64_t seed, uint64_t k) {
+    return mix64(seed ^ mix64(k));
+}
+
+// uniform_stream element (hashing.py:66-68): u64 -> f64 rounds to nearest
+// even exactly like numpy's cast, then an exact scaling by 2^-64.
+__device__ __forceinline__ double stream_uniform(uint64_t seed, uint64_t k) {
+    return __ull2double_rn(stream_word(seed, k)) * 0x1p-64;
+}
+
+// size filter of cpsjoin.py:134: min >= lam * max - 1e-9, evaluated with
+// the same two IEEE roundings numpy performs (no FMA contraction).
+__device__ __forceinline__ bool size_filter(int sa, int sb, double lam) {
+    int mn = sa < sb ? sa : sb, mx = sa < sb ? sb : sa;
+    return (double)mn >= __dsub_rn(__dmul_rn(lam, (double)mx), 1e-9);
+}
+
+__device__ __forceinline__ int64_t upper_bound_i64(const int64_t *a, int64_t n, int64_t x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+}  // namespace cpsj
+
+// -------------------------------------------------------------- context
+
+struct cpsj_ctx {
+    int device = 0;
+    std::string err;
+    int sm_count = 0;
+    // result arena of the last join
+    cpsj::DevBuf<uint64_t> res_keys;
+    cpsj::DevBuf<double> res_sims;
+    int64_t n_pairs = 0;
+    std::vector<int64_t> cap_events;
+    // pinned scratch for small device->host reads
+    int64_t *h_scalars = nullptr;
+    int64_t launches = 0;
+};
+
+struct cpsj_family {
+    cpsj_ctx *ctx = nullptr;
+    int32_t F = 0;
+    uint32_t *d_hi = nullptr;       // [F][4][256] high words of the u64 tables
+    uint32_t *d_lo = nullptr;       // [F][4][256] low words
+    uint32_t *d_bitmask = nullptr;  // [F][4][8] low bits of the bit tables, or null
+};
+
+namespace cpsj {
+int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,
+                   const int64_t *d_offsets, int64_t n, uint32_t max_token, uint32_t *d_values,
+                   uint64_t *d_sketch, cudaStream_t stream);
+void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
+               cudaStream_t stream);
+}  // namespace cpsj
