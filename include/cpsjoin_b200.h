@@ -17,6 +17,12 @@
 
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define CPSJ_API __attribute__((visibility("default")))
+#else
+#define CPSJ_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -32,12 +38,12 @@ typedef struct cpsj_ctx cpsj_ctx;
 typedef struct cpsj_family cpsj_family;
 
 /* library version, (major << 16) | minor */
-int cpsj_version(void);
+CPSJ_API int cpsj_version(void);
 
 /* context: device selection + stream-ordered memory pool + result arena */
-int cpsj_ctx_create(int device, cpsj_ctx **out);
-int cpsj_ctx_destroy(cpsj_ctx *ctx);
-const char *cpsj_last_error(const cpsj_ctx *ctx);
+CPSJ_API int cpsj_ctx_create(int device, cpsj_ctx **out);
+CPSJ_API int cpsj_ctx_destroy(cpsj_ctx *ctx);
+CPSJ_API const char *cpsj_last_error(const cpsj_ctx *ctx);
 
 /*
  * A family of F tabulation-hash MinHash functions made device-resident.
@@ -47,10 +53,10 @@ const char *cpsj_last_error(const cpsj_ctx *ctx);
  * h_bit_tables: (F, 4, 256) u64 or NULL (SketchFamily.bit_tables,
  *   hashing.py:177-178); required to produce sketches.
  */
-int cpsj_family_create(cpsj_ctx *ctx, const uint64_t *h_minhash_tables,
+CPSJ_API int cpsj_family_create(cpsj_ctx *ctx, const uint64_t *h_minhash_tables,
                        const uint64_t *h_bit_tables, int32_t n_functions,
                        cpsj_family **out);
-int cpsj_family_destroy(cpsj_family *fam);
+CPSJ_API int cpsj_family_destroy(cpsj_family *fam);
 
 /*
  * K1: MinHash values and/or 1-bit minwise sketches of n_sets CSR sets.
@@ -63,7 +69,7 @@ int cpsj_family_destroy(cpsj_family *fam);
  * max_token: an upper bound on every token (selects the key-byte count).
  * Either output may be NULL.
  */
-int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam,
+CPSJ_API int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam,
                         const uint32_t *d_tokens, const int64_t *d_offsets,
                         int64_t n_sets, uint32_t max_token,
                         uint32_t *d_values_out, uint64_t *d_sketch_out,
@@ -115,17 +121,17 @@ typedef struct {
  * ((min_row << 32) | max_row) and similarities stay in a ctx-owned arena
  * until the next join call; fetch them with cpsj_join_copy_result.
  */
-int cpsj_self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
+CPSJ_API int cpsj_self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
                    cpsj_join_stats *stats, void *stream);
 
 /* copy the last join's pairs (and optionally the survivor counts of
  * depth-capped nodes, one per reference warning, cpsjoin.py:295-296) */
-int cpsj_join_copy_result(cpsj_ctx *ctx, uint64_t *h_keys, double *h_sims,
+CPSJ_API int cpsj_join_copy_result(cpsj_ctx *ctx, uint64_t *h_keys, double *h_sims,
                           int64_t capacity, int64_t *h_depth_cap_sizes,
                           int64_t depth_cap_capacity, void *stream);
 
 /* device pointers to the last join's arena (valid until the next call) */
-int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys,
+CPSJ_API int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys,
                             const double **d_sims, int64_t *n_pairs);
 
 #ifdef __cplusplus

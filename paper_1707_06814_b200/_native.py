@@ -1,0 +1,138 @@
+"""ctypes binding of the sm_100a library (include/cpsjoin_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing or
+no CUDA device is present, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .build import SO
+
+P = ctypes.c_void_p
+i32, i64, u32, u64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double
+
+CPSJ_E_ARG, CPSJ_E_CUDA, CPSJ_E_OOM, CPSJ_E_PICK = -1, -2, -3, -4
+
+
+class Inputs(ctypes.Structure):
+    _fields_ = [("d_tokens", P), ("d_offsets", P), ("d_sizes", P), ("n", i64),
+                ("d_values", P), ("t", i32), ("d_sketch", P), ("ell", i32)]
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("lambda_", dbl), ("limit", i32), ("depth_cap", i32), ("accept_dist", i32),
+                ("flag_dist", i32), ("split_p", dbl), ("h_rep_seeds", P), ("n_reps", i32)]
+
+
+class JoinStats(ctypes.Structure):
+    _fields_ = [("n_pairs", i64), ("pre_candidates", i64), ("candidates", i64), ("results", i64),
+                ("max_depth", i64), ("peak_live_members", i64), ("n_depth_cap_events", i64),
+                ("n_levels", i64), ("gpu_launches", i64)]
+
+
+EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_error",
+           "cpsj_family_create", "cpsj_family_destroy", "cpsj_minhash_sketch", "cpsj_self_join",
+           "cpsj_join_copy_result", "cpsj_join_result_device"]
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def load(path: str | None = None):
+    """Load (never build) the shared library; raises if it is absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        so = path or SO
+        if not os.path.exists(so):
+            raise ImportError(f"CUDA library not built: {so} (run python -m paper_1707_06814_b200.build)")
+        L = ctypes.CDLL(so)
+        L.cpsj_version.restype = ctypes.c_int
+        L.cpsj_ctx_create.argtypes = [ctypes.c_int, ctypes.POINTER(P)]
+        L.cpsj_ctx_destroy.argtypes = [P]
+        L.cpsj_last_error.restype = ctypes.c_char_p
+        L.cpsj_last_error.argtypes = [P]
+        L.cpsj_family_create.argtypes = [P, P, P, i32, ctypes.POINTER(P)]
+        L.cpsj_family_destroy.argtypes = [P]
+        L.cpsj_minhash_sketch.argtypes = [P, P, P, P, i64, u32, P, P, P]
+        L.cpsj_self_join.argtypes = [P, ctypes.POINTER(Inputs), ctypes.POINTER(Plan),
+                                     ctypes.POINTER(JoinStats), P]
+        L.cpsj_join_copy_result.argtypes = [P, P, P, i64, P, i64, P]
+        L.cpsj_join_result_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)]
+        _lib = L
+        return L
+
+
+def check(ctx, rc: int) -> None:
+    if rc == 0:
+        return
+    msg = load().cpsj_last_error(ctx).decode(errors="replace") if ctx else "error"
+    if rc == CPSJ_E_ARG:
+        raise ValueError(msg)
+    if rc == CPSJ_E_PICK:
+        raise IndexError(msg)
+    if rc == CPSJ_E_OOM:
+        raise MemoryError(msg)
+    raise NativeError(f"cpsjoin_b200 error {rc}: {msg}")
+
+
+class Context:
+    """One library context per CUDA device."""
+
+    _by_device: dict = {}
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lib = load()
+        h = P()
+        check(None, self.lib.cpsj_ctx_create(device, ctypes.byref(h)))
+        self.handle = h
+
+    @classmethod
+    def get(cls, device: int | None = None) -> "Context":
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("cpsjoin_b200 needs a CUDA device; no CPU fallback exists")
+        if device is None:
+            device = torch.cuda.current_device()
+        ctx = cls._by_device.get(device)
+        if ctx is None:
+            ctx = cls._by_device[device] = Context(device)
+        return ctx
+
+    def check(self, rc: int) -> None:
+        check(self.handle, rc)
+
+
+class Family:
+    """A device-resident tabulation-hash family (minhash + optional bit tables)."""
+
+    def __init__(self, ctx: Context, minhash_tables, bit_tables=None):
+        import numpy as np
+        mh = np.ascontiguousarray(minhash_tables, dtype=np.uint64)
+        bt = None if bit_tables is None else np.ascontiguousarray(bit_tables, dtype=np.uint64)
+        if mh.ndim != 3 or mh.shape[1:] != (4, 256):
+            raise ValueError("tables must have shape (F, 4, 256)")
+        self.ctx = ctx
+        self.F = mh.shape[0]
+        self.has_bits = bt is not None
+        h = P()
+        ctx.check(ctx.lib.cpsj_family_create(ctx.handle, mh.ctypes.data, None if bt is None else bt.ctypes.data,
+                                             self.F, ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.ctx.lib.cpsj_family_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass

@@ -1,0 +1,162 @@
+// C ABI entry points (include/cpsjoin_b200.h): argument checks, error
+// capture, context and family lifetime.  No C++ exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+
+#include "cpsj_common.cuh"
+
+namespace cpsj {
+void prepare_family(cpsj_ctx *ctx, cpsj_family *fam, const uint64_t *h_mh, const uint64_t *h_bt,
+                    cudaStream_t stream);
+}
+
+namespace {
+
+template <typename F>
+int guarded(cpsj_ctx *ctx, F &&f) {
+    try {
+        f();
+        if (ctx) ctx->err.clear();
+        return CPSJ_OK;
+    } catch (const cpsj::Error &e) {
+        if (ctx) ctx->err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        if (ctx) ctx->err = "host allocation failed";
+        return CPSJ_E_OOM;
+    } catch (...) {
+        if (ctx) ctx->err = "unknown error";
+        return CPSJ_E_CUDA;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int cpsj_version(void) { return (1 << 16) | 0; }
+
+int cpsj_ctx_create(int device, cpsj_ctx **out) {
+    if (out == nullptr) return CPSJ_E_ARG;
+    *out = nullptr;
+    cpsj_ctx *ctx = new (std::nothrow) cpsj_ctx();
+    if (!ctx) return CPSJ_E_OOM;
+    int rc = guarded(ctx, [&] {
+        CPSJ_CUDA(cudaSetDevice(device));
+        ctx->device = device;
+        CPSJ_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+        // keep freed pool memory cached across calls (stream-ordered allocator)
+        cudaMemPool_t pool;
+        CPSJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        CPSJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        CPSJ_CUDA(cudaMallocHost(&ctx->h_scalars, 16 * sizeof(int64_t)));
+    });
+    if (rc != CPSJ_OK) {
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return CPSJ_OK;
+}
+
+int cpsj_ctx_destroy(cpsj_ctx *ctx) {
+    if (!ctx) return CPSJ_OK;
+    int rc = guarded(ctx, [&] {
+        CPSJ_CUDA(cudaSetDevice(ctx->device));
+        CPSJ_CUDA(cudaDeviceSynchronize());
+        ctx->res_keys.release();
+        ctx->res_sims.release();
+        if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
+        ctx->h_scalars = nullptr;
+    });
+    delete ctx;
+    return rc;
+}
+
+const char *cpsj_last_error(const cpsj_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int cpsj_family_create(cpsj_ctx *ctx, const uint64_t *h_minhash_tables, const uint64_t *h_bit_tables,
+                       int32_t n_functions, cpsj_family **out) {
+    if (!ctx || !out) return CPSJ_E_ARG;
+    *out = nullptr;
+    cpsj_family *fam = new (std::nothrow) cpsj_family();
+    if (!fam) return CPSJ_E_OOM;
+    int rc = guarded(ctx, [&] {
+        cpsj::require(h_minhash_tables != nullptr, "minhash tables are null");
+        cpsj::require(n_functions >= 1, "need at least one function");
+        CPSJ_CUDA(cudaSetDevice(ctx->device));
+        fam->ctx = ctx;
+        fam->F = n_functions;
+        cpsj::prepare_family(ctx, fam, h_minhash_tables, h_bit_tables, nullptr);
+    });
+    if (rc != CPSJ_OK) {
+        cpsj_family_destroy(fam);
+        return rc;
+    }
+    *out = fam;
+    return CPSJ_OK;
+}
+
+int cpsj_family_destroy(cpsj_family *fam) {
+    if (!fam) return CPSJ_OK;
+    if (fam->d_hi) cudaFree(fam->d_hi);
+    if (fam->d_lo) cudaFree(fam->d_lo);
+    if (fam->d_bitmask) cudaFree(fam->d_bitmask);
+    delete fam;
+    return CPSJ_OK;
+}
+
+int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,
+                        const int64_t *d_offsets, int64_t n_sets, uint32_t max_token, uint32_t *d_values_out,
+                        uint64_t *d_sketch_out, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(n_sets == 0 || (d_tokens && d_offsets), "null CSR pointers");
+        cpsj::minhash_sketch(ctx, fam, d_tokens, d_offsets, n_sets, max_token, d_values_out, d_sketch_out,
+                             (cudaStream_t)stream);
+    });
+}
+
+int cpsj_self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
+                   void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(in && plan && stats, "null argument");
+        cpsj::require(in->n < (int64_t)1 << 31, "at most 2^31 - 1 sets");
+        cpsj::require(in->n < 2 || (in->d_tokens && in->d_offsets && in->d_sizes && in->d_values && in->d_sketch),
+                      "null input pointers");
+        cpsj::require(plan->n_reps == 0 || plan->h_rep_seeds != nullptr, "null repetition seeds");
+        cpsj::self_join(ctx, in, plan, stats, (cudaStream_t)stream);
+    });
+}
+
+int cpsj_join_copy_result(cpsj_ctx *ctx, uint64_t *h_keys, double *h_sims, int64_t capacity,
+                          int64_t *h_depth_cap_sizes, int64_t depth_cap_capacity, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cudaStream_t st = (cudaStream_t)stream;
+        const int64_t n = ctx->n_pairs < capacity ? ctx->n_pairs : capacity;
+        if (n > 0 && h_keys)
+            CPSJ_CUDA(cudaMemcpyAsync(h_keys, ctx->res_keys.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        if (n > 0 && h_sims)
+            CPSJ_CUDA(cudaMemcpyAsync(h_sims, ctx->res_sims.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        const int64_t ne = (int64_t)ctx->cap_events.size();
+        if (h_depth_cap_sizes)
+            std::memcpy(h_depth_cap_sizes, ctx->cap_events.data(),
+                        (size_t)(ne < depth_cap_capacity ? ne : depth_cap_capacity) * sizeof(int64_t));
+    });
+}
+
+int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys, const double **d_sims, int64_t *n_pairs) {
+    if (!ctx) return CPSJ_E_ARG;
+    if (d_keys) *d_keys = ctx->res_keys.p;
+    if (d_sims) *d_sims = ctx->res_sims.p;
+    if (n_pairs) *n_pairs = ctx->n_pairs;
+    return CPSJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,821 @@
+// K2..K6: the Chosen Path self-join as a level-synchronous frontier (B200).
+//
+// Replaces cpsjoin_self (cpsjoin.py:331-351) and everything under it:
+//   _run_tree           cpsjoin.py:278-305  -> host level loop below
+//   brute_force_step    cpsjoin.py:248-275  -> k_plan / k_node_sketch /
+//                                              k_flags / k_point / k_survivors
+//   node_sketch         cpsjoin.py:182-198  -> k_node_sketch
+//   _sketch_estimates   cpsjoin.py:201-206  -> k_flags (integer threshold)
+//   brute_force_pairs   cpsjoin.py:139-157  -> k_leaf_tiles (K4)
+//   brute_force_point   cpsjoin.py:159-171  -> k_point
+//   _size_side_filter   cpsjoin.py:129-137  -> size_filter()
+//   _verify_and_emit    cpsjoin.py:114-127  -> k_verify (K5)
+//   split_buckets       cpsjoin.py:222-245  -> k_select / k_build_keys /
+//                                              radix sort / k_children (K3)
+//   _build_self_pairs   cpsjoin.py:308-319  -> sort + unique (K6)
+//
+// Why a BFS is exact: a node's processing depends only on (members, depth,
+// seed) and the immutable dataset arrays; emissions and counters are
+// commutative sums.  All repetitions share one
+// frontier.  Member lists stay ascending by row (root = arange(n), the
+// survivor filter keeps order, the split sort is stable).  The DFS-specific
+// peak_live_members is reproduced exactly from the tree: when node v is
+// popped the reference's stack holds the lower-index siblings of every node
+// on the root->v path, so with S(child_j) = S(parent) + sum_{i<j} |child_i|
+// the peak is max(n, max_children S(c) + |c|).
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "cpsj_common.cuh"
+
+namespace cpsj {
+
+namespace {
+
+constexpr int TPB = 256;
+
+struct DevCounters {
+    unsigned long long pre;      // pre_candidates
+    unsigned long long res;      // results
+    unsigned long long cand_n;   // candidate slots used this level
+    unsigned long long res_n;    // result slots used (cumulative)
+    long long peak;              // peak_live_members
+    unsigned long long cap_n;    // depth-cap events
+    int err;                     // CPSJ_E_PICK
+};
+
+inline unsigned blocks_for(int64_t n, int tpb = TPB) {
+    return (unsigned)std::max<int64_t>(1, (n + tpb - 1) / tpb);
+}
+
+// ------------------------------------------------------------- level plan
+
+// per node: leaf tiles (32x32 upper-triangle tiles of the pair space),
+// internal flag + member count; leaf pre-candidates m(m-1)/2 (cps:144)
+__global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit,
+                       int64_t *__restrict__ tiles, int64_t *__restrict__ internal,
+                       int64_t *__restrict__ imem, DevCounters *ctr) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long pre = 0;
+    if (i < N) {
+        const int64_t m = cnt[i];
+        const bool leaf = m <= limit;
+        const int64_t T = (m + 31) / 32;
+        tiles[i] = leaf ? T * (T + 1) / 2 : 0;
+        internal[i] = leaf ? 0 : 1;
+        imem[i] = leaf ? 0 : m;
+        if (leaf) pre = (unsigned long long)(m * (m - 1) / 2);
+    } else if (i == N) {
+        tiles[i] = 0;
+        internal[i] = 0;
+        imem[i] = 0;
+    }
+    // warp-aggregated counter update
+    for (int o = 16; o > 0; o >>= 1) pre += __shfl_down_sync(0xffffffffu, pre, o);
+    if ((threadIdx.x & 31) == 0 && pre) atomicAdd(&ctr->pre, pre);
+}
+
+__global__ void k_compact_internal(int64_t N, const int64_t *__restrict__ internal,
+                                   const int64_t *__restrict__ iscan, int64_t *__restrict__ ilist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N && internal[i]) ilist[iscan[i]] = i;
+}
+
+// ------------------------------------------------------ K4 leaf BruteForce
+
+template <int ELL>
+struct Sk {
+    uint64_t w[ELL];
+};
+
+// one warp per 32x32 tile of a leaf's pair space; lane = column member,
+// loop over the 32 row members; popcount(xor) <= accept passes the sketch
+// filter (matches >= k*), then the size filter; survivors are appended to
+// the candidate list with one atomic per warp (ballot + prefix).
+template <int ELL>
+__global__ void __launch_bounds__(TPB) k_leaf_tiles(
+    int64_t total_tiles, const int64_t *__restrict__ tile_off, int64_t N,
+    const int64_t *__restrict__ nd_off, const int32_t *__restrict__ nd_cnt,
+    const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch, int ell_rt,
+    const int32_t *__restrict__ sizes, int32_t accept, double lam, int2 *__restrict__ cand,
+    unsigned long long cap, DevCounters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (tile >= total_tiles) return;
+    const int ell = ELL > 0 ? ELL : ell_rt;
+    const int64_t node = upper_bound_i64(tile_off, N + 1, tile) - 1;
+    int64_t local = tile - tile_off[node];
+    const int m = nd_cnt[node];
+    const int T = (m + 31) >> 5;
+    int bi = 0;
+    while (local >= T - bi) { local -= T - bi; ++bi; }
+    const int bj = bi + (int)local;
+    const int32_t *mem = members + nd_off[node];
+    const int j = (bj << 5) + lane;
+    const bool jvalid = j < m;
+    const int32_t col = jvalid ? mem[j] : 0;
+    const int32_t col_size = jvalid ? sizes[col] : 0;
+    constexpr int EL = ELL > 0 ? ELL : 1;
+    Sk<EL> cs;
+    if (ELL > 0) {
+#pragma unroll
+        for (int k = 0; k < EL; ++k) cs.w[k] = jvalid ? __ldg(sketch + (size_t)col * ELL + k) : 0;
+    }
+    const int iend = min(m, (bi << 5) + 32);
+    for (int i = bi << 5; i < iend; ++i) {
+        const int32_t row = mem[i];
+        const uint64_t *rs = sketch + (size_t)row * ell;
+        int dist = 0;
+        if (ELL > 0) {
+#pragma unroll
+            for (int k = 0; k < EL; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+        } else {
+            const uint64_t *csp = sketch + (size_t)col * ell;
+            for (int k = 0; k < ell; ++k) dist += __popcll(__ldg(rs + k) ^ (jvalid ? __ldg(csp + k) : 0));
+        }
+        bool pass = jvalid && j > i && dist <= accept;
+        if (pass) pass = size_filter(sizes[row], col_size, lam);
+        const unsigned mask = __ballot_sync(0xffffffffu, pass);
+        if (mask) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(&ctr->cand_n, (unsigned long long)__popc(mask));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (pass) {
+                const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1));
+                if (slot < cap) cand[slot] = make_int2(row, col);
+            }
+        }
+    }
+}
+
+// -------------------------------------------- K2 node sketch + flag rule
+
+// one block per internal node: bit i of the node sketch is bit i of the
+// sketch of member floor(u_i * m), u from the node's counter stream at
+// offset t (cps:192-198).  The f64 product and the truncation round like
+// numpy's; u == 1.0 (w >= 2^64 - 1024) would index past the node and makes
+// the reference raise, so it is reported as CPSJ_E_PICK.
+__global__ void k_node_sketch(const int64_t *__restrict__ ilist, const int64_t *__restrict__ nd_off,
+                              const int32_t *__restrict__ nd_cnt, const uint64_t *__restrict__ nd_seed,
+                              const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch,
+                              int ell, int t, uint32_t *__restrict__ nsk32, DevCounters *ctr) {
+    const int64_t k = blockIdx.x;
+    const int64_t node = ilist[k];
+    const int64_t off = nd_off[node];
+    const int m = nd_cnt[node];
+    const uint64_t seed = nd_seed[node];
+    const int mbits = 64 * ell;
+    for (int base = 0; base < mbits; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        uint32_t bit = 0;
+        if (i < mbits) {
+            const double u = stream_uniform(seed, (uint64_t)t + (uint64_t)i);
+            long long idx = (long long)__dmul_rn(u, (double)m);
+            if (idx >= m) { atomicExch(&ctr->err, CPSJ_E_PICK); idx = m - 1; }
+            const int32_t pick = members[off + idx];
+            bit = (uint32_t)((sketch[(size_t)pick * ell + (i >> 6)] >> (i & 63)) & 1ull);
+        }
+        const uint32_t w = __ballot_sync(0xffffffffu, bit);
+        if ((threadIdx.x & 31) == 0 && i < mbits) nsk32[k * (2 * ell) + (i >> 5)] = w;
+    }
+}
+
+// thread per internal member: flag iff dist(member, node sketch) <=
+// flag_dist, the integer form of est > (1 - eps) * lam (cps:268)
+__global__ void k_flags(int64_t Mi, const int64_t *__restrict__ im_off, int64_t n_int,
+                        const int64_t *__restrict__ ilist, const int64_t *__restrict__ nd_off,
+                        const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch, int ell,
+                        const uint64_t *__restrict__ nsk, int32_t flag_dist, int64_t *__restrict__ flags) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e > Mi) return;
+    if (e == Mi) { flags[e] = 0; return; }
+    const int64_t k = upper_bound_i64(im_off, n_int + 1, e) - 1;
+    const int32_t x = members[nd_off[ilist[k]] + (e - im_off[k])];
+    const uint64_t *a = sketch + (size_t)x * ell, *b = nsk + (size_t)k * ell;
+    int dist = 0;
+    for (int w = 0; w < ell; ++w) dist += __popcll(a[w] ^ b[w]);
+    flags[e] = dist <= flag_dist ? 1 : 0;
+}
+
+__global__ void k_flag_list(int64_t Mi, const int64_t *__restrict__ flags,
+                            const int64_t *__restrict__ fscan, int64_t *__restrict__ flist) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < Mi && flags[e]) flist[fscan[e]] = e;
+}
+
+// one warp per flagged member x at node position p with flag rank r:
+// compared against every member except itself and the flagged members
+// before it (they were removed first, cps:271-274); pre += m - 1 - r.
+__global__ void k_point(int64_t n_flag, const int64_t *__restrict__ flist, const int64_t *__restrict__ fscan,
+                        const int64_t *__restrict__ flags, const int64_t *__restrict__ im_off, int64_t n_int,
+                        const int64_t *__restrict__ ilist, const int64_t *__restrict__ nd_off,
+                        const int32_t *__restrict__ nd_cnt, const int32_t *__restrict__ members,
+                        const uint64_t *__restrict__ sketch, int ell, const int32_t *__restrict__ sizes,
+                        int32_t accept, double lam, int2 *__restrict__ cand, unsigned long long cap,
+                        int count_pre, DevCounters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= n_flag) return;
+    const int64_t e = flist[w];
+    const int64_t k = upper_bound_i64(im_off, n_int + 1, e) - 1;
+    const int64_t node = ilist[k];
+    const int32_t *mem = members + nd_off[node];
+    const int m = nd_cnt[node];
+    const int p = (int)(e - im_off[k]);
+    const int64_t rank = fscan[e] - fscan[im_off[k]];
+    const int32_t x = mem[p];
+    if (count_pre && lane == 0 && m - 1 - rank > 0) atomicAdd(&ctr->pre, (unsigned long long)(m - 1 - rank));
+    const uint64_t *sx = sketch + (size_t)x * ell;
+    const int32_t size_x = sizes[x];
+    const int64_t *fl = flags + im_off[k];
+    for (int base = 0; base < m; base += 32) {
+        const int j = base + lane;
+        bool pass = false;
+        int32_t y = 0;
+        if (j < m) {
+            y = mem[j];
+            const bool removed = fl[j] && j < p;
+            if (y != x && !removed) {
+                const uint64_t *sy = sketch + (size_t)y * ell;
+                int dist = 0;
+                for (int q = 0; q < ell; ++q) dist += __popcll(sx[q] ^ sy[q]);
+                pass = dist <= accept && size_filter(size_x, sizes[y], lam);
+            }
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, pass);
+        if (mask) {
+            unsigned long long b = 0;
+            if (lane == 0) b = atomicAdd(&ctr->cand_n, (unsigned long long)__popc(mask));
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (pass) {
+                const unsigned long long slot = b + __popc(mask & ((1u << lane) - 1));
+                if (slot < cap) cand[slot] = make_int2(x, y);
+            }
+        }
+    }
+}
+
+// survivors of internal nodes, in member order (cps:275)
+__global__ void k_survivors(int64_t Mi, const int64_t *__restrict__ im_off, int64_t n_int,
+                            const int64_t *__restrict__ ilist, const int64_t *__restrict__ nd_off,
+                            const int32_t *__restrict__ members, const int64_t *__restrict__ flags,
+                            const int64_t *__restrict__ fscan, int32_t *__restrict__ surv) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= Mi || flags[e]) return;
+    const int64_t k = upper_bound_i64(im_off, n_int + 1, e) - 1;
+    surv[e - fscan[e]] = members[nd_off[ilist[k]] + (e - im_off[k])];
+}
+
+// ------------------------------------------------------------- K3 split
+
+// one warp per internal node: positions i < t with u_i < 1/(lam t)
+// (cps:233-234).  Nodes with < 2 survivors or at the depth cap do not
+// split; the cap is reported like the reference's warning (cps:294-297).
+__global__ void k_select(int64_t n_int, const int64_t *__restrict__ ilist, const int32_t *__restrict__ nd_cnt,
+                         const uint64_t *__restrict__ nd_seed, int32_t depth, int32_t depth_cap,
+                         const int64_t *__restrict__ im_off, const int64_t *__restrict__ fscan, int t,
+                         double split_p, int16_t *__restrict__ sel_pos, int64_t *__restrict__ nsel,
+                         int64_t *__restrict__ nent, int64_t *__restrict__ cap_sizes, DevCounters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (k > n_int) return;
+    if (k == n_int) {
+        if (lane == 0) { nsel[k] = 0; nent[k] = 0; }
+        return;
+    }
+    const int64_t node = ilist[k];
+    const int64_t s = nd_cnt[node] - (fscan[im_off[k + 1]] - fscan[im_off[k]]);
+    if (s < 2 || depth >= depth_cap) {
+        if (lane == 0) {
+            nsel[k] = 0;
+            nent[k] = 0;
+            if (s >= 2) {
+                const unsigned long long slot = atomicAdd(&ctr->cap_n, 1ull);
+                cap_sizes[slot] = s;
+            }
+        }
+        return;
+    }
+    const uint64_t seed = nd_seed[node];
+    int count = 0;
+    for (int base = 0; base < t; base += 32) {
+        const int i = base + lane;
+        const bool sel = i < t && stream_uniform(seed, (uint64_t)i) < split_p;
+        const unsigned mask = __ballot_sync(0xffffffffu, sel);
+        if (sel) sel_pos[k * t + count + __popc(mask & ((1u << lane) - 1))] = (int16_t)i;
+        count += __popc(mask);
+    }
+    if (lane == 0) {
+        nsel[k] = count;
+        nent[k] = count * s;
+    }
+}
+
+// one entry per (node, selected position, survivor) in that order; the key
+// (segment << 32 | minhash value) sorts stably into the groups of
+// split_buckets: position ascending, value ascending, members ascending.
+__global__ void k_build_keys(int64_t E, const int64_t *__restrict__ e_off, int64_t n_int,
+                             const int64_t *__restrict__ seg_off, const int64_t *__restrict__ nsel,
+                             const int64_t *__restrict__ im_off, const int64_t *__restrict__ fscan,
+                             const int16_t *__restrict__ sel_pos, int t, const int32_t *__restrict__ surv,
+                             const uint32_t *__restrict__ values, uint64_t *__restrict__ keys,
+                             int32_t *__restrict__ vals) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const int64_t k = upper_bound_i64(e_off, n_int + 1, e) - 1;
+    const int64_t local = e - e_off[k];
+    const int64_t s = (e_off[k + 1] - e_off[k]) / nsel[k];
+    const int64_t r = local / s, p = local - r * s;
+    const int pos = sel_pos[k * t + r];
+    const int32_t x = surv[(im_off[k] - fscan[im_off[k]]) + p];
+    keys[e] = ((uint64_t)(seg_off[k] + r) << 32) | values[(size_t)x * t + pos];
+    vals[e] = x;
+}
+
+__global__ void k_heads(int64_t E, const uint64_t *__restrict__ keys, int64_t *__restrict__ head) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E) head[e] = (e == 0 || keys[e] != keys[e - 1]) ? 1 : 0;
+    else if (e == E) head[e] = 0;
+}
+
+__global__ void k_group_start(int64_t E, const int64_t *__restrict__ head, const int64_t *__restrict__ hscan,
+                              int64_t *__restrict__ gstart) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E && head[e]) gstart[hscan[e]] = e;
+}
+
+// groups of >= 2 members become children (cps:242-244)
+__global__ void k_group_keep(int64_t G, int64_t E, const int64_t *__restrict__ gstart,
+                             int64_t *__restrict__ keep, int64_t *__restrict__ ksize) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < G) {
+        const int64_t sz = (g + 1 < G ? gstart[g + 1] : E) - gstart[g];
+        keep[g] = sz >= 2;
+        ksize[g] = sz >= 2 ? sz : 0;
+    } else if (g == G) {
+        keep[g] = 0;
+        ksize[g] = 0;
+    }
+}
+
+// child node records: seed = word(parent seed, t + 64 ell + j) for the
+// parent's j-th child (cps:286,301); S for the DFS-peak replay
+__global__ void k_children(int64_t G, int64_t E, const int64_t *__restrict__ gstart,
+                           const int64_t *__restrict__ keep, const int64_t *__restrict__ kscan,
+                           const int64_t *__restrict__ mscan, const int64_t *__restrict__ hscan,
+                           const uint64_t *__restrict__ keys, const int64_t *__restrict__ seg_off,
+                           int64_t n_int, const int64_t *__restrict__ e_off,
+                           const int64_t *__restrict__ ilist, const uint64_t *__restrict__ nd_seed,
+                           const int64_t *__restrict__ nd_S, uint64_t child_off,
+                           int64_t *__restrict__ c_off, int32_t *__restrict__ c_cnt,
+                           uint64_t *__restrict__ c_seed, int64_t *__restrict__ c_S, DevCounters *ctr) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    long long cand_peak = 0;
+    if (g < G && keep[g]) {
+        const int64_t st = gstart[g];
+        const int64_t sz = (g + 1 < G ? gstart[g + 1] : E) - st;
+        const int64_t seg = (int64_t)(keys[st] >> 32);
+        const int64_t k = upper_bound_i64(seg_off, n_int + 1, seg) - 1;
+        const int64_t node = ilist[k];
+        const int64_t g0 = hscan[e_off[k]];  // parent's first group
+        const int64_t ci = kscan[g];
+        const int64_t j = ci - kscan[g0];
+        const int64_t S = nd_S[node] + (mscan[g] - mscan[g0]);
+        c_off[ci] = mscan[g];
+        c_cnt[ci] = (int32_t)sz;
+        c_seed[ci] = stream_word(nd_seed[node], child_off + (uint64_t)j);
+        c_S[ci] = S;
+        cand_peak = S + sz;
+    }
+    for (int o = 16; o > 0; o >>= 1) cand_peak = max(cand_peak, __shfl_down_sync(0xffffffffu, cand_peak, o));
+    if ((threadIdx.x & 31) == 0 && cand_peak) atomicMax(&ctr->peak, cand_peak);
+}
+
+__global__ void k_scatter_children(int64_t E, const int64_t *__restrict__ head, const int64_t *__restrict__ hscan,
+                                   const int64_t *__restrict__ gstart, const int64_t *__restrict__ keep,
+                                   const int64_t *__restrict__ mscan, const int32_t *__restrict__ vals,
+                                   int32_t *__restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const int64_t g = hscan[e] + head[e] - 1;
+    if (keep[g]) out[mscan[g] + (e - gstart[g])] = vals[e];
+}
+
+// ------------------------------------------------------------ K5 verify
+
+// one warp per candidate: |x n y| by binary-searching the shorter sorted
+// row's tokens in the longer one; sim = inter / (|x| + |y| - inter) in
+// IEEE f64 (cps:118-122); kept iff sim >= lam.
+__global__ void k_verify(int64_t nc, const int2 *__restrict__ cand, const uint32_t *__restrict__ tokens,
+                         const int64_t *__restrict__ offsets, const int32_t *__restrict__ sizes, double lam,
+                         uint64_t *__restrict__ rkeys, double *__restrict__ rsims, DevCounters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= nc) return;
+    const int2 c = cand[w];
+    int64_t ab = offsets[c.x], ae = offsets[c.x + 1], bb = offsets[c.y], be = offsets[c.y + 1];
+    if (ae - ab > be - bb) { int64_t t0 = ab, t1 = ae; ab = bb; ae = be; bb = t0; be = t1; }
+    int inter = 0;
+    for (int64_t i = ab + lane; i < ae; i += 32) {
+        const uint32_t v = tokens[i];
+        int64_t lo = bb, hi = be;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (tokens[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        inter += (lo < be && tokens[lo] == v);
+    }
+    inter = __reduce_add_sync(0xffffffffu, inter);
+    if (lane == 0) {
+        const long long uni = (long long)sizes[c.x] + sizes[c.y] - inter;
+        const double sim = (double)inter / (double)uni;
+        if (sim >= lam) {
+            const unsigned long long slot = atomicAdd(&ctr->res_n, 1ull);
+            const uint32_t lo = (uint32_t)min(c.x, c.y), hi = (uint32_t)max(c.x, c.y);
+            rkeys[slot] = ((uint64_t)lo << 32) | hi;
+            rsims[slot] = sim;
+        }
+    }
+}
+
+__global__ void k_gather_counts(int64_t ni, const int64_t *__restrict__ il, const int32_t *__restrict__ cnt,
+                                int64_t *__restrict__ out) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < ni) out[k] = cnt[il[k]];
+    else if (k == ni) out[k] = 0;
+}
+
+__global__ void k_fill_roots(int64_t n, int32_t R, int32_t *__restrict__ members) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n * R) members[e] = (int32_t)(e % n);
+}
+
+__global__ void k_gather_scalars(const int64_t *__restrict__ a, int64_t ia, const int64_t *__restrict__ b,
+                                 int64_t ib, const int64_t *__restrict__ c, int64_t ic, int64_t *__restrict__ out) {
+    if (threadIdx.x == 0) {
+        out[0] = a ? a[ia] : 0;
+        out[1] = b ? b[ib] : 0;
+        out[2] = c ? c[ic] : 0;
+    }
+}
+
+// ------------------------------------------------------------ host side
+
+struct Level {
+    int64_t N = 0, M = 0;
+    DevBuf<int64_t> off;
+    DevBuf<int32_t> cnt;
+    DevBuf<uint64_t> seed;
+    DevBuf<int64_t> S;
+    DevBuf<int32_t> members;
+};
+
+struct Driver {
+    cpsj_ctx *ctx;
+    cudaStream_t st;
+    DevBuf<uint8_t> cub_tmp;
+
+    void scan(const int64_t *in, int64_t *out, int64_t n) {
+        size_t bytes = 0;
+        CPSJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, st));
+        if (bytes > cub_tmp.n) cub_tmp.alloc(bytes * 2, st);
+        CPSJ_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp.p, bytes, in, out, n, st));
+        ctx->launches++;
+    }
+
+    // read up to three device scalars with one synchronisation
+    void read3(const int64_t *a, int64_t ia, const int64_t *b, int64_t ib, const int64_t *c, int64_t ic,
+               int64_t *dscal, int64_t out[3]) {
+        k_gather_scalars<<<1, 32, 0, st>>>(a, ia, b, ib, c, ic, dscal);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+        CPSJ_CUDA(cudaMemcpyAsync(ctx->h_scalars, dscal, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        out[0] = ctx->h_scalars[0];
+        out[1] = ctx->h_scalars[1];
+        out[2] = ctx->h_scalars[2];
+    }
+};
+
+template <int ELL>
+void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, int64_t tiles, const int64_t *tile_off, const Level &lv,
+                 const cpsj_inputs *in, int32_t accept, double lam, int2 *cand, unsigned long long cap,
+                 DevCounters *ctr) {
+    const int64_t threads = tiles * 32;
+    k_leaf_tiles<ELL><<<blocks_for(threads), TPB, 0, st>>>(tiles, tile_off, lv.N, lv.off.p, lv.cnt.p, lv.members.p,
+                                                           in->d_sketch, in->ell, in->d_sizes, accept, lam, cand,
+                                                           cap, ctr);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
+void leaf_dispatch(cpsj_ctx *ctx, cudaStream_t st, int64_t tiles, const int64_t *tile_off, const Level &lv,
+                   const cpsj_inputs *in, int32_t accept, double lam, int2 *cand, unsigned long long cap,
+                   DevCounters *ctr) {
+    switch (in->ell) {
+        case 1: launch_leaf<1>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
+        case 2: launch_leaf<2>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
+        case 4: launch_leaf<4>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
+        case 8: launch_leaf<8>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
+        case 16: launch_leaf<16>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
+        default: launch_leaf<0>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
+    }
+}
+
+}  // namespace
+
+void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
+               cudaStream_t st) {
+    require(in && plan && stats, "null argument");
+    require(in->n >= 0 && in->t >= 1 && in->t <= 32767 && in->ell >= 1, "bad input shape");
+    require(plan->n_reps >= 0 && plan->limit >= 1, "bad plan");
+    std::memset(stats, 0, sizeof(*stats));
+    const int64_t launches0 = ctx->launches;
+    const int64_t n = in->n;
+    const int t = in->t, ell = in->ell;
+    const double lam = plan->lambda_;
+    ctx->n_pairs = 0;
+    ctx->cap_events.clear();
+
+    Driver drv{ctx, st};
+    DevBuf<DevCounters> ctr(1, st);
+    DevBuf<int64_t> dscal(4, st);
+    CPSJ_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(DevCounters), st));
+    {
+        DevCounters init{};
+        init.peak = n;
+        CPSJ_CUDA(cudaMemcpyAsync(ctr.p, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+    }
+    // candidate and result buffers grow on demand
+    unsigned long long cand_cap = 1 << 20;
+    DevBuf<int2> cand(cand_cap, st);
+    unsigned long long res_cap = 1 << 16;
+    DevBuf<uint64_t> rkeys(res_cap, st);
+    DevBuf<double> rsims(res_cap, st);
+    DevBuf<int64_t> cap_sizes;  // depth-cap survivor counts, per level
+    int64_t total_cand = 0, max_depth = 0, levels = 0;
+
+    Level lv;
+    const int32_t R = plan->n_reps;
+    if (n >= 2 && R > 0) {
+        lv.N = R;
+        lv.M = n * (int64_t)R;
+        lv.off.alloc(R, st);
+        lv.cnt.alloc(R, st);
+        lv.seed.alloc(R, st);
+        lv.S.alloc(R, st);
+        lv.members.alloc(lv.M, st);
+        std::vector<int64_t> off(R), S(R, 0);
+        std::vector<int32_t> cnt(R, (int32_t)n);
+        for (int r = 0; r < R; ++r) off[r] = (int64_t)r * n;
+        CPSJ_CUDA(cudaMemcpyAsync(lv.off.p, off.data(), R * 8, cudaMemcpyHostToDevice, st));
+        CPSJ_CUDA(cudaMemcpyAsync(lv.cnt.p, cnt.data(), R * 4, cudaMemcpyHostToDevice, st));
+        CPSJ_CUDA(cudaMemcpyAsync(lv.seed.p, plan->h_rep_seeds, R * 8, cudaMemcpyHostToDevice, st));
+        CPSJ_CUDA(cudaMemcpyAsync(lv.S.p, S.data(), R * 8, cudaMemcpyHostToDevice, st));
+        k_fill_roots<<<blocks_for(lv.M), TPB, 0, st>>>(n, R, lv.members.p);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+        CPSJ_CUDA(cudaStreamSynchronize(st));  // host vectors above go out of scope
+    }
+    const uint64_t child_off = (uint64_t)t + 64ull * (uint64_t)ell;
+    unsigned long long res_bound = 0;  // host upper bound of result slots used
+
+    // K5 on the candidates emitted since the last flush; `regen` re-emits
+    // them into a larger buffer if the first pass overflowed
+    auto flush = [&](auto &&regen) {
+        unsigned long long nc = 0;
+        CPSJ_CUDA(cudaMemcpyAsync(&nc, &ctr.p->cand_n, sizeof(nc), cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        if (nc > cand_cap) {
+            cand_cap = nc + nc / 4 + 1024;
+            cand.alloc(cand_cap, st);
+            CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cand_n, 0, sizeof(unsigned long long), st));
+            regen();
+        }
+        if (nc > 0) {
+            if (res_bound + nc > res_cap) {
+                const unsigned long long want = std::max(res_bound + nc, 2 * res_cap);
+                rkeys.grow(want, res_cap, st);
+                rsims.grow(want, res_cap, st);
+                res_cap = want;
+            }
+            k_verify<<<blocks_for((int64_t)nc * 32), TPB, 0, st>>>((int64_t)nc, cand.p, in->d_tokens,
+                                                                   in->d_offsets, in->d_sizes, lam, rkeys.p,
+                                                                   rsims.p, ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            total_cand += (int64_t)nc;
+            res_bound += nc;
+        }
+        CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cand_n, 0, sizeof(unsigned long long), st));
+    };
+
+    for (int depth = 0; lv.N > 0; ++depth) {
+        levels++;
+        max_depth = depth;
+        const int64_t N = lv.N;
+        // ---- plan: leaves vs internal nodes
+        DevBuf<int64_t> tiles(N + 1, st), internal(N + 1, st), imem(N + 1, st);
+        DevBuf<int64_t> tile_off(N + 1, st), iscan(N + 1, st), im_off(N + 1, st);
+        k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, internal.p, imem.p, ctr.p);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+        drv.scan(tiles.p, tile_off.p, N + 1);
+        drv.scan(internal.p, iscan.p, N + 1);
+        drv.scan(imem.p, im_off.p, N + 1);
+        int64_t sc[3];
+        drv.read3(tile_off.p, N, iscan.p, N, im_off.p, N, dscal.p, sc);
+        const int64_t total_tiles = sc[0], n_int = sc[1], Mi = sc[2];
+        CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cand_n, 0, sizeof(unsigned long long), st));
+
+        // ---- leaves: K4, then K5 on their candidates
+        if (total_tiles > 0) {
+            auto gen = [&]() {
+                leaf_dispatch(ctx, st, total_tiles, tile_off.p, lv, in, plan->accept_dist, lam, cand.p, cand_cap,
+                              ctr.p);
+            };
+            gen();
+            flush(gen);
+        }
+
+        // ---- internal nodes: K2 (+ point comparisons), K3
+        Level nx;
+        if (n_int > 0) {
+            DevBuf<int64_t> ilist(n_int, st), im_off_c(n_int + 1, st);
+            k_compact_internal<<<blocks_for(N), TPB, 0, st>>>(N, internal.p, iscan.p, ilist.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            // member offsets of the internal nodes, compacted
+            {
+                DevBuf<int64_t> icnt(n_int + 1, st);
+                k_gather_counts<<<blocks_for(n_int + 1), TPB, 0, st>>>(n_int, ilist.p, lv.cnt.p, icnt.p);
+                CPSJ_LAUNCH_CHECK();
+                ctx->launches++;
+                drv.scan(icnt.p, im_off_c.p, n_int + 1);
+            }
+            DevBuf<uint64_t> nsk(n_int * ell, st);
+            k_node_sketch<<<(unsigned)n_int, TPB, 0, st>>>(ilist.p, lv.off.p, lv.cnt.p, lv.seed.p, lv.members.p,
+                                                           in->d_sketch, ell, t,
+                                                           reinterpret_cast<uint32_t *>(nsk.p), ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            DevBuf<int64_t> flags(Mi + 1, st), fscan(Mi + 1, st);
+            k_flags<<<blocks_for(Mi + 1), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p, lv.members.p,
+                                                        in->d_sketch, ell, nsk.p, plan->flag_dist, flags.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            drv.scan(flags.p, fscan.p, Mi + 1);
+            drv.read3(fscan.p, Mi, nullptr, 0, nullptr, 0, dscal.p, sc);
+            const int64_t n_flag = sc[0];
+            if (n_flag > 0) {
+                DevBuf<int64_t> flist(n_flag, st);
+                k_flag_list<<<blocks_for(Mi), TPB, 0, st>>>(Mi, flags.p, fscan.p, flist.p);
+                CPSJ_LAUNCH_CHECK();
+                ctx->launches++;
+                int count_pre = 1;
+                auto gen = [&]() {
+                    k_point<<<blocks_for(n_flag * 32), TPB, 0, st>>>(
+                        n_flag, flist.p, fscan.p, flags.p, im_off_c.p, n_int, ilist.p, lv.off.p, lv.cnt.p,
+                        lv.members.p, in->d_sketch, ell, in->d_sizes, plan->accept_dist, lam, cand.p, cand_cap,
+                        count_pre, ctr.p);
+                    CPSJ_LAUNCH_CHECK();
+                    ctx->launches++;
+                    count_pre = 0;  // a regeneration must not count twice
+                };
+                gen();
+                flush(gen);
+            }
+            DevBuf<int32_t> surv(std::max<int64_t>(1, Mi - n_flag), st);
+            k_survivors<<<blocks_for(Mi), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p, lv.members.p,
+                                                        flags.p, fscan.p, surv.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            // ---- split
+            DevBuf<int16_t> sel_pos(n_int * t, st);
+            DevBuf<int64_t> nsel(n_int + 1, st), nent(n_int + 1, st), seg_off(n_int + 1, st), e_off(n_int + 1, st);
+            DevBuf<int64_t> capsz(n_int, st);
+            CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cap_n, 0, sizeof(unsigned long long), st));
+            k_select<<<blocks_for((n_int + 1) * 32), TPB, 0, st>>>(
+                n_int, ilist.p, lv.cnt.p, lv.seed.p, depth, plan->depth_cap, im_off_c.p, fscan.p, t, plan->split_p,
+                sel_pos.p, nsel.p, nent.p, capsz.p, ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            drv.scan(nsel.p, seg_off.p, n_int + 1);
+            drv.scan(nent.p, e_off.p, n_int + 1);
+            drv.read3(e_off.p, n_int, seg_off.p, n_int, nullptr, 0, dscal.p, sc);
+            const int64_t E = sc[0], n_seg = sc[1];
+            {
+                unsigned long long ncap = 0;
+                CPSJ_CUDA(cudaMemcpyAsync(&ncap, &ctr.p->cap_n, sizeof(ncap), cudaMemcpyDeviceToHost, st));
+                CPSJ_CUDA(cudaStreamSynchronize(st));
+                if (ncap) {
+                    std::vector<int64_t> h(ncap);
+                    CPSJ_CUDA(cudaMemcpyAsync(h.data(), capsz.p, ncap * 8, cudaMemcpyDeviceToHost, st));
+                    CPSJ_CUDA(cudaStreamSynchronize(st));
+                    ctx->cap_events.insert(ctx->cap_events.end(), h.begin(), h.end());
+                }
+            }
+            if (E > 0) {
+                DevBuf<uint64_t> keys(E, st), keys2(E, st);
+                DevBuf<int32_t> vals(E, st), vals2(E, st);
+                k_build_keys<<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p, im_off_c.p,
+                                                            fscan.p, sel_pos.p, t, surv.p, in->d_values, keys.p,
+                                                            vals.p);
+                CPSJ_LAUNCH_CHECK();
+                ctx->launches++;
+                int end_bit = 32;
+                while (end_bit < 64 && ((uint64_t)n_seg >> (end_bit - 32)) > 0) ++end_bit;
+                size_t bytes = 0;
+                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0,
+                                                          end_bit, st));
+                if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
+                                                          0, end_bit, st));
+                ctx->launches++;
+                DevBuf<int64_t> head(E + 1, st), hscan(E + 1, st);
+                k_heads<<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
+                CPSJ_LAUNCH_CHECK();
+                ctx->launches++;
+                drv.scan(head.p, hscan.p, E + 1);
+                drv.read3(hscan.p, E, nullptr, 0, nullptr, 0, dscal.p, sc);
+                const int64_t G = sc[0];
+                DevBuf<int64_t> gstart(G, st), keep(G + 1, st), ksize(G + 1, st), kscan(G + 1, st),
+                    mscan(G + 1, st);
+                k_group_start<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p);
+                CPSJ_LAUNCH_CHECK();
+                k_group_keep<<<blocks_for(G + 1), TPB, 0, st>>>(G, E, gstart.p, keep.p, ksize.p);
+                CPSJ_LAUNCH_CHECK();
+                ctx->launches += 2;
+                drv.scan(keep.p, kscan.p, G + 1);
+                drv.scan(ksize.p, mscan.p, G + 1);
+                drv.read3(kscan.p, G, mscan.p, G, nullptr, 0, dscal.p, sc);
+                nx.N = sc[0];
+                nx.M = sc[1];
+                if (nx.N > 0) {
+                    nx.off.alloc(nx.N, st);
+                    nx.cnt.alloc(nx.N, st);
+                    nx.seed.alloc(nx.N, st);
+                    nx.S.alloc(nx.N, st);
+                    nx.members.alloc(nx.M, st);
+                    k_children<<<blocks_for(G), TPB, 0, st>>>(G, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p,
+                                                              keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p,
+                                                              lv.S.p, child_off, nx.off.p, nx.cnt.p, nx.seed.p,
+                                                              nx.S.p, ctr.p);
+                    CPSJ_LAUNCH_CHECK();
+                    k_scatter_children<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p, keep.p,
+                                                                      mscan.p, vals2.p, nx.members.p);
+                    CPSJ_LAUNCH_CHECK();
+                    ctx->launches += 2;
+                }
+            }
+        }
+
+        lv = std::move(nx);
+    }
+
+    // ---- K6: sort + unique of the verified pairs
+    DevCounters hc{};
+    CPSJ_CUDA(cudaMemcpyAsync(&hc, ctr.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    CPSJ_CUDA(cudaStreamSynchronize(st));
+    const int64_t nres = (int64_t)hc.res_n;
+    ctx->res_keys.release();
+    ctx->res_sims.release();
+    if (nres > 0) {
+        DevBuf<uint64_t> k2(nres, st);
+        DevBuf<double> s2(nres, st);
+        size_t bytes = 0;
+        CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64, st));
+        if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+        CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64, st));
+        ctx->launches++;
+        ctx->res_keys.alloc(nres, st);
+        ctx->res_sims.alloc(nres, st);
+        DevBuf<int64_t> nsel(1, st);
+        bytes = 0;
+        CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(nullptr, bytes, k2.p, s2.p, ctx->res_keys.p, ctx->res_sims.p, nsel.p,
+                                                 nres, st));
+        if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+        CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(drv.cub_tmp.p, bytes, k2.p, s2.p, ctx->res_keys.p, ctx->res_sims.p,
+                                                 nsel.p, nres, st));
+        ctx->launches++;
+        int64_t u = 0;
+        CPSJ_CUDA(cudaMemcpyAsync(&u, nsel.p, 8, cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        ctx->n_pairs = u;
+    }
+    if (hc.err) throw Error{CPSJ_E_PICK, "node-sketch pick index out of range (uniform draw == 1.0)"};
+    stats->n_pairs = ctx->n_pairs;
+    stats->pre_candidates = (int64_t)hc.pre;
+    stats->candidates = total_cand;
+    stats->results = nres;
+    stats->max_depth = max_depth;
+    stats->peak_live_members = (n >= 2 && R > 0) ? hc.peak : 0;
+    stats->n_depth_cap_events = (int64_t)ctx->cap_events.size();
+    stats->n_levels = levels;
+    stats->gpu_launches = ctx->launches - launches0;
+}
+
+}  // namespace cpsj

@@ -1,0 +1,255 @@
+"""MinHash embedding of records (drop-in for the reference's simjoin.embed).
+
+``embed_dataset`` runs K1 (csrc/minhash.cu) over the CSR of the dataset and
+keeps the (n, t) value matrix resident on the GPU; ``EmbeddedDataset``
+exposes the reference's attributes (values, dense, d, t, seed, verify_csr,
+sizes, source_ids, side, origin) and the cached ``sketches(ell, seed)``,
+materialising host copies only when they are read.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .core import Dataset, Record
+from .hashing import KIND_EMBED, derive_rng, minhash_segments_many, sketch_family
+
+DEFAULT_T = 128
+
+
+class EmbeddingParams:
+    """t independent MinHash functions drawn from a master seed
+    (reference embed.py:36-48)."""
+
+    def __init__(self, t: int = DEFAULT_T, seed: int = 0):
+        if t < 1:
+            raise ValueError("embedding size t must be at least 1")
+        self.t = t
+        self.seed = seed
+        self.tables = derive_rng(seed, KIND_EMBED).integers(0, 2 ** 64, size=(t, 4, 256), dtype=np.uint64)
+        self._device = {}
+
+    def device(self, ctx):
+        fam = self._device.get(ctx.device)
+        if fam is None:
+            from ._native import Family
+            fam = self._device[ctx.device] = Family(ctx, self.tables)
+        return fam
+
+
+def _first_seen_dense(keys: np.ndarray) -> tuple[np.ndarray, int]:
+    """Remap keys to 0..k-1 in order of first appearance (host)."""
+    uniq, first, inverse = np.unique(keys, return_index=True, return_inverse=True)
+    order = np.empty(len(uniq), dtype=np.int64)
+    order[np.argsort(first, kind="stable")] = np.arange(len(uniq))
+    return order[inverse], len(uniq)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class EmbeddedDataset:
+    """Records embedded to t MinHash values each, plus verification data
+    (reference embed.py:51-98).  Device copies are made lazily and dropped
+    whenever a host attribute is reassigned."""
+
+    def __init__(self, values, dense, d, t: int, seed: int, verify_csr, sizes, source_ids,
+                 side=None, origin: Dataset | None = None):
+        self._values = None if values is None else np.asarray(values, dtype=np.uint32)
+        self._dense = None if dense is None else np.asarray(dense)
+        self._d = d
+        self.t = t
+        self.seed = seed
+        self._csr = verify_csr
+        self._csr_arrays = None
+        self._sizes = None if sizes is None else np.asarray(sizes, dtype=np.int64)
+        self.source_ids = source_ids
+        self.side = side
+        self.origin = origin
+        self._n = None
+        self._sketch_cache: dict = {}
+        self._dev_sketch: dict = {}
+        self._dev: dict = {}
+
+    # ------------------------------------------------------------- internal
+    @classmethod
+    def _device_backed(cls, dev_values, t, seed, tokens, offsets, d_universe, origin, dev_csr):
+        obj = cls(None, None, None, t, seed, None, np.diff(offsets), np.arange(len(offsets) - 1, dtype=np.int64),
+                  origin=origin)
+        obj._csr_arrays = (tokens, offsets, d_universe)
+        obj._dev["values"] = dev_values
+        obj._dev["tokens"], obj._dev["offsets"] = dev_csr
+        obj._n = len(offsets) - 1
+        return obj
+
+    def _csr_host(self):
+        if self._csr_arrays is None:
+            m = self._csr
+            self._csr_arrays = (np.asarray(m.indices).astype(np.uint32, copy=False),
+                                np.asarray(m.indptr).astype(np.int64, copy=False), int(m.shape[1]))
+        return self._csr_arrays
+
+    def device_inputs(self, ctx):
+        """Device tensors the join reads: tokens, offsets, sizes (i32), values."""
+        torch = _torch()
+        dev = torch.device("cuda", ctx.device)
+        if "tokens" not in self._dev:
+            tok, off, _ = self._csr_host()
+            self._dev["tokens"] = torch.from_numpy(np.ascontiguousarray(tok).view(np.int32)).to(dev, non_blocking=True)
+            self._dev["offsets"] = torch.from_numpy(np.ascontiguousarray(off)).to(dev, non_blocking=True)
+        if "sizes" not in self._dev:
+            self._dev["sizes"] = torch.from_numpy(self.sizes.astype(np.int32)).to(dev, non_blocking=True)
+        if "values" not in self._dev:
+            v = np.ascontiguousarray(self.values, dtype=np.uint32)
+            self._dev["values"] = torch.from_numpy(v.view(np.int32)).to(dev, non_blocking=True)
+        return self._dev["tokens"], self._dev["offsets"], self._dev["sizes"], self._dev["values"]
+
+    # ------------------------------------------------------------ reference
+    def __len__(self) -> int:
+        if self._n is None:
+            self._n = len(self._values) if self._values is not None else len(self._csr_host()[1]) - 1
+        return self._n
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values is None:
+            self._values = self._dev["values"].cpu().numpy().view(np.uint32)
+        return self._values
+
+    @values.setter
+    def values(self, v):
+        self._values = np.asarray(v, dtype=np.uint32)
+        self._dev.pop("values", None)
+        self._dense = None
+        self._d = None
+        self._n = len(self._values)
+
+    @property
+    def dense(self) -> np.ndarray:
+        if self._dense is None:
+            self._compute_dense()
+        return self._dense
+
+    @dense.setter
+    def dense(self, v):
+        self._dense = v
+
+    @property
+    def d(self) -> int:
+        if self._d is None:
+            self._compute_dense()
+        return self._d
+
+    @d.setter
+    def d(self, v):
+        self._d = v
+
+    def _compute_dense(self):
+        vals = self.values
+        n, t = vals.shape
+        if n == 0:
+            self._dense, self._d = np.zeros((0, t), dtype=np.uint32), 0
+            return
+        keys = (np.arange(t, dtype=np.uint64)[None, :] << np.uint64(32)) | vals.astype(np.uint64)
+        flat, d = _first_seen_dense(keys.ravel())
+        self._dense, self._d = flat.reshape(n, t).astype(np.uint32), d
+
+    @property
+    def verify_csr(self):
+        if self._csr is None:
+            from scipy.sparse import csr_matrix
+            tok, off, width = self._csr_arrays
+            self._csr = csr_matrix((np.ones(len(tok), dtype=np.int32), tok.astype(np.int32), off),
+                                   shape=(len(off) - 1, width))
+        return self._csr
+
+    @verify_csr.setter
+    def verify_csr(self, m):
+        self._csr = m
+        self._csr_arrays = None
+        self._dev.pop("tokens", None)
+        self._dev.pop("offsets", None)
+
+    @property
+    def sizes(self) -> np.ndarray:
+        return self._sizes
+
+    @sizes.setter
+    def sizes(self, v):
+        self._sizes = np.asarray(v, dtype=np.int64)
+        self._dev.pop("sizes", None)
+
+    def embedded_record(self, row: int) -> np.ndarray:
+        return np.sort(self.dense[row])
+
+    def original_record(self, row: int) -> Record:
+        tok, off, _ = self._csr_host()
+        return Record(int(self.source_ids[row]), tok[off[row]:off[row + 1]].astype(np.uint32))
+
+    def sketches_device(self, ell: int, seed: int):
+        """(n, ell) sketch matrix as a device tensor (int64 view of u64),
+        computed once per (ell, seed) by K1 (hashing.py:197-211)."""
+        key = (ell, seed)
+        if key not in self._dev_sketch:
+            torch = _torch()
+            from ._native import Context
+            ctx = Context.get()
+            n = len(self)
+            dev = torch.device("cuda", ctx.device)
+            out = torch.zeros((n, ell), dtype=torch.int64, device=dev)
+            if n > 0:
+                tok, off, sizes, _ = self.device_inputs(ctx)
+                fam = sketch_family(ell, seed).device(ctx)
+                _, _, width = self._csr_host()
+                stream = torch.cuda.current_stream(dev).cuda_stream
+                ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, fam.handle, tok.data_ptr(), off.data_ptr(), n,
+                                                      max(0, min(int(width) - 1, 0xFFFFFFFF)) if width else
+                                                      0xFFFFFFFF, None, out.data_ptr(), stream))
+            self._dev_sketch[key] = out
+        return self._dev_sketch[key]
+
+    def sketches(self, ell: int, seed: int) -> np.ndarray:
+        """(n, ell) sketch matrix of the original records, cached per family."""
+        key = (ell, seed)
+        if key not in self._sketch_cache:
+            self._sketch_cache[key] = self.sketches_device(ell, seed).cpu().numpy().view(np.uint64)
+        return self._sketch_cache[key]
+
+
+def embed_record(params: EmbeddingParams, x: Record) -> list[tuple[int, int]]:
+    if len(x) == 0:
+        raise ValueError("cannot embed an empty record")
+    tok = np.asarray(x.tokens, dtype=np.uint32)
+    vals = minhash_segments_many(params.tables, tok, np.array([0, len(tok)], dtype=np.int64))[0]
+    return [(i, int(v)) for i, v in enumerate(vals)]
+
+
+def embed_dataset(params: EmbeddingParams, ds: Dataset) -> EmbeddedDataset:
+    """Embed every record with the shared function family (embed.py:117-139)
+    on the GPU; the value matrix stays device-resident."""
+    n = len(ds)
+    t = params.t
+    tok, off = ds.flat_tokens()
+    tok = np.ascontiguousarray(tok, dtype=np.uint32)
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    if n == 0:
+        return EmbeddedDataset(np.zeros((0, t), dtype=np.uint32), np.zeros((0, t), dtype=np.uint32), 0, t,
+                               params.seed, verify_csr=ds.csr(), sizes=np.zeros(0, dtype=np.int64),
+                               source_ids=np.arange(0, dtype=np.int64), origin=ds)
+    if np.any(off[1:] == off[:-1]):
+        raise ValueError("cannot embed an empty record")
+    torch = _torch()
+    from ._native import Context
+    ctx = Context.get()
+    fam = params.device(ctx)
+    dev = torch.device("cuda", ctx.device)
+    d_tok = torch.from_numpy(tok.view(np.int32)).to(dev, non_blocking=True)
+    d_off = torch.from_numpy(off).to(dev, non_blocking=True)
+    d_vals = torch.empty((n, t), dtype=torch.int32, device=dev)
+    width = int(getattr(ds, "d", 0) or 0)
+    max_token = min(width - 1, 0xFFFFFFFF) if width > 0 else 0xFFFFFFFF
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, fam.handle, d_tok.data_ptr(), d_off.data_ptr(), n,
+                                          max_token, d_vals.data_ptr(), None, stream))
+    return EmbeddedDataset._device_backed(d_vals, t, params.seed, tok, off, width, ds, (d_tok, d_off))

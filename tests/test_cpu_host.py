@@ -1,0 +1,135 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol the
+header declares; host-side plan derivation; data model and workloads."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "cpsjoin_b200.h")
+
+
+def header_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"CPSJ_API\s+[\w\s\*]*?\b(cpsj_\w+)\s*\(", src)))
+
+
+def test_library_builds_and_exports_header_symbols():
+    from paper_1707_06814_b200 import _native
+    from paper_1707_06814_b200.build import SO, build
+    build()
+    out = subprocess.run(["nm", "-D", "--defined-only", SO], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (cpsj_\w+)", out))
+    declared = header_symbols()
+    assert declared, "no declarations parsed"
+    assert set(declared) == exported
+    assert set(declared) == set(_native.EXPORTS)
+    lib = _native.load()
+    for name in declared:
+        assert hasattr(lib, name)
+    assert lib.cpsj_version() >= (1 << 16)
+
+
+def test_library_is_sm100a():
+    from paper_1707_06814_b200.build import SO, build
+    build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", SO], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cuda_means_loud_failure(monkeypatch):
+    import torch
+
+    from paper_1707_06814_b200 import _native
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        _native.Context.get()
+
+
+def reference_flag(dist, mbits, lam, eps):
+    # cpsjoin.py:206 and :268 with dist as numpy's uint64 popcount sum
+    est = 2.0 * (mbits - np.uint64(dist)) / mbits - 1.0
+    return bool(est > (1.0 - eps) * lam)
+
+
+@pytest.mark.parametrize("ell", [1, 8, 16])
+@pytest.mark.parametrize("lam", [0.3, 0.5, 0.6, 0.7, 0.8, 0.9, 0.99])
+@pytest.mark.parametrize("eps", [0.0, 0.1, 0.3])
+def test_flag_distance_is_the_numpy_rule(ell, lam, eps):
+    from paper_1707_06814_b200.cpsjoin import flag_distance
+    mbits = 64 * ell
+    d = flag_distance(lam, eps, mbits)
+    for dist in range(mbits + 1):
+        assert reference_flag(dist, mbits, lam, eps) == (dist <= d)
+
+
+def test_survey_threshold_tables():
+    from paper_1707_06814_b200.cpsjoin import CPSJoinParams, make_plan
+    acc = {0.5: 144, 0.6: 117, 0.7: 90, 0.8: 63, 0.9: 34}
+    flag = {0.5: 140, 0.6: 117, 0.7: 94, 0.8: 71, 0.9: 48}
+    for lam in acc:
+        p = make_plan(CPSJoinParams(lambda_=lam), 128)
+        assert p.accept_dist == acc[lam] and p.flag_dist == flag[lam]
+        assert p.split_p == 1.0 / (lam * 128)
+    acc16 = {0.5: 279, 0.6: 226, 0.7: 173, 0.8: 118, 0.9: 63}
+    for lam in acc16:
+        assert make_plan(CPSJoinParams(lambda_=lam, ell=16), 128).accept_dist == acc16[lam]
+
+
+def test_rep_seeds_prefix_stable():
+    from paper_1707_06814_b200.cpsjoin import CPSJoinParams, make_plan
+    a = make_plan(CPSJoinParams(lambda_=0.5, repetitions=3, seed=7), 128).rep_seeds
+    b = make_plan(CPSJoinParams(lambda_=0.5, repetitions=10, seed=7), 128).rep_seeds
+    assert np.array_equal(a, b[:3])
+
+
+def test_params_validation():
+    from paper_1707_06814_b200 import CPSJoinParams
+    for kw in [dict(lambda_=1.5), dict(lambda_=0.5, epsilon=1.0), dict(lambda_=0.5, limit=0),
+               dict(lambda_=0.5, delta=0.0), dict(lambda_=0.5, repetitions=0), dict(lambda_=0.5, ell=0)]:
+        with pytest.raises(ValueError):
+            CPSJoinParams(**kw)
+
+
+def test_hash_stream_matches_oracle():
+    from oracle import oracle as O
+    from paper_1707_06814_b200.hashing import mix64, uniform_stream, word_stream
+    assert int(mix64(0)) == O.mix64(0)
+    assert np.array_equal(word_stream(123, 500, offset=17), O.word_stream(123, 500, 17))
+    u = uniform_stream(9, 1000)
+    assert np.all((u >= 0) & (u <= 1))
+
+
+def test_dataset_cleaning_semantics():
+    from paper_1707_06814_b200 import Dataset
+    ds = Dataset.from_token_lists([[5, 3, 3], [7], [3, 5], [9, 8, 1], [100, 200]])
+    # [7] dropped (< 2 tokens), second [3, 5] dropped (duplicate), dense remap
+    assert len(ds) == 3
+    assert [r.tokens.tolist() for r in ds.records] == [[1, 2], [0, 3, 4], [5, 6]]
+    assert ds.d == 7
+    assert ds.sizes.tolist() == [2, 3, 2]
+    ds2 = Dataset.from_token_lists([[5, 3], [9, 8, 1]], d=10)
+    assert ds2.records[1].tokens.tolist() == [1, 8, 9]
+    assert ds2.csr().shape == (2, 10)
+    assert ds2.token_frequency[8] == 1
+
+
+def test_workload_generator_deterministic_and_planted_exact():
+    from paper_1707_06814_b200.workloads import CONFIGS, generate
+    a = generate(1, scale=0.02)
+    b = generate(1, scale=0.02)
+    assert np.array_equal(a.tokens, b.tokens) and np.array_equal(a.offsets, b.offsets)
+    lo, hi = CONFIGS[1].j_range
+    for s, p in a.planted_pairs[:50]:
+        x = set(a.tokens[a.offsets[s]:a.offsets[s + 1]].tolist())
+        y = set(a.tokens[a.offsets[p]:a.offsets[p + 1]].tolist())
+        assert len(x) == len(y)
+        j = len(x & y) / len(x | y)
+        assert 0.3 < j < 1.0
+    for i in range(a.n):
+        row = a.tokens[a.offsets[i]:a.offsets[i + 1]]
+        assert np.all(np.diff(row.astype(np.int64)) > 0)
+        assert row.max() < a.d

@@ -1,0 +1,266 @@
+"""Bit-exact parity of the sm_100a path against golden vectors made by the
+reference itself (tests/golden, oracle/gen_golden.py) and against the C
+oracle on seeded inputs.  Every call goes through the C ABI."""
+import hashlib
+import logging
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1707_06814_b200 import _native
+    _native.load()
+
+
+def _params(z, k):
+    from paper_1707_06814_b200 import CPSJoinParams
+    lam, ell, seed, reps, limit, eps, delta, cap = z[f"j{k}_params"].tolist()
+    return CPSJoinParams(lambda_=lam, ell=int(ell), seed=int(seed), repetitions=int(reps), limit=int(limit),
+                         epsilon=eps, delta=delta, depth_cap=int(cap))
+
+
+def _check_join(res, z, k):
+    assert np.array_equal(res.a, z[f"j{k}_pair_a"])
+    assert np.array_equal(res.b, z[f"j{k}_pair_b"])
+    assert np.array_equal(res.similarity, z[f"j{k}_pair_sim"])  # bit-exact f64
+    c = res.counters
+    assert [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members] == \
+        z[f"j{k}_counters"].tolist()
+    assert len(res.depth_cap_sizes) == int(z[f"j{k}_n_depth_cap_warnings"])
+
+
+def test_minhash_kat_tables():
+    from paper_1707_06814_b200.hashing import minhash_segments_many
+    z = load("kat_minhash")
+    got = minhash_segments_many(z["tables"], z["tokens"], z["offsets"])
+    assert np.array_equal(got, z["minhash"])
+
+
+def test_sketch_kat():
+    from paper_1707_06814_b200.hashing import SketchFamily, build_sketch_matrix
+    z = load("kat_minhash")
+    fam = SketchFamily(int(z["sketch_ell"]), int(z["sketch_seed"]))
+    assert np.array_equal(build_sketch_matrix(fam, z["tokens"], z["offsets"]), z["sketch"])
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 4])
+def test_minhash_every_key_width_matches_oracle(L):
+    from oracle import oracle as O
+    from paper_1707_06814_b200.hashing import minhash_segments_many
+    rng = np.random.default_rng(L)
+    hi = (1 << (8 * L)) - 1
+    rows = [np.unique(rng.integers(0, hi + 1, size=int(rng.integers(1, 300)), dtype=np.uint64)) for _ in range(400)]
+    tok = np.concatenate(rows).astype(np.uint32)
+    off = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    tables = O.derive_rng(5, L).integers(0, 2 ** 64, size=(70, 4, 256), dtype=np.uint64)
+    got = minhash_segments_many(tables, tok, off, d=hi + 1)
+    assert np.array_equal(got, O.minhash(tok, off, tables))
+
+
+def test_minhash_high_word_ties_resolved_on_full_hash():
+    # tables whose high 32 bits are constant: every token ties on the
+    # compared word, the lane must fall back to the full 64-bit hash
+    from oracle import oracle as O
+    from paper_1707_06814_b200.hashing import minhash_segments_many
+    rng = np.random.default_rng(3)
+    rows = [np.unique(rng.integers(0, 5000, size=50)) for _ in range(200)]
+    tok = np.concatenate(rows).astype(np.uint32)
+    off = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    tables = O.derive_rng(8).integers(0, 2 ** 64, size=(40, 4, 256), dtype=np.uint64)
+    tables[:20] &= np.uint64(0xFFFFFFFF)
+    tables[20:30] = 0  # full ties: smallest token wins
+    got = minhash_segments_many(tables, tok, off, d=5000)
+    assert np.array_equal(got, O.minhash(tok, off, tables))
+
+
+EMB_FIXTURES = ["planted_small", "planted_880", "dense_cluster", "c1_sample", "c3_sample", "c4_sample"]
+
+
+@pytest.mark.parametrize("name", EMB_FIXTURES)
+def test_join_matches_reference_golden(name):
+    from paper_1707_06814_b200 import Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    z = load(name)
+    ds = Dataset.from_csr(z["tokens"], z["offsets"], int(z["d"]))
+    emb = embed_dataset(EmbeddingParams(t=int(z["t"]), seed=int(z["emb_seed"])), ds)
+    assert sha(emb.values) == str(z["values_sha"])
+    for k in range(int(z["n_joins"])):
+        p = _params(z, k)
+        assert sha(emb.sketches(p.ell, p.seed)) == str(z[f"j{k}_sketch_sha"])
+        _check_join(cpsjoin_self_arrays(emb, p), z, k)
+
+
+def _synthetic_emb(z):
+    from scipy.sparse import csr_matrix
+
+    from paper_1707_06814_b200 import EmbeddedDataset
+    n = len(z["offsets"]) - 1
+    csr = csr_matrix((np.ones(len(z["tokens"]), np.int32), z["tokens"].astype(np.int32), z["offsets"]),
+                     shape=(n, int(z["d"])))
+    return EmbeddedDataset(z["values"], None, None, z["values"].shape[1], 0, verify_csr=csr, sizes=z["sizes"],
+                           source_ids=np.arange(n, dtype=np.int64))
+
+
+@pytest.mark.parametrize("name", ["depth_cap", "synthetic_flags"])
+def test_join_synthetic_matches_reference_golden(name, caplog):
+    from paper_1707_06814_b200 import cpsjoin_self_arrays
+    z = load(name)
+    emb = _synthetic_emb(z)
+    for k in range(int(z["n_joins"])):
+        p = _params(z, k)
+        assert np.array_equal(emb.sketches(p.ell, p.seed), z[f"j{k}_sketch"])
+        with caplog.at_level(logging.WARNING, logger="simjoin.cpsjoin"):
+            caplog.clear()
+            res = cpsjoin_self_arrays(emb, p)
+        _check_join(res, z, k)
+        n_cap = sum("depth cap" in r.getMessage() for r in caplog.records)
+        assert n_cap == int(z[f"j{k}_n_depth_cap_warnings"])
+
+
+@pytest.mark.parametrize("cfg,scale,lam,ell,reps", [(1, 1.0, 0.5, 8, 3), (3, 0.01, 0.7, 8, 4),
+                                                    (4, 0.004, 0.6, 16, 2), (5, 0.002, 0.6, 8, 3),
+                                                    (2, 0.01, 0.5, 8, 2)])
+def test_join_matches_oracle_on_workloads(cfg, scale, lam, ell, reps):
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    from paper_1707_06814_b200.workloads import generate
+    w = generate(cfg, scale=scale)
+    ds = Dataset.from_csr(w.tokens, w.offsets, w.d)
+    emb = embed_dataset(EmbeddingParams(t=128, seed=7), ds)
+    p = CPSJoinParams(lambda_=lam, ell=ell, seed=7, repetitions=reps)
+    res = cpsjoin_self_arrays(emb, p)
+    values, sk, ref = O.full_pipeline(w.tokens, w.offsets, w.sizes, lam=lam, emb_seed=7, ell=ell, seed=7,
+                                      repetitions=reps)
+    assert np.array_equal(emb.values, values)
+    assert np.array_equal(emb.sketches(ell, 7), sk)
+    assert np.array_equal(res.a, ref.a) and np.array_equal(res.b, ref.b)
+    assert np.array_equal(res.similarity, ref.sims)
+    c = res.counters
+    assert [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members] == \
+        [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members]
+
+
+def test_small_limit_deep_tree_matches_oracle():
+    # limit=8 forces many internal nodes and deep frontiers
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    from paper_1707_06814_b200.workloads import generate
+    w = generate(1, scale=0.1)
+    ds = Dataset.from_csr(w.tokens, w.offsets, w.d)
+    emb = embed_dataset(EmbeddingParams(t=64, seed=1), ds)
+    p = CPSJoinParams(lambda_=0.5, seed=2, repetitions=4, limit=8, epsilon=0.3)
+    res = cpsjoin_self_arrays(emb, p)
+    ref = O.self_join(w.tokens, w.offsets, w.sizes, emb.values, emb.sketches(8, 2), 0.5, epsilon=0.3, limit=8,
+                      repetitions=4, seed=2)
+    assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)
+    c = res.counters
+    assert [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members] == \
+        [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members]
+
+
+# ---- reference test strategy through the drop-in (tests/test_cpsjoin.py shapes)
+
+def _planted(n_background, n_planted, seed):
+    from paper_1707_06814_b200 import Dataset
+    rng = np.random.default_rng(seed)
+    size, overlap, lists = 17, 14, []
+    for k in range(n_planted):
+        lo = 10_000 + k * (2 * size - overlap)
+        common = list(range(lo, lo + overlap))
+        lists.append(common + list(range(lo + overlap, lo + size)))
+        lists.append(common + list(range(lo + size, lo + 2 * size - overlap)))
+    for _ in range(n_background):
+        lists.append(rng.choice(5000, size=size, replace=False))
+    return Dataset.from_token_lists(lists)
+
+
+def _naive(ds, lam):
+    recs = [set(r.tokens.tolist()) for r in ds.records]
+    out = set()
+    for i in range(len(recs)):
+        for j in range(i + 1, len(recs)):
+            inter = len(recs[i] & recs[j])
+            if inter / (len(recs[i]) + len(recs[j]) - inter) >= lam:
+                out.add((i, j))
+    return out
+
+
+def test_small_dataset_equals_naive():
+    from paper_1707_06814_b200 import CPSJoinParams, EmbeddingParams, cpsjoin_self, embed_dataset
+    ds = _planted(60, 12, 31)
+    pairs, c = cpsjoin_self(embed_dataset(EmbeddingParams(seed=3), ds), CPSJoinParams(lambda_=0.5, seed=3))
+    assert {p.key() for p in pairs} == _naive(ds, 0.5)
+    assert c.max_depth == 0
+
+
+def test_recall_precision_and_exact_similarity():
+    from paper_1707_06814_b200 import CPSJoinParams, EmbeddingParams, cpsjoin_self, embed_dataset, jaccard
+    ds = _planted(420, 40, 41)
+    pairs, c = cpsjoin_self(embed_dataset(EmbeddingParams(seed=7), ds), CPSJoinParams(lambda_=0.5, seed=7))
+    truth = _naive(ds, 0.5)
+    got = {p.key() for p in pairs}
+    assert got <= truth and len(got) >= 0.9 * len(truth)
+    for p in pairs:
+        assert jaccard(ds.records[p.a], ds.records[p.b]) == p.similarity
+    assert c.results <= c.candidates <= c.pre_candidates
+
+
+def test_no_pairs_and_degenerate_sizes():
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self, embed_dataset
+    rng = np.random.default_rng(17)
+    ds = Dataset.from_token_lists([rng.choice(4000, size=10, replace=False) for _ in range(120)])
+    pairs, _ = cpsjoin_self(embed_dataset(EmbeddingParams(seed=5), ds), CPSJoinParams(lambda_=0.5, seed=5))
+    assert pairs == []
+    one = Dataset.from_token_lists([[1, 2, 3]])
+    pairs, c = cpsjoin_self(embed_dataset(EmbeddingParams(seed=1), one), CPSJoinParams(lambda_=0.5))
+    assert pairs == [] and c.pre_candidates == 0 and c.peak_live_members == 0
+    empty = Dataset.from_token_lists([])
+    pairs, _ = cpsjoin_self(embed_dataset(EmbeddingParams(seed=1), empty), CPSJoinParams(lambda_=0.5))
+    assert pairs == []
+
+
+def test_deterministic_and_count_table_gap():
+    from paper_1707_06814_b200 import CPSJoinParams, EmbeddingParams, cpsjoin_self, embed_dataset
+    ds = _planted(300, 25, 51)
+    p1, c1 = cpsjoin_self(embed_dataset(EmbeddingParams(seed=9), ds), CPSJoinParams(lambda_=0.6, seed=9))
+    p2, c2 = cpsjoin_self(embed_dataset(EmbeddingParams(seed=9), ds), CPSJoinParams(lambda_=0.6, seed=9))
+    assert [(p.a, p.b, p.similarity) for p in p1] == [(p.a, p.b, p.similarity) for p in p2]
+    assert c1 == c2
+    with pytest.raises(NotImplementedError):
+        cpsjoin_self(embed_dataset(EmbeddingParams(seed=9), ds),
+                     CPSJoinParams(lambda_=0.6, seed=9, use_count_table=True))
+
+
+def test_full_config1_against_oracle_and_exact_truth():
+    """Config 1 at full size (n = 20,000, R = 10): bit-exact vs the oracle;
+    100% precision and recall >= 0.9 against the exact join."""
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    from paper_1707_06814_b200.workloads import generate
+    w = generate(1)
+    ds = Dataset.from_csr(w.tokens, w.offsets, w.d)
+    emb = embed_dataset(EmbeddingParams(t=128, seed=7), ds)
+    res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=0.5, seed=7, repetitions=10))
+    values, sk, ref = O.full_pipeline(w.tokens, w.offsets, w.sizes, lam=0.5, emb_seed=7, seed=7, repetitions=10)
+    assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)
+    truth, _ = O.exact_join(w.tokens, w.offsets, w.d, 0.5)
+    keys = (res.a.astype(np.uint64) << np.uint64(32)) | res.b.astype(np.uint64)
+    assert np.isin(keys, truth).all()
+    assert len(keys) >= 0.9 * len(truth)
