@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""CPSJoin self-join benchmark (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2] [--reps auto|R]
+
+A step is one pass of the hot path over the whole synthetic workload:
+MinHash embedding values (K1, t = 128) + 1-bit sketches (K1, 64 ell
+functions) + the Chosen Path self-join with R repetitions (K2..K6), R the
+smallest repetition count reaching the config's target recall against the
+exact join (prefix-stable seeds).  `value` is measured with the CSR already
+resident in HBM; `e2e` runs the public API from pinned host buffers with
+the host->device copy of the CSR and the device->host read of the result
+pairs inside every step.
+
+--impl reference times the CPU implementation of the same path (the C
+oracle port of the reference, all host threads) on a bounded sample of the
+same workload; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "self-join sets/s at lambda=0.5, >=90% recall (embed + sketch + join)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--reps", default="auto")
+    ap.add_argument("--cpu-scale", type=float, default=None, help="CPU sample scale (default: auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------ clock sampling
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+def load_truth(cfg: int, scale: float, lam: float, tokens, offsets):
+    from oracle.make_truth import csr_sha, truth_path
+    path = truth_path(cfg, scale, lam)
+    if not os.path.exists(path):
+        return None
+    z = np.load(path)
+    if str(z["csr_sha"]) != csr_sha(tokens, offsets):
+        log(f"truth file {path} does not match the generated workload; ignoring")
+        return None
+    return z["keys"]
+
+
+def recall_of(a, b, truth) -> float:
+    if truth is None or len(truth) == 0:
+        return float("nan")
+    keys = (np.asarray(a).astype(np.uint64) << np.uint64(32)) | np.asarray(b).astype(np.uint64)
+    return float(np.isin(truth, keys).mean())
+
+
+def workload_dict(w, cfg, R, rec, lam, extra=None):
+    d = {"workload": f"{cfg.name} (BASELINE.json configs[{int(cfg.data_seed) - 1}])",
+         "n_sets": int(w.n), "nnz_tokens": int(len(w.tokens)), "universe": int(w.d), "lambda": lam,
+         "ell": cfg.ell, "t": 128, "repetitions": int(R), "recall": rec, "target_recall": cfg.recall,
+         "epsilon": 0.1, "delta": 0.05, "limit": 250, "seeds": {"data": cfg.data_seed, "embed": cfg.emb_seed,
+                                                                  "join": cfg.join_seed},
+         "l2_policy": f"inputs larger than L2 (CSR {4 * len(w.tokens) / 1e6:.0f} MB + values "
+                      f"{4 * 128 * w.n / 1e6:.0f} MB > 126 MB L2)"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# -------------------------------------------------------------- CPU (oracle)
+
+def cpu_pipeline_time(cfg_id: int, scale: float, threads: int, reps=None):
+    """Oracle (C port of the reference) on a sample: (sets, seconds, R, recall)."""
+    from oracle import oracle as O
+    from paper_1707_06814_b200.workloads import CONFIGS, generate
+    cfg = CONFIGS[cfg_id]
+    lam = cfg.lambdas[0]
+    w = generate(cfg_id, scale=scale)
+    truth = None
+    if reps is None:
+        truth, _ = O.exact_join(w.tokens, w.offsets, w.d, lam, threads)
+        R, rec = 1, 0.0
+        values = O.minhash(w.tokens, w.offsets, O.embedding_tables(128, cfg.emb_seed), threads)
+        mh, bt = O.sketch_tables(cfg.ell, cfg.join_seed)
+        sk = O.sketch(w.tokens, w.offsets, mh, bt, threads)
+        for R in range(1, 11):
+            out = O.self_join(w.tokens, w.offsets, w.sizes, values, sk, lam, repetitions=R, seed=cfg.join_seed,
+                              threads=threads)
+            rec = float(np.isin(truth, out.keys).mean()) if len(truth) else 1.0
+            if rec >= cfg.recall:
+                break
+        reps = R
+    t0 = time.perf_counter()
+    values, sk, out = O.full_pipeline(w.tokens, w.offsets, w.sizes, lam=lam, t=128, emb_seed=cfg.emb_seed,
+                                      ell=cfg.ell, seed=cfg.join_seed, repetitions=reps, threads=threads)
+    dt = time.perf_counter() - t0
+    rec = float(np.isin(truth, out.keys).mean()) if truth is not None and len(truth) else None
+    return w.n, dt, reps, rec
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank: int, world: int):
+    from paper_1707_06814_b200.workloads import CONFIGS
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    threads = cpu_threads()
+    scale = args.cpu_scale or min(1.0, 25_000 / (cfg.n_background + cfg.n_planted)) * args.scale
+    n, _, R, rec = cpu_pipeline_time(args.config, scale, threads)  # warm-up run also fixes R
+    for _ in range(max(0, args.warmup - 1)):
+        cpu_pipeline_time(args.config, scale, threads, reps=R)
+    times = []
+    for _ in range(args.steps):
+        times.append(cpu_pipeline_time(args.config, scale, threads, reps=R)[1])
+    total = sum(times)
+    value = n * len(times) / total
+    sample = f"{cfg.name} scaled x{scale:g}: {n} sets, R={R} (recall {rec:.3f} on the sample's exact join)"
+    line = {"metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64 integer hashing, f64 verify",
+            "data": "synthetic (seeded generator for BASELINE.json config, sampled)",
+            "config": {"workload": f"{cfg.name} sample", "n_sets": n, "repetitions": R, "recall": rec,
+                       "lambda": cfg.lambdas[0], "ell": cfg.ell, "t": 128},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "sets/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "sets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def run_ours(args, rank: int, world: int):
+    import torch
+
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    from paper_1707_06814_b200._native import Context
+    from paper_1707_06814_b200.distributed import shard_reps
+    from paper_1707_06814_b200.embed import embed_device_csr
+    from paper_1707_06814_b200.workloads import CONFIGS, generate
+
+    cfg = CONFIGS[args.config]
+    lam = cfg.lambdas[0]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t0 = time.time()
+    w = generate(args.config, scale=args.scale)
+    log(f"[rank {rank}] workload {cfg.name} x{args.scale}: n={w.n} nnz={len(w.tokens)} in {time.time() - t0:.1f}s")
+    n = w.n
+    ctx = Context.get()
+
+    # pinned host inputs (the e2e source) and an HBM-resident copy (value)
+    tok_pin = torch.from_numpy(w.tokens.view(np.int32)).pin_memory()
+    off_pin = torch.from_numpy(w.offsets).pin_memory()
+    ds = Dataset.from_csr(tok_pin.numpy().view(np.uint32), off_pin.numpy(), w.d)
+    d_tok = tok_pin.to(dev)
+    d_off = off_pin.to(dev)
+    eparams = EmbeddingParams(t=128, seed=cfg.emb_seed)
+
+    # repetitions: smallest R reaching the target recall (prefix-stable seeds)
+    truth = load_truth(args.config, args.scale, lam, w.tokens, w.offsets)
+    emb0 = embed_device_csr(eparams, d_tok, d_off, w.d, host_csr=(w.tokens, w.offsets))
+    if args.reps != "auto":
+        R = int(args.reps)
+        res = cpsjoin_self_arrays(emb0, CPSJoinParams(lambda_=lam, ell=cfg.ell, seed=cfg.join_seed, repetitions=R))
+        rec = recall_of(res.a, res.b, truth)
+    elif truth is None:
+        R, rec = 3, float("nan")
+        log("no exact-join truth for this workload: R fixed at 3, recall unmeasured")
+    else:
+        for R in range(1, 11):
+            res = cpsjoin_self_arrays(emb0, CPSJoinParams(lambda_=lam, ell=cfg.ell, seed=cfg.join_seed,
+                                                          repetitions=R))
+            rec = recall_of(res.a, res.b, truth)
+            if rec >= cfg.recall:
+                break
+    log(f"[rank {rank}] R={R} recall={rec:.4f} truth={None if truth is None else len(truth)}")
+    del emb0
+    params = CPSJoinParams(lambda_=lam, ell=cfg.ell, seed=cfg.join_seed, repetitions=R)
+
+    stream = torch.cuda.current_stream(dev)
+    k1_events = []
+
+    def step_device():
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        emb = embed_device_csr(eparams, d_tok, d_off, w.d)
+        ev[1].record(stream)
+        emb.sketches_device(cfg.ell, cfg.join_seed)
+        ev[2].record(stream)
+        k1_events.append(ev)
+        return shard_reps(emb, params, rank, world)
+
+    def step_e2e():
+        emb = embed_dataset(eparams, ds)
+        return shard_reps(emb, params, rank, world)
+
+    def timed(fn, steps):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        out = None
+        for _ in range(steps):
+            out = fn()
+        end.record(stream)
+        torch.cuda.synchronize()
+        ms = start.elapsed_time(end)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, out
+
+    for _ in range(args.warmup):
+        step_device()
+        step_e2e()
+    k1_events.clear()
+    launches0 = ctx_launch_count(ctx)
+    ctx.profile(True)
+    with ClockSampler(dev.index) as clk:
+        ms_dev, res = timed(step_device, args.steps)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    launches = ctx_launch_count(ctx) - launches0
+    ms_e2e, res_e2e = timed(step_e2e, args.steps)
+    value = n * args.steps / (ms_dev / 1e3)
+    e2e_value = n * args.steps / (ms_e2e / 1e3)
+
+    # dominant kernel: K1 sketch launch (64 ell functions); algorithmic bytes
+    # = CSR read once (4 nnz + 8 (n+1)) + sketch written (8 ell n)
+    k1_val_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in k1_events)
+    k1_sk_ms = statistics.mean(b.elapsed_time(c) for _, b, c in k1_events)
+    nnz = len(w.tokens)
+    peaks = measured_peaks()
+    sk_bytes = 4 * nnz + 8 * (n + 1) + 8 * cfg.ell * n
+    achieved = sk_bytes / (k1_sk_ms / 1e3) / 1e9
+    L = 1 if w.d <= 1 << 8 else 2 if w.d <= 1 << 16 else 3 if w.d <= 1 << 24 else 4
+    f_clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    evals = nnz * 64 * cfg.ell
+    lookup_peak = 148 * f_clk * 32 / L   # one conflict-free 32-lane LDS wavefront per clk per SM
+    k4_ms = prof["k4_leaf"][0] + prof["point"][0]
+    pre = res.counters.pre_candidates
+    pairs_per_s = pre * args.steps / (k4_ms / 1e3) if k4_ms > 0 else None
+    popc_peak = 148 * 16 * f_clk / (2 * cfg.ell)  # POPC 16/clk/SM assumed, 2 per u64 word
+    h2d = int(w.tokens.nbytes + w.offsets.nbytes)
+    d2h = int(len(res_e2e.a) * 16)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        scale = args.cpu_scale or min(1.0, 25_000 / (cfg.n_background + cfg.n_planted)) * args.scale
+        cn, cdt, cR, crec = cpu_pipeline_time(args.config, scale, threads)
+        cpu = {"value": cn / cdt, "unit": "sets/s", "cores": threads, "kind": "port",
+               "sample": f"{cfg.name} scaled x{scale:g}: {cn} sets, embed+sketch+join R={cR} "
+                         f"(recall {crec:.3f} on the sample's exact join), {cdt:.1f} s"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded generator for BASELINE.json config; Mann et al. datasets unavailable)",
+        "config": workload_dict(w, cfg, R, rec, lam, {"parallelism": f"reps sharded over {world} GPU(s)"}),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
+                     "frac": achieved / float(peaks["hbm_gbs"]), "traffic": None,
+                     "kernel": "k_minhash<L> sketch launch (K1, 64*ell functions)",
+                     "algorithmic_bytes": sk_bytes, "avg_launch_ms": k1_sk_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
+        "roofline_smem": {"bound": "shared-memory lookups (LDS.32, 32 lanes/clk/SM)",
+                          "achieved_evals_per_s": evals / (k1_sk_ms / 1e3), "peak_evals_per_s": lookup_peak,
+                          "frac": evals / (k1_sk_ms / 1e3) / lookup_peak, "key_bytes": L,
+                          "values_launch_ms": k1_val_ms},
+        "roofline_int": {"kernel": "k_leaf_tiles + k_point (K4 BruteForce)", "pairs_per_s": pairs_per_s,
+                         "peak_pairs_per_s": popc_peak,
+                         "frac": (pairs_per_s / popc_peak) if pairs_per_s else None,
+                         "peak_basis": "POPC 16/clk/SM x 148 x sm_max_mhz / (2 ell) (assumed, SURVEY.md 8(d))"},
+        "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+        "join_counters": {"pre_candidates": pre, "candidates": res.counters.candidates,
+                          "results": res.counters.results, "max_depth": res.counters.max_depth,
+                          "pairs": int(len(res.a))},
+        "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": ms_e2e / args.steps},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "impl": "ours",
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def ctx_launch_count(ctx) -> int:
+    """Own kernels launched so far on this context (K1 + join kernels)."""
+    return ctx.launch_counts()[0]
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -112,7 +112,8 @@ typedef struct {
     int64_t peak_live_members;/* DFS stack peak, reproduced exactly            */
     int64_t n_depth_cap_events;
     int64_t n_levels;         /* frontier levels processed                    */
-    int64_t gpu_launches;     /* kernels launched by this call                */
+    int64_t gpu_launches;     /* own kernels launched by this call            */
+    int64_t lib_calls;        /* CUB device-wide scans/sorts issued           */
 } cpsj_join_stats;
 
 /*
@@ -133,6 +134,19 @@ CPSJ_API int cpsj_join_copy_result(cpsj_ctx *ctx, uint64_t *h_keys, double *h_si
 /* device pointers to the last join's arena (valid until the next call) */
 CPSJ_API int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys,
                             const double **d_sims, int64_t *n_pairs);
+
+/*
+ * Device-time profile by kernel class (CUDA events on the call's stream).
+ * Classes: 0 K1 minhash/sketch, 1 K4 leaf BruteForce, 2 point compares,
+ * 3 node sketch + flags, 4 split, 5 K5 verify, 6 K6 dedup, 7 level plan.
+ * enable != 0 clears the accumulators and starts recording; read
+ * synchronises the recorded events and returns per-class totals.
+ */
+#define CPSJ_PROF_CLASSES 8
+/* cumulative counts on this context: own kernels launched, CUB calls */
+CPSJ_API int cpsj_launch_counts(const cpsj_ctx *ctx, int64_t *own_kernels, int64_t *lib_calls);
+CPSJ_API int cpsj_profile_enable(cpsj_ctx *ctx, int enable);
+CPSJ_API int cpsj_profile_read(cpsj_ctx *ctx, double *h_ms, int64_t *h_count, int32_t n_classes);
 
 #ifdef __cplusplus
 }

@@ -30,12 +30,15 @@ class Plan(ctypes.Structure):
 class JoinStats(ctypes.Structure):
     _fields_ = [("n_pairs", i64), ("pre_candidates", i64), ("candidates", i64), ("results", i64),
                 ("max_depth", i64), ("peak_live_members", i64), ("n_depth_cap_events", i64),
-                ("n_levels", i64), ("gpu_launches", i64)]
+                ("n_levels", i64), ("gpu_launches", i64), ("lib_calls", i64)]
 
 
 EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_error",
            "cpsj_family_create", "cpsj_family_destroy", "cpsj_minhash_sketch", "cpsj_self_join",
-           "cpsj_join_copy_result", "cpsj_join_result_device"]
+           "cpsj_join_copy_result", "cpsj_join_result_device", "cpsj_profile_enable", "cpsj_profile_read",
+           "cpsj_launch_counts"]
+
+PROF_CLASSES = ["k1_minhash", "k4_leaf", "point", "node", "split", "k5_verify", "k6_dedup", "plan"]
 
 _lib = None
 _lock = threading.Lock()
@@ -67,6 +70,9 @@ def load(path: str | None = None):
                                      ctypes.POINTER(JoinStats), P]
         L.cpsj_join_copy_result.argtypes = [P, P, P, i64, P, i64, P]
         L.cpsj_join_result_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)]
+        L.cpsj_profile_enable.argtypes = [P, ctypes.c_int]
+        L.cpsj_profile_read.argtypes = [P, P, P, i32]
+        L.cpsj_launch_counts.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         _lib = L
         return L
 
@@ -110,6 +116,21 @@ class Context:
 
     def check(self, rc: int) -> None:
         check(self.handle, rc)
+
+    def launch_counts(self) -> tuple[int, int]:
+        own, lib = i64(), i64()
+        self.check(self.lib.cpsj_launch_counts(self.handle, ctypes.byref(own), ctypes.byref(lib)))
+        return int(own.value), int(lib.value)
+
+    def profile(self, enable: bool) -> None:
+        self.check(self.lib.cpsj_profile_enable(self.handle, int(enable)))
+
+    def profile_read(self) -> dict:
+        import numpy as np
+        ms = np.zeros(len(PROF_CLASSES), dtype=np.float64)
+        cnt = np.zeros(len(PROF_CLASSES), dtype=np.int64)
+        self.check(self.lib.cpsj_profile_read(self.handle, ms.ctypes.data, cnt.ctypes.data, len(PROF_CLASSES)))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(PROF_CLASSES)}
 
 
 class Family:

@@ -106,7 +106,7 @@ class JoinArrays:
     stats: dict
 
 
-def _run(emb: EmbeddedDataset, params: CPSJoinParams) -> JoinArrays:
+def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinArrays:
     import torch
 
     from ._native import Context, Inputs, JoinStats, Plan
@@ -130,9 +130,10 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams) -> JoinArrays:
                         sk.data_ptr(), params.ell)
     else:
         inputs = Inputs(None, None, None, n, None, t, None, params.ell)
-    seeds = np.ascontiguousarray(plan.rep_seeds)
+    seeds = plan.rep_seeds if rep_indices is None else plan.rep_seeds[np.asarray(rep_indices, dtype=np.int64)]
+    seeds = np.ascontiguousarray(seeds)
     cplan = Plan(float(params.lambda_), int(params.limit), int(params.depth_cap), plan.accept_dist,
-                 plan.flag_dist, float(plan.split_p), seeds.ctypes.data, int(params.repetitions))
+                 plan.flag_dist, float(plan.split_p), seeds.ctypes.data, int(len(seeds)))
     st = JoinStats()
     ctx.check(ctx.lib.cpsj_self_join(ctx.handle, ctypes.byref(inputs), ctypes.byref(cplan), ctypes.byref(st),
                                      stream))
@@ -168,9 +169,11 @@ def _emit_warnings(res: JoinArrays, params: CPSJoinParams, n: int) -> None:
                            res.counters.max_depth, bound, n)
 
 
-def cpsjoin_self_arrays(emb: EmbeddedDataset, params: CPSJoinParams) -> JoinArrays:
-    """cpsjoin_self returning numpy arrays instead of ResultPair objects."""
-    res = _run(emb, params)
+def cpsjoin_self_arrays(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinArrays:
+    """cpsjoin_self returning numpy arrays instead of ResultPair objects.
+    ``rep_indices`` restricts the run to a subset of the repetition trees
+    (used to shard repetitions across GPUs)."""
+    res = _run(emb, params, rep_indices)
     _emit_warnings(res, params, len(emb))
     return res
 

@@ -159,4 +159,47 @@ int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys, const double
     return CPSJ_OK;
 }
 
+int cpsj_launch_counts(const cpsj_ctx *ctx, int64_t *own_kernels, int64_t *lib_calls) {
+    if (!ctx) return CPSJ_E_ARG;
+    if (own_kernels) *own_kernels = ctx->launches;
+    if (lib_calls) *lib_calls = ctx->lib_calls;
+    return CPSJ_OK;
+}
+
+int cpsj_profile_enable(cpsj_ctx *ctx, int enable) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        for (auto &e : ctx->prof_events) {
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        ctx->prof_events.clear();
+        for (int i = 0; i < PROF_CLASSES; ++i) {
+            ctx->prof_ms[i] = 0;
+            ctx->prof_count[i] = 0;
+        }
+        ctx->prof = enable != 0;
+    });
+}
+
+int cpsj_profile_read(cpsj_ctx *ctx, double *h_ms, int64_t *h_count, int32_t n_classes) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        for (auto &e : ctx->prof_events) {
+            CPSJ_CUDA(cudaEventSynchronize(e.b));
+            float ms = 0;
+            CPSJ_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+            ctx->prof_ms[e.cls] += ms;
+            ctx->prof_count[e.cls] += 1;
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        ctx->prof_events.clear();
+        for (int i = 0; i < n_classes && i < PROF_CLASSES; ++i) {
+            if (h_ms) h_ms[i] = ctx->prof_ms[i];
+            if (h_count) h_count[i] = ctx->prof_count[i];
+        }
+    });
+}
+
 }  // extern "C"

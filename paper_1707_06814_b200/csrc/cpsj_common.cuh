@@ -115,8 +115,30 @@ __device__ __forceinline__ int64_t upper_bound_i64(const int64_t *a, int64_t n, 
 
 // -------------------------------------------------------------- context
 
+enum {
+    PROF_K1 = 0,       // minhash values / sketches
+    PROF_LEAF = 1,     // K4 leaf all-pairs popcount filter
+    PROF_POINT = 2,    // flagged-member point comparisons
+    PROF_NODE = 3,     // node sketch + flag rule + survivors
+    PROF_SPLIT = 4,    // position selection, keys, radix sort, children
+    PROF_VERIFY = 5,   // K5 exact verification
+    PROF_DEDUP = 6,    // K6 sort + unique
+    PROF_PLAN = 7,     // level planning scans and host reads
+    PROF_CLASSES = 8
+};
+
+struct ProfEvent {
+    int cls;
+    cudaEvent_t a, b;
+};
+
 struct cpsj_ctx {
     int device = 0;
+    bool prof = false;
+    std::vector<ProfEvent> prof_events;
+    double prof_ms[PROF_CLASSES] = {};
+    int64_t prof_count[PROF_CLASSES] = {};
+    int64_t lib_calls = 0;  // CUB device-wide primitive invocations
     std::string err;
     int sm_count = 0;
     // result arena of the last join
@@ -138,6 +160,29 @@ struct cpsj_family {
 };
 
 namespace cpsj {
+
+// records the device time of everything issued on `st` inside its scope
+// when profiling is on (cpsj_profile_enable); no-op otherwise
+struct ProfScope {
+    cpsj_ctx *ctx;
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(cpsj_ctx *c, int k, cudaStream_t s) : ctx(c), cls(k), st(s) {
+        if (ctx->prof) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEventRecord(b, st);
+            ctx->prof_events.push_back({cls, a, b});
+        }
+    }
+};
+
 int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,
                    const int64_t *d_offsets, int64_t n, uint32_t max_token, uint32_t *d_values,
                    uint64_t *d_sketch, cudaStream_t stream);

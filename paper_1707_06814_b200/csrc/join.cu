@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 
 #include "cpsj_common.cuh"
 
@@ -483,7 +484,7 @@ struct Driver {
         CPSJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, st));
         if (bytes > cub_tmp.n) cub_tmp.alloc(bytes * 2, st);
         CPSJ_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp.p, bytes, in, out, n, st));
-        ctx->launches++;
+        ctx->lib_calls++;
     }
 
     // read up to three device scalars with one synchronisation
@@ -505,6 +506,7 @@ void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, int64_t tiles, const int64_t *t
                  const cpsj_inputs *in, int32_t accept, double lam, int2 *cand, unsigned long long cap,
                  DevCounters *ctr) {
     const int64_t threads = tiles * 32;
+    ProfScope prof(ctx, PROF_LEAF, st);
     k_leaf_tiles<ELL><<<blocks_for(threads), TPB, 0, st>>>(tiles, tile_off, lv.N, lv.off.p, lv.cnt.p, lv.members.p,
                                                            in->d_sketch, in->ell, in->d_sizes, accept, lam, cand,
                                                            cap, ctr);
@@ -534,6 +536,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     require(plan->n_reps >= 0 && plan->limit >= 1, "bad plan");
     std::memset(stats, 0, sizeof(*stats));
     const int64_t launches0 = ctx->launches;
+    const int64_t lib0 = ctx->lib_calls;
     const int64_t n = in->n;
     const int t = in->t, ell = in->ell;
     const double lam = plan->lambda_;
@@ -602,6 +605,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 rsims.grow(want, res_cap, st);
                 res_cap = want;
             }
+            ProfScope prof(ctx, PROF_VERIFY, st);
             k_verify<<<blocks_for((int64_t)nc * 32), TPB, 0, st>>>((int64_t)nc, cand.p, in->d_tokens,
                                                                    in->d_offsets, in->d_sizes, lam, rkeys.p,
                                                                    rsims.p, ctr.p);
@@ -618,6 +622,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         max_depth = depth;
         const int64_t N = lv.N;
         // ---- plan: leaves vs internal nodes
+        std::unique_ptr<ProfScope> prof_plan(new ProfScope(ctx, PROF_PLAN, st));
         DevBuf<int64_t> tiles(N + 1, st), internal(N + 1, st), imem(N + 1, st);
         DevBuf<int64_t> tile_off(N + 1, st), iscan(N + 1, st), im_off(N + 1, st);
         k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, internal.p, imem.p, ctr.p);
@@ -630,6 +635,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         drv.read3(tile_off.p, N, iscan.p, N, im_off.p, N, dscal.p, sc);
         const int64_t total_tiles = sc[0], n_int = sc[1], Mi = sc[2];
         CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cand_n, 0, sizeof(unsigned long long), st));
+        prof_plan.reset();
 
         // ---- leaves: K4, then K5 on their candidates
         if (total_tiles > 0) {
@@ -657,6 +663,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 drv.scan(icnt.p, im_off_c.p, n_int + 1);
             }
             DevBuf<uint64_t> nsk(n_int * ell, st);
+            std::unique_ptr<ProfScope> prof_node(new ProfScope(ctx, PROF_NODE, st));
             k_node_sketch<<<(unsigned)n_int, TPB, 0, st>>>(ilist.p, lv.off.p, lv.cnt.p, lv.seed.p, lv.members.p,
                                                            in->d_sketch, ell, t,
                                                            reinterpret_cast<uint32_t *>(nsk.p), ctr.p);
@@ -670,6 +677,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             drv.scan(flags.p, fscan.p, Mi + 1);
             drv.read3(fscan.p, Mi, nullptr, 0, nullptr, 0, dscal.p, sc);
             const int64_t n_flag = sc[0];
+            prof_node.reset();
             if (n_flag > 0) {
                 DevBuf<int64_t> flist(n_flag, st);
                 k_flag_list<<<blocks_for(Mi), TPB, 0, st>>>(Mi, flags.p, fscan.p, flist.p);
@@ -677,6 +685,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 ctx->launches++;
                 int count_pre = 1;
                 auto gen = [&]() {
+                    ProfScope prof(ctx, PROF_POINT, st);
                     k_point<<<blocks_for(n_flag * 32), TPB, 0, st>>>(
                         n_flag, flist.p, fscan.p, flags.p, im_off_c.p, n_int, ilist.p, lv.off.p, lv.cnt.p,
                         lv.members.p, in->d_sketch, ell, in->d_sizes, plan->accept_dist, lam, cand.p, cand_cap,
@@ -689,11 +698,15 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 flush(gen);
             }
             DevBuf<int32_t> surv(std::max<int64_t>(1, Mi - n_flag), st);
-            k_survivors<<<blocks_for(Mi), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p, lv.members.p,
-                                                        flags.p, fscan.p, surv.p);
-            CPSJ_LAUNCH_CHECK();
-            ctx->launches++;
+            {
+                ProfScope prof(ctx, PROF_NODE, st);
+                k_survivors<<<blocks_for(Mi), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p,
+                                                            lv.members.p, flags.p, fscan.p, surv.p);
+                CPSJ_LAUNCH_CHECK();
+                ctx->launches++;
+            }
             // ---- split
+            ProfScope prof_split(ctx, PROF_SPLIT, st);
             DevBuf<int16_t> sel_pos(n_int * t, st);
             DevBuf<int64_t> nsel(n_int + 1, st), nent(n_int + 1, st), seg_off(n_int + 1, st), e_off(n_int + 1, st);
             DevBuf<int64_t> capsz(n_int, st);
@@ -734,7 +747,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
                 CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
                                                           0, end_bit, st));
-                ctx->launches++;
+                ctx->lib_calls++;
                 DevBuf<int64_t> head(E + 1, st), hscan(E + 1, st);
                 k_heads<<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
                 CPSJ_LAUNCH_CHECK();
@@ -781,6 +794,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     CPSJ_CUDA(cudaMemcpyAsync(&hc, ctr.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
     CPSJ_CUDA(cudaStreamSynchronize(st));
     const int64_t nres = (int64_t)hc.res_n;
+    ProfScope prof_dedup(ctx, PROF_DEDUP, st);
     ctx->res_keys.release();
     ctx->res_sims.release();
     if (nres > 0) {
@@ -790,7 +804,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64, st));
         if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
         CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64, st));
-        ctx->launches++;
+        ctx->lib_calls++;
         ctx->res_keys.alloc(nres, st);
         ctx->res_sims.alloc(nres, st);
         DevBuf<int64_t> nsel(1, st);
@@ -800,7 +814,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
         CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(drv.cub_tmp.p, bytes, k2.p, s2.p, ctx->res_keys.p, ctx->res_sims.p,
                                                  nsel.p, nres, st));
-        ctx->launches++;
+        ctx->lib_calls++;
         int64_t u = 0;
         CPSJ_CUDA(cudaMemcpyAsync(&u, nsel.p, 8, cudaMemcpyDeviceToHost, st));
         CPSJ_CUDA(cudaStreamSynchronize(st));
@@ -816,6 +830,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     stats->n_depth_cap_events = (int64_t)ctx->cap_events.size();
     stats->n_levels = levels;
     stats->gpu_launches = ctx->launches - launches0;
+    stats->lib_calls = ctx->lib_calls - lib0;
 }
 
 }  // namespace cpsj

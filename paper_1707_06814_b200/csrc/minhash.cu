@@ -162,6 +162,7 @@ static void launch_minhash(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t
     per_sm = std::max(per_sm, 1);
     const int64_t want = (n + K1_WARPS - 1) / K1_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count * per_sm));
+    ProfScope prof(ctx, PROF_K1, stream);
     k_minhash<L><<<grid, K1_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask,
                                                      fam->F, values, sketch32);
     CPSJ_LAUNCH_CHECK();

@@ -71,6 +71,8 @@ class EmbeddedDataset:
         self._sketch_cache: dict = {}
         self._dev_sketch: dict = {}
         self._dev: dict = {}
+        self._width = None      # token universe bound of the CSR, if known
+        self._sizes_fn = None   # lazy host sizes for device-only datasets
 
     # ------------------------------------------------------------- internal
     @classmethod
@@ -78,6 +80,7 @@ class EmbeddedDataset:
         obj = cls(None, None, None, t, seed, None, np.diff(offsets), np.arange(len(offsets) - 1, dtype=np.int64),
                   origin=origin)
         obj._csr_arrays = (tokens, offsets, d_universe)
+        obj._width = d_universe
         obj._dev["values"] = dev_values
         obj._dev["tokens"], obj._dev["offsets"] = dev_csr
         obj._n = len(offsets) - 1
@@ -173,6 +176,8 @@ class EmbeddedDataset:
 
     @property
     def sizes(self) -> np.ndarray:
+        if self._sizes is None and self._sizes_fn is not None:
+            self._sizes = self._sizes_fn()
         return self._sizes
 
     @sizes.setter
@@ -201,7 +206,7 @@ class EmbeddedDataset:
             if n > 0:
                 tok, off, sizes, _ = self.device_inputs(ctx)
                 fam = sketch_family(ell, seed).device(ctx)
-                _, _, width = self._csr_host()
+                width = self._width if self._width is not None else self._csr_host()[2]
                 stream = torch.cuda.current_stream(dev).cuda_stream
                 ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, fam.handle, tok.data_ptr(), off.data_ptr(), n,
                                                       max(0, min(int(width) - 1, 0xFFFFFFFF)) if width else
@@ -223,6 +228,37 @@ def embed_record(params: EmbeddingParams, x: Record) -> list[tuple[int, int]]:
     tok = np.asarray(x.tokens, dtype=np.uint32)
     vals = minhash_segments_many(params.tables, tok, np.array([0, len(tok)], dtype=np.int64))[0]
     return [(i, int(v)) for i, v in enumerate(vals)]
+
+
+def embed_device_csr(params: EmbeddingParams, d_tokens, d_offsets, d: int, host_csr=None,
+                     origin: Dataset | None = None) -> EmbeddedDataset:
+    """embed_dataset for a CSR that is already resident on the GPU (torch
+    int32 token / int64 offset tensors).  ``host_csr`` = (tokens, offsets)
+    numpy arrays, if the caller has them, back the lazy host attributes."""
+    torch = _torch()
+    from ._native import Context
+    ctx = Context.get()
+    n = int(d_offsets.shape[0]) - 1
+    t = params.t
+    fam = params.device(ctx)
+    dev = torch.device("cuda", ctx.device)
+    d_vals = torch.empty((max(n, 0), t), dtype=torch.int32, device=dev)
+    max_token = min(int(d) - 1, 0xFFFFFFFF) if d and d > 0 else 0xFFFFFFFF
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if n > 0:
+        ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, fam.handle, d_tokens.data_ptr(), d_offsets.data_ptr(), n,
+                                              max_token, d_vals.data_ptr(), None, stream))
+    if host_csr is None:
+        host_csr = (None, None)
+    tok, off = host_csr
+    obj = EmbeddedDataset(None, None, None, t, params.seed, None, None, np.arange(n, dtype=np.int64), origin=origin)
+    obj._csr_arrays = (tok, off, int(d)) if tok is not None else None
+    obj._width = int(d)
+    obj._dev.update(values=d_vals, tokens=d_tokens, offsets=d_offsets)
+    obj._dev["sizes"] = (d_offsets[1:] - d_offsets[:-1]).to(torch.int32)
+    obj._n = n
+    obj._sizes_fn = lambda: obj._dev["sizes"].cpu().numpy().astype(np.int64)
+    return obj
 
 
 def embed_dataset(params: EmbeddingParams, ds: Dataset) -> EmbeddedDataset:
