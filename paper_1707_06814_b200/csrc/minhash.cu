@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "cpsj_common.cuh"
 
@@ -132,6 +133,294 @@ __global__ void __launch_bounds__(K1_THREADS) k_minhash(
     }
 }
 
+// ---------------------------------------------------------------------
+// 64-function variant (key bytes L <= 3): every lane owns TWO functions of
+// a 64-function chunk (f = lane and f = lane + 32), the table row of one
+// (byte table k, byte value b) is 32 lanes x uint2 = 256 B, and one LDS.64
+// per lane fetches both functions' entries (2 conflict-free wavefronts).
+// Per token the warp-uniform address math (3 byte offsets) and the token
+// broadcast are amortised over 64 evaluations instead of 32.
+constexpr int K1W_WARPS = 32;
+constexpr int K1W_THREADS = K1W_WARPS * 32;
+
+struct MinState {
+    uint32_t best, tok;
+    bool tie;
+};
+
+__device__ __forceinline__ void min_update(MinState &m, uint32_t h, uint32_t tok) {
+    const bool lt = h < m.best;
+    m.tie = lt ? false : (m.tie | (h == m.best));
+    m.tok = lt ? tok : m.tok;
+    m.best = lt ? h : m.best;
+}
+
+template <int L>
+__device__ __forceinline__ uint2 hi_pair(const char *tab, uint32_t tok, uint32_t lane8) {
+    // byte offsets of entries (k, b, lane) = k * 64 KiB + b * 256 + lane * 8
+    const uint32_t o0 = ((tok << 8) & 0xFF00u) | lane8;
+    uint2 h = *reinterpret_cast<const uint2 *>(tab + o0);
+    if (L > 1) {
+        const uint32_t o1 = (tok & 0xFF00u) | lane8;
+        const uint2 v = *reinterpret_cast<const uint2 *>(tab + 65536 + o1);
+        h.x ^= v.x;
+        h.y ^= v.y;
+    }
+    if (L > 2) {
+        const uint32_t o2 = ((tok >> 8) & 0xFF00u) | lane8;
+        const uint2 v = *reinterpret_cast<const uint2 *>(tab + 131072 + o2);
+        h.x ^= v.x;
+        h.y ^= v.y;
+    }
+    return h;
+}
+
+__device__ __forceinline__ uint32_t resolve_tie(const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+                                                int fn, const uint32_t *__restrict__ tokens, int64_t beg,
+                                                int64_t end) {
+    uint64_t bg = full_hash(hi, lo, fn, tokens[beg]);
+    uint32_t bt = tokens[beg];
+    for (int64_t i = beg + 1; i < end; ++i) {
+        const uint32_t tk = tokens[i];
+        const uint64_t g = full_hash(hi, lo, fn, tk);
+        if (g < bg || (g == bg && tk < bt)) { bg = g; bt = tk; }
+    }
+    return bt;
+}
+
+__device__ __forceinline__ uint32_t sketch_bit(const uint32_t *__restrict__ bitmask, int fn, uint32_t tok) {
+    const uint32_t *bm = bitmask + (size_t)fn * 32;
+    const uint32_t b0 = tok & 255, b1 = (tok >> 8) & 255, b2 = (tok >> 16) & 255, b3 = tok >> 24;
+    return ((bm[b0 >> 5] >> (b0 & 31)) ^ (bm[8 + (b1 >> 5)] >> (b1 & 31)) ^ (bm[16 + (b2 >> 5)] >> (b2 & 31)) ^
+            (bm[24 + (b3 >> 5)] >> (b3 & 31))) & 1u;
+}
+
+template <int L>
+__global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash64(
+    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
+    const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+    const uint32_t *__restrict__ bitmask, int F, uint32_t *__restrict__ values,
+    uint64_t *__restrict__ sketch) {
+    extern __shared__ uint2 tab2[];  // [L][256][32] x {f = lane, f = lane + 32}
+    const char *tab = reinterpret_cast<const char *>(tab2);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lane8 = (uint32_t)lane << 3;
+    const int nchunks = (F + 63) >> 6;
+    const int words = F >> 6;  // sketch words per set
+    for (int c = 0; c < nchunks; ++c) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < L * 256 * 32; e += K1W_THREADS) {
+            const int k = e >> 13, b = (e >> 5) & 255, ln = e & 31;
+            uint2 v = make_uint2(0u, 0u);
+            const int f0 = (c << 6) + ln, f1 = f0 + 32;
+            if (f0 < F) {
+                const size_t base = (size_t)f0 * 1024;
+                v.x = hi[base + k * 256 + b];
+                if (k == L - 1)
+                    for (int kk = L; kk < 4; ++kk) v.x ^= hi[base + kk * 256];
+            }
+            if (f1 < F) {
+                const size_t base = (size_t)f1 * 1024;
+                v.y = hi[base + k * 256 + b];
+                if (k == L - 1)
+                    for (int kk = L; kk < 4; ++kk) v.y ^= hi[base + kk * 256];
+            }
+            tab2[e] = v;
+        }
+        __syncthreads();
+        const int fn0 = (c << 6) + lane, fn1 = fn0 + 32;
+        for (int64_t s = (int64_t)blockIdx.x * K1W_WARPS + warp; s < n; s += (int64_t)gridDim.x * K1W_WARPS) {
+            const int64_t beg = offsets[s], end = offsets[s + 1];
+            MinState m0{0, 0, false}, m1{0, 0, false};
+            for (int64_t base = beg; base < end; base += 32) {
+                const int cnt = end - base < 32 ? (int)(end - base) : 32;
+                const uint32_t mine = lane < cnt ? __ldg(tokens + base + lane) : 0u;
+                int j = 0;
+                if (base == beg) {
+                    const uint32_t tok = __shfl_sync(0xffffffffu, mine, 0);
+                    const uint2 h = hi_pair<L>(tab, tok, lane8);
+                    m0 = MinState{h.x, tok, false};
+                    m1 = MinState{h.y, tok, false};
+                    j = 1;
+                }
+#pragma unroll 4
+                for (; j < cnt; ++j) {
+                    const uint32_t tok = __shfl_sync(0xffffffffu, mine, j);
+                    const uint2 h = hi_pair<L>(tab, tok, lane8);
+                    min_update(m0, h.x, tok);
+                    min_update(m1, h.y, tok);
+                }
+            }
+            // full 64-bit resolution of a high-word tie (hashing.py:124)
+            if (m0.tie && fn0 < F) m0.tok = resolve_tie(hi, lo, fn0, tokens, beg, end);
+            if (m1.tie && fn1 < F) m1.tok = resolve_tie(hi, lo, fn1, tokens, beg, end);
+            if (end == beg) m0.tok = m1.tok = 0;
+            if (values != nullptr) {
+                if (fn0 < F) values[s * F + fn0] = m0.tok;
+                if (fn1 < F) values[s * F + fn1] = m1.tok;
+            }
+            if (sketch != nullptr) {
+                const uint32_t w0 = __ballot_sync(0xffffffffu, end > beg && sketch_bit(bitmask, fn0, m0.tok));
+                const uint32_t w1 = __ballot_sync(0xffffffffu, end > beg && sketch_bit(bitmask, fn1, m1.tok));
+                if (lane == 0) sketch[s * words + c] = ((uint64_t)w1 << 32) | w0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------
+// Keyed variant (sets of <= 2048 tokens).  The smem tables hold the high
+// hash word with its low 11 bits cleared, so key = (T0 ^ T1 ^ T2) | p is
+// (21-bit hash part, 11-bit position p of the token in its set); a single
+// unsigned min over keys is the argmin over the hash part (ties broken by
+// position).  The second smallest key is tracked with min(max(.)); if its
+// hash part equals the minimum's, two tokens tie on the compared bits and
+// the lane re-resolves the set with the full 64-bit hash (hashing.py:124),
+// which also settles every case the 21-bit compare cannot.  Five integer
+// ops per evaluation instead of eight for the flag-based update.
+constexpr int KEY_BITS = 11;
+constexpr uint32_t KEY_MASK = (1u << KEY_BITS) - 1;
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+
+template <int L>
+__device__ __forceinline__ uint2 key_pair(uint32_t tok, uint32_t lane_base) {
+    // entry (k, b, lane) lives at k * 64 KiB + b * 256 + lane * 8
+    uint2 h = lds64(lane_base + __byte_perm(tok, 0u, 0x4404));
+    if (L > 1) {
+        const uint2 v = lds64(lane_base + 65536u + (tok & 0xFF00u));
+        h.x ^= v.x;
+        h.y ^= v.y;
+    }
+    if (L > 2) {
+        const uint2 v = lds64(lane_base + 131072u + __byte_perm(tok, 0u, 0x4424));
+        h.x ^= v.x;
+        h.y ^= v.y;
+    }
+    return h;
+}
+
+struct KeyMin {
+    uint32_t m1, m2;
+};
+
+__device__ __forceinline__ void key_update(KeyMin &k, uint32_t key) {
+    k.m2 = min(k.m2, max(k.m1, key));
+    k.m1 = min(k.m1, key);
+}
+
+template <int L>
+__global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_keyed(
+    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
+    const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+    const uint32_t *__restrict__ bitmask, int F, uint32_t *__restrict__ values,
+    uint64_t *__restrict__ sketch) {
+    extern __shared__ uint2 tab2[];  // [L][256][32] x {f = lane, f = lane + 32}
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lane_base = (uint32_t)__cvta_generic_to_shared(tab2) + ((uint32_t)lane << 3);
+    const int nchunks = (F + 63) >> 6;
+    const int words = F >> 6;
+    for (int c = 0; c < nchunks; ++c) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < L * 256 * 32; e += K1W_THREADS) {
+            const int k = e >> 13, b = (e >> 5) & 255, ln = e & 31;
+            uint2 v = make_uint2(0u, 0u);
+            const int f0 = (c << 6) + ln, f1 = f0 + 32;
+            if (f0 < F) {
+                const size_t base = (size_t)f0 * 1024;
+                v.x = hi[base + k * 256 + b];
+                if (k == L - 1)
+                    for (int kk = L; kk < 4; ++kk) v.x ^= hi[base + kk * 256];
+            }
+            if (f1 < F) {
+                const size_t base = (size_t)f1 * 1024;
+                v.y = hi[base + k * 256 + b];
+                if (k == L - 1)
+                    for (int kk = L; kk < 4; ++kk) v.y ^= hi[base + kk * 256];
+            }
+            v.x &= ~KEY_MASK;
+            v.y &= ~KEY_MASK;
+            tab2[e] = v;
+        }
+        __syncthreads();
+        const int fn0 = (c << 6) + lane, fn1 = fn0 + 32;
+        for (int64_t s = (int64_t)blockIdx.x * K1W_WARPS + warp; s < n; s += (int64_t)gridDim.x * K1W_WARPS) {
+            const int64_t beg = offsets[s], end = offsets[s + 1];
+            const int len = (int)(end - beg);
+            uint32_t t0 = 0, t1 = 0;
+            if (len > (int)KEY_MASK + 1) {
+                // long set: the 11-bit position field would wrap; resolve
+                // every function exactly (rare: sets > 2048 tokens)
+                if (fn0 < F) t0 = resolve_tie(hi, lo, fn0, tokens, beg, end);
+                if (fn1 < F) t1 = resolve_tie(hi, lo, fn1, tokens, beg, end);
+            } else if (len > 0) {
+                KeyMin k0{0xFFFFFFFFu, 0xFFFFFFFFu}, k1{0xFFFFFFFFu, 0xFFFFFFFFu};
+                for (int base = 0; base < len; base += 32) {
+                    const int cnt = len - base < 32 ? len - base : 32;
+                    const uint32_t mine = lane < cnt ? __ldg(tokens + beg + base + lane) : 0u;
+#pragma unroll 4
+                    for (int j = 0; j < cnt; ++j) {
+                        const uint32_t tok = __shfl_sync(0xffffffffu, mine, j);
+                        const uint2 h = key_pair<L>(tok, lane_base);
+                        const uint32_t p = (uint32_t)(base + j);
+                        key_update(k0, h.x | p);
+                        key_update(k1, h.y | p);
+                    }
+                }
+                if ((k0.m1 >> KEY_BITS) == (k0.m2 >> KEY_BITS) && fn0 < F)
+                    t0 = resolve_tie(hi, lo, fn0, tokens, beg, end);
+                else
+                    t0 = __ldg(tokens + beg + (k0.m1 & KEY_MASK));
+                if ((k1.m1 >> KEY_BITS) == (k1.m2 >> KEY_BITS) && fn1 < F)
+                    t1 = resolve_tie(hi, lo, fn1, tokens, beg, end);
+                else
+                    t1 = __ldg(tokens + beg + (k1.m1 & KEY_MASK));
+            }
+            if (values != nullptr) {
+                if (fn0 < F) values[s * F + fn0] = t0;
+                if (fn1 < F) values[s * F + fn1] = t1;
+            }
+            if (sketch != nullptr) {
+                const uint32_t w0 = __ballot_sync(0xffffffffu, len > 0 && fn0 < F && sketch_bit(bitmask, fn0, t0));
+                const uint32_t w1 = __ballot_sync(0xffffffffu, len > 0 && fn1 < F && sketch_bit(bitmask, fn1, t1));
+                if (lane == 0) sketch[s * words + c] = ((uint64_t)w1 << 32) | w0;
+            }
+        }
+    }
+}
+
+template <int L>
+static void launch_minhash_keyed(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
+                                 int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
+    const int smem = L * 256 * 32 * 8;
+    CPSJ_CUDA(cudaFuncSetAttribute(k_minhash_keyed<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
+    ProfScope prof(ctx, PROF_K1, stream);
+    k_minhash_keyed<L><<<grid, K1W_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask,
+                                                            fam->F, values, sketch);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
+template <int L>
+static void launch_minhash64(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
+                             int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
+    const int smem = L * 256 * 32 * 8;
+    CPSJ_CUDA(cudaFuncSetAttribute(k_minhash64<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
+    ProfScope prof(ctx, PROF_K1, stream);
+    k_minhash64<L><<<grid, K1W_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask,
+                                                        fam->F, values, sketch);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
 // family preparation: split u64 tables into hi/lo words and pack the low
 // bits of the bit tables into 256-bit masks per (function, byte table)
 __global__ void k_prepare_family(const uint64_t *__restrict__ mh, const uint64_t *__restrict__ bt,
@@ -181,10 +470,28 @@ int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_toke
     if (n == 0 || (d_values == nullptr && d_sketch == nullptr)) return 0;
     const int L = max_token < (1u << 8) ? 1 : max_token < (1u << 16) ? 2 : max_token < (1u << 24) ? 3 : 4;
     uint32_t *sk32 = reinterpret_cast<uint32_t *>(d_sketch);
+    const char *force32 = getenv("CPSJ_K1_NARROW");  // A/B switch for the 32-function kernel
+    if (force32 != nullptr && force32[0] == '1' && L < 4) {
+        switch (L) {
+            case 1: launch_minhash<1>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
+            case 2: launch_minhash<2>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
+            default: launch_minhash<3>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
+        }
+        return 0;
+    }
+    const char *flagged = getenv("CPSJ_K1_FLAGGED");  // A/B switch for the flag-based 64-function kernel
+    if (flagged != nullptr && flagged[0] == '1' && L < 4) {
+        switch (L) {
+            case 1: launch_minhash64<1>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+            case 2: launch_minhash64<2>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+            default: launch_minhash64<3>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+        }
+        return 0;
+    }
     switch (L) {
-        case 1: launch_minhash<1>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
-        case 2: launch_minhash<2>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
-        case 3: launch_minhash<3>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
+        case 1: launch_minhash_keyed<1>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+        case 2: launch_minhash_keyed<2>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+        case 3: launch_minhash_keyed<3>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
         default: launch_minhash<4>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
     }
     return 0;
