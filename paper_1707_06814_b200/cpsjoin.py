@@ -145,7 +145,7 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinA
     a = (keys >> np.uint64(32)).astype(np.int64)
     b = (keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
     src = emb.source_ids
-    if src is not None and not (len(src) == n and np.array_equal(src, np.arange(n))):
+    if src is not None and not emb.ids_are_rows():
         # map rows to source ids, re-orient and re-dedup (cpsjoin.py:313-318)
         ia, ib = np.asarray(src)[a], np.asarray(src)[b]
         lo, hi = np.minimum(ia, ib).astype(np.uint64), np.maximum(ia, ib).astype(np.uint64)

@@ -56,8 +56,10 @@ inline unsigned blocks_for(int64_t n, int tpb = TPB) {
 
 // per node: leaf tiles (32x32 upper-triangle tiles of the pair space),
 // internal flag + member count; leaf pre-candidates m(m-1)/2 (cps:144)
+// Leaves of <= 32 members go to the pair-packed kernel (one thread per
+// pair), larger leaves to the tile kernel.
 __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit,
-                       int64_t *__restrict__ tiles, int64_t *__restrict__ internal,
+                       int64_t *__restrict__ tiles, int64_t *__restrict__ spairs, int64_t *__restrict__ internal,
                        int64_t *__restrict__ imem, DevCounters *ctr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long pre = 0;
@@ -65,12 +67,15 @@ __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit
         const int64_t m = cnt[i];
         const bool leaf = m <= limit;
         const int64_t T = (m + 31) / 32;
-        tiles[i] = leaf ? T * (T + 1) / 2 : 0;
+        const int64_t pairs = m * (m - 1) / 2;
+        tiles[i] = (leaf && m > 32) ? T * (T + 1) / 2 : 0;
+        spairs[i] = (leaf && m <= 32) ? pairs : 0;
         internal[i] = leaf ? 0 : 1;
         imem[i] = leaf ? 0 : m;
-        if (leaf) pre = (unsigned long long)(m * (m - 1) / 2);
+        if (leaf) pre = (unsigned long long)pairs;
     } else if (i == N) {
         tiles[i] = 0;
+        spairs[i] = 0;
         internal[i] = 0;
         imem[i] = 0;
     }
@@ -129,15 +134,24 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
     for (int i = bi << 5; i < iend; ++i) {
         const int32_t row = mem[i];
         const uint64_t *rs = sketch + (size_t)row * ell;
+        const bool active = jvalid && j > i;
         int dist = 0;
-        if (ELL > 0) {
+        if (ELL >= 8) {
+            // the distance only grows word by word: once no lane of the warp
+            // can still pass after half the words, the row is done
+#pragma unroll
+            for (int k = 0; k < EL / 2; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+            if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
+#pragma unroll
+            for (int k = EL / 2; k < EL; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+        } else if (ELL > 0) {
 #pragma unroll
             for (int k = 0; k < EL; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
         } else {
             const uint64_t *csp = sketch + (size_t)col * ell;
             for (int k = 0; k < ell; ++k) dist += __popcll(__ldg(rs + k) ^ (jvalid ? __ldg(csp + k) : 0));
         }
-        bool pass = jvalid && j > i && dist <= accept;
+        bool pass = active && dist <= accept;
         if (pass) pass = size_filter(sizes[row], col_size, lam);
         const unsigned mask = __ballot_sync(0xffffffffu, pass);
         if (mask) {
@@ -148,6 +162,60 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
                 const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1));
                 if (slot < cap) cand[slot] = make_int2(row, col);
             }
+        }
+    }
+}
+
+// Pair-packed BruteForce for leaves of <= 32 members: thread per pair
+// (i < j in member order), so tiny leaves do not waste a 32x32 tile.  A warp
+// covers 32 consecutive pairs; lane 0 finds the first pair's leaf by binary
+// search and every lane walks forward over the (short) leaves it spans.
+template <int ELL>
+__global__ void __launch_bounds__(TPB) k_leaf_pairs(
+    int64_t total_pairs, const int64_t *__restrict__ pair_off, int64_t N,
+    const int64_t *__restrict__ nd_off, const int32_t *__restrict__ nd_cnt,
+    const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch, int ell_rt,
+    const int32_t *__restrict__ sizes, int32_t accept, double lam, int2 *__restrict__ cand,
+    unsigned long long cap, DevCounters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t wbase = p - lane;
+    if (wbase >= total_pairs) return;
+    int64_t node = 0;
+    if (lane == 0) node = upper_bound_i64(pair_off, N + 1, wbase) - 1;
+    node = __shfl_sync(0xffffffffu, node, 0);
+    const bool valid = p < total_pairs;
+    bool pass = false;
+    int32_t a = 0, b = 0;
+    if (valid) {
+        while (pair_off[node + 1] <= p) ++node;
+        int64_t q = p - pair_off[node];
+        const int m = nd_cnt[node];
+        int i = 0, rowlen = m - 1;
+        while (q >= rowlen) { q -= rowlen; ++i; --rowlen; }
+        const int j = i + 1 + (int)q;
+        const int32_t *mem = members + nd_off[node];
+        a = mem[i];
+        b = mem[j];
+        const int ell = ELL > 0 ? ELL : ell_rt;
+        const uint64_t *sa = sketch + (size_t)a * ell, *sb = sketch + (size_t)b * ell;
+        int dist = 0;
+        if (ELL > 0) {
+#pragma unroll
+            for (int k = 0; k < (ELL > 0 ? ELL : 1); ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
+        } else {
+            for (int k = 0; k < ell; ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
+        }
+        pass = dist <= accept && size_filter(sizes[a], sizes[b], lam);
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, pass);
+    if (mask) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&ctr->cand_n, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (pass) {
+            const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1));
+            if (slot < cap) cand[slot] = make_int2(a, b);
         }
     }
 }
@@ -349,14 +417,18 @@ __global__ void k_group_start(int64_t E, const int64_t *__restrict__ head, const
 }
 
 // groups of >= 2 members become children (cps:242-244)
-__global__ void k_group_keep(int64_t G, int64_t E, const int64_t *__restrict__ gstart,
+// (G = number of groups is read on the device: hscan[E]; the grid covers
+// the upper bound E + 1 so the host never waits for G)
+__global__ void k_group_keep(const int64_t *__restrict__ Gp, int64_t E, const int64_t *__restrict__ gstart,
                              int64_t *__restrict__ keep, int64_t *__restrict__ ksize) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t G = *Gp;
+    if (g > E) return;
     if (g < G) {
         const int64_t sz = (g + 1 < G ? gstart[g + 1] : E) - gstart[g];
         keep[g] = sz >= 2;
         ksize[g] = sz >= 2 ? sz : 0;
-    } else if (g == G) {
+    } else {
         keep[g] = 0;
         ksize[g] = 0;
     }
@@ -364,7 +436,7 @@ __global__ void k_group_keep(int64_t G, int64_t E, const int64_t *__restrict__ g
 
 // child node records: seed = word(parent seed, t + 64 ell + j) for the
 // parent's j-th child (cps:286,301); S for the DFS-peak replay
-__global__ void k_children(int64_t G, int64_t E, const int64_t *__restrict__ gstart,
+__global__ void k_children(const int64_t *__restrict__ Gp, int64_t E, const int64_t *__restrict__ gstart,
                            const int64_t *__restrict__ keep, const int64_t *__restrict__ kscan,
                            const int64_t *__restrict__ mscan, const int64_t *__restrict__ hscan,
                            const uint64_t *__restrict__ keys, const int64_t *__restrict__ seg_off,
@@ -374,6 +446,7 @@ __global__ void k_children(int64_t G, int64_t E, const int64_t *__restrict__ gst
                            int64_t *__restrict__ c_off, int32_t *__restrict__ c_cnt,
                            uint64_t *__restrict__ c_seed, int64_t *__restrict__ c_S, DevCounters *ctr) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t G = *Gp;
     long long cand_peak = 0;
     if (g < G && keep[g]) {
         const int64_t st = gstart[g];
@@ -454,6 +527,15 @@ __global__ void k_fill_roots(int64_t n, int32_t R, int32_t *__restrict__ members
     if (e < n * R) members[e] = (int32_t)(e % n);
 }
 
+struct Gather8 {
+    const int64_t *p[8];
+};
+
+__global__ void k_gather8(Gather8 g, int cnt, int64_t *__restrict__ out) {
+    const int i = threadIdx.x;
+    if (i < cnt) out[i] = *g.p[i];
+}
+
 __global__ void k_gather_scalars(const int64_t *__restrict__ a, int64_t ia, const int64_t *__restrict__ b,
                                  int64_t ib, const int64_t *__restrict__ c, int64_t ic, int64_t *__restrict__ out) {
     if (threadIdx.x == 0) {
@@ -487,6 +569,16 @@ struct Driver {
         ctx->lib_calls++;
     }
 
+    // read up to eight device scalars with one synchronisation
+    void gather(Gather8 g, int cnt, int64_t *dscal, int64_t *out) {
+        k_gather8<<<1, 32, 0, st>>>(g, cnt, dscal);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+        CPSJ_CUDA(cudaMemcpyAsync(ctx->h_scalars, dscal, cnt * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        for (int i = 0; i < cnt; ++i) out[i] = ctx->h_scalars[i];
+    }
+
     // read up to three device scalars with one synchronisation
     void read3(const int64_t *a, int64_t ia, const int64_t *b, int64_t ib, const int64_t *c, int64_t ic,
                int64_t *dscal, int64_t out[3]) {
@@ -501,29 +593,42 @@ struct Driver {
     }
 };
 
+struct LeafWork {
+    int64_t tiles = 0;            // 32x32 tiles of leaves with m > 32
+    const int64_t *tile_off = nullptr;
+    int64_t pairs = 0;            // pairs of leaves with m <= 32 (pair-packed)
+    const int64_t *pair_off = nullptr;
+};
+
 template <int ELL>
-void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, int64_t tiles, const int64_t *tile_off, const Level &lv,
-                 const cpsj_inputs *in, int32_t accept, double lam, int2 *cand, unsigned long long cap,
-                 DevCounters *ctr) {
-    const int64_t threads = tiles * 32;
+void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level &lv, const cpsj_inputs *in,
+                 int32_t accept, double lam, int2 *cand, unsigned long long cap, DevCounters *ctr) {
     ProfScope prof(ctx, PROF_LEAF, st);
-    k_leaf_tiles<ELL><<<blocks_for(threads), TPB, 0, st>>>(tiles, tile_off, lv.N, lv.off.p, lv.cnt.p, lv.members.p,
-                                                           in->d_sketch, in->ell, in->d_sizes, accept, lam, cand,
-                                                           cap, ctr);
-    CPSJ_LAUNCH_CHECK();
-    ctx->launches++;
+    if (wk.tiles > 0) {
+        k_leaf_tiles<ELL><<<blocks_for(wk.tiles * 32), TPB, 0, st>>>(wk.tiles, wk.tile_off, lv.N, lv.off.p,
+                                                                     lv.cnt.p, lv.members.p, in->d_sketch, in->ell,
+                                                                     in->d_sizes, accept, lam, cand, cap, ctr);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+    }
+    if (wk.pairs > 0) {
+        k_leaf_pairs<ELL><<<blocks_for(wk.pairs), TPB, 0, st>>>(wk.pairs, wk.pair_off, lv.N, lv.off.p, lv.cnt.p,
+                                                                lv.members.p, in->d_sketch, in->ell, in->d_sizes,
+                                                                accept, lam, cand, cap, ctr);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+    }
 }
 
-void leaf_dispatch(cpsj_ctx *ctx, cudaStream_t st, int64_t tiles, const int64_t *tile_off, const Level &lv,
-                   const cpsj_inputs *in, int32_t accept, double lam, int2 *cand, unsigned long long cap,
-                   DevCounters *ctr) {
+void leaf_dispatch(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level &lv, const cpsj_inputs *in,
+                   int32_t accept, double lam, int2 *cand, unsigned long long cap, DevCounters *ctr) {
     switch (in->ell) {
-        case 1: launch_leaf<1>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
-        case 2: launch_leaf<2>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
-        case 4: launch_leaf<4>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
-        case 8: launch_leaf<8>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
-        case 16: launch_leaf<16>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
-        default: launch_leaf<0>(ctx, st, tiles, tile_off, lv, in, accept, lam, cand, cap, ctr); break;
+        case 1: launch_leaf<1>(ctx, st, wk, lv, in, accept, lam, cand, cap, ctr); break;
+        case 2: launch_leaf<2>(ctx, st, wk, lv, in, accept, lam, cand, cap, ctr); break;
+        case 4: launch_leaf<4>(ctx, st, wk, lv, in, accept, lam, cand, cap, ctr); break;
+        case 8: launch_leaf<8>(ctx, st, wk, lv, in, accept, lam, cand, cap, ctr); break;
+        case 16: launch_leaf<16>(ctx, st, wk, lv, in, accept, lam, cand, cap, ctr); break;
+        default: launch_leaf<0>(ctx, st, wk, lv, in, accept, lam, cand, cap, ctr); break;
     }
 }
 
@@ -545,7 +650,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
 
     Driver drv{ctx, st};
     DevBuf<DevCounters> ctr(1, st);
-    DevBuf<int64_t> dscal(4, st);
+    DevBuf<int64_t> dscal(8, st);
     CPSJ_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(DevCounters), st));
     {
         DevCounters init{};
@@ -586,12 +691,10 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     const uint64_t child_off = (uint64_t)t + 64ull * (uint64_t)ell;
     unsigned long long res_bound = 0;  // host upper bound of result slots used
 
-    // K5 on the candidates emitted since the last flush; `regen` re-emits
-    // them into a larger buffer if the first pass overflowed
-    auto flush = [&](auto &&regen) {
-        unsigned long long nc = 0;
-        CPSJ_CUDA(cudaMemcpyAsync(&nc, &ctr.p->cand_n, sizeof(nc), cudaMemcpyDeviceToHost, st));
-        CPSJ_CUDA(cudaStreamSynchronize(st));
+    // K5 on `nc` candidates emitted since the last reset; `regen` re-emits
+    // them into a larger buffer when the first pass overflowed
+    auto verify_batch = [&](int64_t nc_in, auto &&regen) {
+        unsigned long long nc = (unsigned long long)nc_in;
         if (nc > cand_cap) {
             cand_cap = nc + nc / 4 + 1024;
             cand.alloc(cand_cap, st);
@@ -617,99 +720,85 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cand_n, 0, sizeof(unsigned long long), st));
     };
 
+    // Three host synchronisations per level: (A) leaf/internal totals,
+    // (B) candidate count + flag/entry totals, (C) child totals.  Every
+    // other size is an upper bound known on the host or read on the device.
     for (int depth = 0; lv.N > 0; ++depth) {
         levels++;
         max_depth = depth;
         const int64_t N = lv.N;
-        // ---- plan: leaves vs internal nodes
+        // ---- (A) plan: leaves vs internal nodes
         std::unique_ptr<ProfScope> prof_plan(new ProfScope(ctx, PROF_PLAN, st));
-        DevBuf<int64_t> tiles(N + 1, st), internal(N + 1, st), imem(N + 1, st);
-        DevBuf<int64_t> tile_off(N + 1, st), iscan(N + 1, st), im_off(N + 1, st);
-        k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, internal.p, imem.p, ctr.p);
+        DevBuf<int64_t> tiles(N + 1, st), spairs(N + 1, st), internal(N + 1, st), imem(N + 1, st);
+        DevBuf<int64_t> tile_off(N + 1, st), pair_off(N + 1, st), iscan(N + 1, st), im_off(N + 1, st);
+        k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, spairs.p, internal.p, imem.p,
+                                                  ctr.p);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
         drv.scan(tiles.p, tile_off.p, N + 1);
+        drv.scan(spairs.p, pair_off.p, N + 1);
         drv.scan(internal.p, iscan.p, N + 1);
         drv.scan(imem.p, im_off.p, N + 1);
-        int64_t sc[3];
-        drv.read3(tile_off.p, N, iscan.p, N, im_off.p, N, dscal.p, sc);
-        const int64_t total_tiles = sc[0], n_int = sc[1], Mi = sc[2];
-        CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cand_n, 0, sizeof(unsigned long long), st));
+        int64_t sc[8];
+        drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, pair_off.p + N}}, 4, dscal.p, sc);
+        LeafWork work;
+        work.tiles = sc[0];
+        work.tile_off = tile_off.p;
+        work.pairs = sc[3];
+        work.pair_off = pair_off.p;
+        const int64_t n_int = sc[1], Mi = sc[2];
         prof_plan.reset();
 
-        // ---- leaves: K4, then K5 on their candidates
-        if (total_tiles > 0) {
-            auto gen = [&]() {
-                leaf_dispatch(ctx, st, total_tiles, tile_off.p, lv, in, plan->accept_dist, lam, cand.p, cand_cap,
-                              ctr.p);
-            };
-            gen();
-            flush(gen);
-        }
+        // ---- leaves: K4 (candidates verified after sync B)
+        auto gen_leaf = [&]() {
+            if (work.tiles > 0 || work.pairs > 0)
+                leaf_dispatch(ctx, st, work, lv, in, plan->accept_dist, lam, cand.p, cand_cap, ctr.p);
+        };
+        gen_leaf();
 
-        // ---- internal nodes: K2 (+ point comparisons), K3
         Level nx;
+        // internal-node state that lives until the end of the level
+        DevBuf<int64_t> ilist, im_off_c, flags, fscan, nsel, nent, seg_off, e_off, capsz;
+        DevBuf<uint64_t> nsk;
+        DevBuf<int32_t> surv;
+        DevBuf<int16_t> sel_pos;
         if (n_int > 0) {
-            DevBuf<int64_t> ilist(n_int, st), im_off_c(n_int + 1, st);
+            std::unique_ptr<ProfScope> prof_node(new ProfScope(ctx, PROF_NODE, st));
+            ilist.alloc(n_int, st);
+            im_off_c.alloc(n_int + 1, st);
             k_compact_internal<<<blocks_for(N), TPB, 0, st>>>(N, internal.p, iscan.p, ilist.p);
             CPSJ_LAUNCH_CHECK();
-            ctx->launches++;
-            // member offsets of the internal nodes, compacted
             {
                 DevBuf<int64_t> icnt(n_int + 1, st);
                 k_gather_counts<<<blocks_for(n_int + 1), TPB, 0, st>>>(n_int, ilist.p, lv.cnt.p, icnt.p);
                 CPSJ_LAUNCH_CHECK();
-                ctx->launches++;
                 drv.scan(icnt.p, im_off_c.p, n_int + 1);
             }
-            DevBuf<uint64_t> nsk(n_int * ell, st);
-            std::unique_ptr<ProfScope> prof_node(new ProfScope(ctx, PROF_NODE, st));
+            nsk.alloc(n_int * ell, st);
             k_node_sketch<<<(unsigned)n_int, TPB, 0, st>>>(ilist.p, lv.off.p, lv.cnt.p, lv.seed.p, lv.members.p,
                                                            in->d_sketch, ell, t,
                                                            reinterpret_cast<uint32_t *>(nsk.p), ctr.p);
             CPSJ_LAUNCH_CHECK();
-            ctx->launches++;
-            DevBuf<int64_t> flags(Mi + 1, st), fscan(Mi + 1, st);
+            flags.alloc(Mi + 1, st);
+            fscan.alloc(Mi + 1, st);
             k_flags<<<blocks_for(Mi + 1), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p, lv.members.p,
                                                         in->d_sketch, ell, nsk.p, plan->flag_dist, flags.p);
             CPSJ_LAUNCH_CHECK();
-            ctx->launches++;
             drv.scan(flags.p, fscan.p, Mi + 1);
-            drv.read3(fscan.p, Mi, nullptr, 0, nullptr, 0, dscal.p, sc);
-            const int64_t n_flag = sc[0];
+            surv.alloc(std::max<int64_t>(1, Mi), st);
+            k_survivors<<<blocks_for(Mi), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p, lv.members.p,
+                                                        flags.p, fscan.p, surv.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 5;
             prof_node.reset();
-            if (n_flag > 0) {
-                DevBuf<int64_t> flist(n_flag, st);
-                k_flag_list<<<blocks_for(Mi), TPB, 0, st>>>(Mi, flags.p, fscan.p, flist.p);
-                CPSJ_LAUNCH_CHECK();
-                ctx->launches++;
-                int count_pre = 1;
-                auto gen = [&]() {
-                    ProfScope prof(ctx, PROF_POINT, st);
-                    k_point<<<blocks_for(n_flag * 32), TPB, 0, st>>>(
-                        n_flag, flist.p, fscan.p, flags.p, im_off_c.p, n_int, ilist.p, lv.off.p, lv.cnt.p,
-                        lv.members.p, in->d_sketch, ell, in->d_sizes, plan->accept_dist, lam, cand.p, cand_cap,
-                        count_pre, ctr.p);
-                    CPSJ_LAUNCH_CHECK();
-                    ctx->launches++;
-                    count_pre = 0;  // a regeneration must not count twice
-                };
-                gen();
-                flush(gen);
-            }
-            DevBuf<int32_t> surv(std::max<int64_t>(1, Mi - n_flag), st);
-            {
-                ProfScope prof(ctx, PROF_NODE, st);
-                k_survivors<<<blocks_for(Mi), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p,
-                                                            lv.members.p, flags.p, fscan.p, surv.p);
-                CPSJ_LAUNCH_CHECK();
-                ctx->launches++;
-            }
-            // ---- split
+            // ---- split, part 1: selected positions and entry counts
             ProfScope prof_split(ctx, PROF_SPLIT, st);
-            DevBuf<int16_t> sel_pos(n_int * t, st);
-            DevBuf<int64_t> nsel(n_int + 1, st), nent(n_int + 1, st), seg_off(n_int + 1, st), e_off(n_int + 1, st);
-            DevBuf<int64_t> capsz(n_int, st);
+            sel_pos.alloc(n_int * t, st);
+            nsel.alloc(n_int + 1, st);
+            nent.alloc(n_int + 1, st);
+            seg_off.alloc(n_int + 1, st);
+            e_off.alloc(n_int + 1, st);
+            capsz.alloc(n_int, st);
             CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cap_n, 0, sizeof(unsigned long long), st));
             k_select<<<blocks_for((n_int + 1) * 32), TPB, 0, st>>>(
                 n_int, ilist.p, lv.cnt.p, lv.seed.p, depth, plan->depth_cap, im_off_c.p, fscan.p, t, plan->split_p,
@@ -718,74 +807,114 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             ctx->launches++;
             drv.scan(nsel.p, seg_off.p, n_int + 1);
             drv.scan(nent.p, e_off.p, n_int + 1);
-            drv.read3(e_off.p, n_int, seg_off.p, n_int, nullptr, 0, dscal.p, sc);
-            const int64_t E = sc[0], n_seg = sc[1];
-            {
-                unsigned long long ncap = 0;
-                CPSJ_CUDA(cudaMemcpyAsync(&ncap, &ctr.p->cap_n, sizeof(ncap), cudaMemcpyDeviceToHost, st));
-                CPSJ_CUDA(cudaStreamSynchronize(st));
-                if (ncap) {
-                    std::vector<int64_t> h(ncap);
-                    CPSJ_CUDA(cudaMemcpyAsync(h.data(), capsz.p, ncap * 8, cudaMemcpyDeviceToHost, st));
-                    CPSJ_CUDA(cudaStreamSynchronize(st));
-                    ctx->cap_events.insert(ctx->cap_events.end(), h.begin(), h.end());
-                }
-            }
-            if (E > 0) {
-                DevBuf<uint64_t> keys(E, st), keys2(E, st);
-                DevBuf<int32_t> vals(E, st), vals2(E, st);
-                k_build_keys<<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p, im_off_c.p,
-                                                            fscan.p, sel_pos.p, t, surv.p, in->d_values, keys.p,
-                                                            vals.p);
-                CPSJ_LAUNCH_CHECK();
-                ctx->launches++;
-                int end_bit = 32;
-                while (end_bit < 64 && ((uint64_t)n_seg >> (end_bit - 32)) > 0) ++end_bit;
-                size_t bytes = 0;
-                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0,
-                                                          end_bit, st));
-                if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
-                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
-                                                          0, end_bit, st));
-                ctx->lib_calls++;
-                DevBuf<int64_t> head(E + 1, st), hscan(E + 1, st);
-                k_heads<<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
-                CPSJ_LAUNCH_CHECK();
-                ctx->launches++;
-                drv.scan(head.p, hscan.p, E + 1);
-                drv.read3(hscan.p, E, nullptr, 0, nullptr, 0, dscal.p, sc);
-                const int64_t G = sc[0];
-                DevBuf<int64_t> gstart(G, st), keep(G + 1, st), ksize(G + 1, st), kscan(G + 1, st),
-                    mscan(G + 1, st);
-                k_group_start<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p);
-                CPSJ_LAUNCH_CHECK();
-                k_group_keep<<<blocks_for(G + 1), TPB, 0, st>>>(G, E, gstart.p, keep.p, ksize.p);
-                CPSJ_LAUNCH_CHECK();
-                ctx->launches += 2;
-                drv.scan(keep.p, kscan.p, G + 1);
-                drv.scan(ksize.p, mscan.p, G + 1);
-                drv.read3(kscan.p, G, mscan.p, G, nullptr, 0, dscal.p, sc);
-                nx.N = sc[0];
-                nx.M = sc[1];
-                if (nx.N > 0) {
-                    nx.off.alloc(nx.N, st);
-                    nx.cnt.alloc(nx.N, st);
-                    nx.seed.alloc(nx.N, st);
-                    nx.S.alloc(nx.N, st);
-                    nx.members.alloc(nx.M, st);
-                    k_children<<<blocks_for(G), TPB, 0, st>>>(G, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p,
-                                                              keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p,
-                                                              lv.S.p, child_off, nx.off.p, nx.cnt.p, nx.seed.p,
-                                                              nx.S.p, ctr.p);
-                    CPSJ_LAUNCH_CHECK();
-                    k_scatter_children<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p, keep.p,
-                                                                      mscan.p, vals2.p, nx.members.p);
-                    CPSJ_LAUNCH_CHECK();
-                    ctx->launches += 2;
-                }
-            }
+        }
+        // ---- (B) one read: leaf candidates, flags, split entries, depth caps
+        {
+            const int64_t *cand_n = reinterpret_cast<const int64_t *>(&ctr.p->cand_n);
+            const int64_t *cap_n = reinterpret_cast<const int64_t *>(&ctr.p->cap_n);
+            if (n_int > 0)
+                drv.gather({{cand_n, fscan.p + Mi, e_off.p + n_int, seg_off.p + n_int, cap_n}}, 5, dscal.p, sc);
+            else
+                drv.gather({{cand_n}}, 1, dscal.p, sc);
+        }
+        const int64_t n_leaf_cand = sc[0];
+        const int64_t n_flag = n_int > 0 ? sc[1] : 0, E = n_int > 0 ? sc[2] : 0, n_seg = n_int > 0 ? sc[3] : 0;
+        const int64_t ncap = n_int > 0 ? sc[4] : 0;
+        if (ncap) {
+            std::vector<int64_t> h(ncap);
+            CPSJ_CUDA(cudaMemcpyAsync(h.data(), capsz.p, ncap * 8, cudaMemcpyDeviceToHost, st));
+            CPSJ_CUDA(cudaStreamSynchronize(st));
+            ctx->cap_events.insert(ctx->cap_events.end(), h.begin(), h.end());
+        }
+        verify_batch(n_leaf_cand, gen_leaf);
+
+        // ---- point comparisons of flagged members (K2)
+        DevBuf<int64_t> flist;
+        int count_pre = 1;
+        auto gen_point = [&]() {
+            ProfScope prof(ctx, PROF_POINT, st);
+            k_point<<<blocks_for(n_flag * 32), TPB, 0, st>>>(
+                n_flag, flist.p, fscan.p, flags.p, im_off_c.p, n_int, ilist.p, lv.off.p, lv.cnt.p, lv.members.p,
+                in->d_sketch, ell, in->d_sizes, plan->accept_dist, lam, cand.p, cand_cap, count_pre, ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            count_pre = 0;  // a regeneration must not count twice
+        };
+        if (n_flag > 0) {
+            flist.alloc(n_flag, st);
+            k_flag_list<<<blocks_for(Mi), TPB, 0, st>>>(Mi, flags.p, fscan.p, flist.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            gen_point();
         }
 
+        // ---- split, part 2: stable group-by (K3)
+        DevBuf<uint64_t> keys, keys2;
+        DevBuf<int32_t> vals, vals2;
+        DevBuf<int64_t> head, hscan, gstart, keep, ksize, kscan, mscan;
+        if (E > 0) {
+            ProfScope prof_split(ctx, PROF_SPLIT, st);
+            keys.alloc(E, st);
+            keys2.alloc(E, st);
+            vals.alloc(E, st);
+            vals2.alloc(E, st);
+            k_build_keys<<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p, im_off_c.p, fscan.p,
+                                                        sel_pos.p, t, surv.p, in->d_values, keys.p, vals.p);
+            CPSJ_LAUNCH_CHECK();
+            int end_bit = 32;
+            while (end_bit < 64 && ((uint64_t)n_seg >> (end_bit - 32)) > 0) ++end_bit;
+            size_t bytes = 0;
+            CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0, end_bit,
+                                                      st));
+            if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+            CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0,
+                                                      end_bit, st));
+            ctx->lib_calls++;
+            head.alloc(E + 1, st);
+            hscan.alloc(E + 1, st);
+            k_heads<<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
+            CPSJ_LAUNCH_CHECK();
+            drv.scan(head.p, hscan.p, E + 1);
+            gstart.alloc(E, st);
+            keep.alloc(E + 1, st);
+            ksize.alloc(E + 1, st);
+            kscan.alloc(E + 1, st);
+            mscan.alloc(E + 1, st);
+            k_group_start<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p);
+            CPSJ_LAUNCH_CHECK();
+            k_group_keep<<<blocks_for(E + 1), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, ksize.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 4;
+            drv.scan(keep.p, kscan.p, E + 1);
+            drv.scan(ksize.p, mscan.p, E + 1);
+        }
+        // ---- (C) one read: point candidates, children totals
+        {
+            const int64_t *cand_n = reinterpret_cast<const int64_t *>(&ctr.p->cand_n);
+            if (E > 0)
+                drv.gather({{cand_n, kscan.p + E, mscan.p + E}}, 3, dscal.p, sc);
+            else
+                drv.gather({{cand_n}}, 1, dscal.p, sc);
+        }
+        if (n_flag > 0) verify_batch(sc[0], gen_point);
+        nx.N = E > 0 ? sc[1] : 0;
+        nx.M = E > 0 ? sc[2] : 0;
+        if (nx.N > 0) {
+            ProfScope prof_split(ctx, PROF_SPLIT, st);
+            nx.off.alloc(nx.N, st);
+            nx.cnt.alloc(nx.N, st);
+            nx.seed.alloc(nx.N, st);
+            nx.S.alloc(nx.N, st);
+            nx.members.alloc(nx.M, st);
+            k_children<<<blocks_for(E), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p,
+                                                      keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p, lv.S.p,
+                                                      child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            k_scatter_children<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p, keep.p, mscan.p, vals2.p,
+                                                              nx.members.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 2;
+        }
         lv = std::move(nx);
     }
 

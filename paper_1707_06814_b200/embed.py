@@ -84,6 +84,7 @@ class EmbeddedDataset:
         obj._dev["values"] = dev_values
         obj._dev["tokens"], obj._dev["offsets"] = dev_csr
         obj._n = len(offsets) - 1
+        obj._ids_checked, obj._ids_ok = (id(obj.source_ids), obj._n), True
         return obj
 
     def _csr_host(self):
@@ -107,6 +108,16 @@ class EmbeddedDataset:
             v = np.ascontiguousarray(self.values, dtype=np.uint32)
             self._dev["values"] = torch.from_numpy(v.view(np.int32)).to(dev, non_blocking=True)
         return self._dev["tokens"], self._dev["offsets"], self._dev["sizes"], self._dev["values"]
+
+    def ids_are_rows(self) -> bool:
+        """True when source_ids == arange(n) (checked once per array)."""
+        src = self.source_ids
+        key = (id(src), len(self))
+        if getattr(self, "_ids_checked", None) != key:
+            ok = src is None or (len(src) == len(self) and np.array_equal(src, np.arange(len(self))))
+            self._ids_checked = key
+            self._ids_ok = ok
+        return self._ids_ok
 
     # ------------------------------------------------------------ reference
     def __len__(self) -> int:
@@ -257,6 +268,7 @@ def embed_device_csr(params: EmbeddingParams, d_tokens, d_offsets, d: int, host_
     obj._dev.update(values=d_vals, tokens=d_tokens, offsets=d_offsets)
     obj._dev["sizes"] = (d_offsets[1:] - d_offsets[:-1]).to(torch.int32)
     obj._n = n
+    obj._ids_checked, obj._ids_ok = (id(obj.source_ids), n), True
     obj._sizes_fn = lambda: obj._dev["sizes"].cpu().numpy().astype(np.int64)
     return obj
 
