@@ -275,7 +275,7 @@ def run_ours(args, rank: int, world: int):
         return shard_reps(emb, params, rank, world)
 
     def step_e2e():
-        emb = embed_dataset(eparams, ds)
+        emb = embed_dataset(eparams, ds, sketch=(cfg.ell, cfg.join_seed))
         return shard_reps(emb, params, rank, world)
 
     def timed(fn, steps):

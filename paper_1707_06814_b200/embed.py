@@ -273,10 +273,24 @@ def embed_device_csr(params: EmbeddingParams, d_tokens, d_offsets, d: int, host_
     return obj
 
 
-def embed_dataset(params: EmbeddingParams, ds: Dataset) -> EmbeddedDataset:
+_PIPELINE_MIN_SETS = 1 << 16
+
+
+def embed_dataset(params: EmbeddingParams, ds: Dataset, sketch: tuple[int, int] | None = None,
+                  chunks: int | None = None) -> EmbeddedDataset:
     """Embed every record with the shared function family (embed.py:117-139)
-    on the GPU; the value matrix stays device-resident."""
+    on the GPU; the value matrix stays device-resident.
+
+    ``sketch=(ell, seed)`` additionally builds the sketch matrix that
+    ``cpsjoin_self(emb, CPSJoinParams(ell=ell, seed=seed))`` will ask for
+    (emb.sketches, embed.py:90-98) in the same pass.  Large inputs are
+    copied to the device in set-aligned chunks on a side stream while K1
+    hashes the chunks already resident (host->device copy overlapped with
+    compute; the copy source should be pinned memory for the overlap).
+    """
     n = len(ds)
+    if n > 0 and ((chunks is None and n >= _PIPELINE_MIN_SETS) or (chunks is not None and chunks > 1)):
+        return _embed_pipelined(params, ds, sketch, min(chunks or 8, n))
     t = params.t
     tok, off = ds.flat_tokens()
     tok = np.ascontiguousarray(tok, dtype=np.uint32)
@@ -301,3 +315,72 @@ def embed_dataset(params: EmbeddingParams, ds: Dataset) -> EmbeddedDataset:
     ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, fam.handle, d_tok.data_ptr(), d_off.data_ptr(), n,
                                           max_token, d_vals.data_ptr(), None, stream))
     return EmbeddedDataset._device_backed(d_vals, t, params.seed, tok, off, width, ds, (d_tok, d_off))
+
+
+def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) -> EmbeddedDataset:
+    torch = _torch()
+    from ._native import Context
+    n = len(ds)
+    t = params.t
+    tok, off = ds.flat_tokens()
+    tok = np.ascontiguousarray(tok, dtype=np.uint32)
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    if np.any(off[1:] == off[:-1]):
+        raise ValueError("cannot embed an empty record")
+    ctx = Context.get()
+    efam = params.device(ctx)
+    sfam = sketch_family(*sketch).device(ctx) if sketch is not None else None
+    dev = torch.device("cuda", ctx.device)
+    compute = torch.cuda.current_stream(dev)
+    copier = _copy_stream(dev)
+    width = int(getattr(ds, "d", 0) or 0)
+    max_token = min(width - 1, 0xFFFFFFFF) if width > 0 else 0xFFFFFFFF
+    src_tok = torch.from_numpy(tok.view(np.int32))
+    src_off = torch.from_numpy(off)
+    d_tok = torch.empty(len(tok), dtype=torch.int32, device=dev)
+    d_vals = torch.empty((n, t), dtype=torch.int32, device=dev)
+    d_sk = torch.empty((n, sketch[0]), dtype=torch.int64, device=dev) if sketch is not None else None
+    # set-aligned chunk boundaries
+    bounds = np.linspace(0, n, chunks + 1).astype(np.int64)
+    events = []
+    copier.wait_stream(compute)  # destination buffers were allocated on `compute`
+    with torch.cuda.stream(copier):
+        d_off = src_off.to(dev, non_blocking=True)
+        for c in range(chunks):
+            t0, t1 = int(off[bounds[c]]), int(off[bounds[c + 1]])
+            if t1 > t0:
+                d_tok[t0:t1].copy_(src_tok[t0:t1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copier)
+            events.append(ev)
+    h = compute.cuda_stream
+    for c in range(chunks):
+        s0, s1 = int(bounds[c]), int(bounds[c + 1])
+        compute.wait_event(events[c])
+        if s1 <= s0:
+            continue
+        offp = d_off.data_ptr() + 8 * s0
+        ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, efam.handle, d_tok.data_ptr(), offp, s1 - s0, max_token,
+                                              d_vals.data_ptr() + 4 * t * s0, None, h))
+        if sfam is not None:
+            ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, sfam.handle, d_tok.data_ptr(), offp, s1 - s0,
+                                                  max_token, None, d_sk.data_ptr() + 8 * sketch[0] * s0, h))
+    # the copier's work is consumed on `compute`; keep the buffers alive there
+    d_tok.record_stream(copier)
+    d_off.record_stream(compute)
+    emb = EmbeddedDataset._device_backed(d_vals, t, params.seed, tok, off, width, ds, (d_tok, d_off))
+    emb._dev["sizes"] = (d_off[1:] - d_off[:-1]).to(torch.int32)
+    if sketch is not None:
+        emb._dev_sketch[tuple(sketch)] = d_sk
+    return emb
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev):
+    torch = _torch()
+    s = _COPY_STREAMS.get(dev.index)
+    if s is None:
+        s = _COPY_STREAMS[dev.index] = torch.cuda.Stream(dev)
+    return s

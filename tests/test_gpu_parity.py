@@ -264,3 +264,18 @@ def test_full_config1_against_oracle_and_exact_truth():
     keys = (res.a.astype(np.uint64) << np.uint64(32)) | res.b.astype(np.uint64)
     assert np.isin(keys, truth).all()
     assert len(keys) >= 0.9 * len(truth)
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_pipelined_embed_with_sketch_hint_matches_oracle(chunks):
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    from paper_1707_06814_b200.workloads import generate
+    w = generate(1, scale=0.25)
+    ds = Dataset.from_csr(w.tokens, w.offsets, w.d)
+    emb = embed_dataset(EmbeddingParams(t=128, seed=7), ds, sketch=(8, 7), chunks=chunks)
+    values, sk, ref = O.full_pipeline(w.tokens, w.offsets, w.sizes, lam=0.5, emb_seed=7, seed=7, repetitions=2)
+    assert np.array_equal(emb.values, values)
+    assert np.array_equal(emb.sketches(8, 7), sk)
+    res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=0.5, seed=7, repetitions=2))
+    assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)

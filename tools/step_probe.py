@@ -36,7 +36,7 @@ for mode in ["device", "e2e", "device", "e2e"]:
         if mode == "device":
             emb = embed_device_csr(ep, d_tok, d_off, w.d)
         else:
-            emb = embed_dataset(ep, ds)
+            emb = embed_dataset(ep, ds, sketch=(cfg.ell, cfg.join_seed))
         t1 = sync_t()
         emb.sketches_device(cfg.ell, cfg.join_seed)
         t2 = sync_t()
