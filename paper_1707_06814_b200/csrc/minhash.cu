@@ -304,13 +304,40 @@ __device__ __forceinline__ uint2 key_pair(uint32_t tok, uint32_t lane_base) {
     return h;
 }
 
+// Tie detection without a second-minimum: `first` is the min over
+// (hash_part | p) and `last` the min over (hash_part | (MASK - p)).  Both
+// find the same minimal hash part; `first` carries the smallest position p
+// holding it and `last` the largest.  They agree iff exactly one token
+// attains the minimum, so a tie on the compared bits is
+// (first & MASK) != MASK - (last & MASK).  Two integer mins per evaluation
+// (ALU pipe) plus two adds issued as IMAD (FMA pipe).
 struct KeyMin {
-    uint32_t m1, m2;
+    uint32_t first, last;
 };
 
-__device__ __forceinline__ void key_update(KeyMin &k, uint32_t key) {
-    k.m2 = min(k.m2, max(k.m1, key));
-    k.m1 = min(k.m1, key);
+// a + b issued on the FMA pipe (IMAD), not the integer ALU pipe
+__device__ __forceinline__ uint32_t imad_add(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(1u), "r"(b));
+    return r;
+}
+
+__device__ __forceinline__ void key_update(KeyMin &k, uint32_t h, uint32_t p, uint32_t q) {
+    k.first = min(k.first, imad_add(h, p));
+    k.last = min(k.last, imad_add(h, q));
+}
+
+__device__ __forceinline__ bool key_tie(const KeyMin &k) {
+    return (k.first & KEY_MASK) != KEY_MASK - (k.last & KEY_MASK);
+}
+
+// sketch bit from the chunk's shared-memory copy of the bit-table low bits
+// (row stride 33 words spreads the 32 lanes over the banks)
+__device__ __forceinline__ uint32_t sketch_bit_s(const uint32_t *bm_s, int fl, uint32_t tok) {
+    const uint32_t *bm = bm_s + fl * 33;
+    const uint32_t b0 = tok & 255, b1 = (tok >> 8) & 255, b2 = (tok >> 16) & 255, b3 = tok >> 24;
+    return ((bm[b0 >> 5] >> (b0 & 31)) ^ (bm[8 + (b1 >> 5)] >> (b1 & 31)) ^ (bm[16 + (b2 >> 5)] >> (b2 & 31)) ^
+            (bm[24 + (b3 >> 5)] >> (b3 & 31))) & 1u;
 }
 
 template <int L>
@@ -319,13 +346,22 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_keyed(
     const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
     const uint32_t *__restrict__ bitmask, int F, uint32_t *__restrict__ values,
     uint64_t *__restrict__ sketch) {
-    extern __shared__ uint2 tab2[];  // [L][256][32] x {f = lane, f = lane + 32}
+    extern __shared__ uint2 tab2[];  // [L][256][32] x {f = lane, f = lane + 32}, then bit masks
+    // low bits of the chunk's bit tables: [64 functions][33 (4 x 8 + pad)] u32
+    uint32_t *bm_s = reinterpret_cast<uint32_t *>(tab2 + L * 256 * 32);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lane_base = (uint32_t)__cvta_generic_to_shared(tab2) + ((uint32_t)lane << 3);
     const int nchunks = (F + 63) >> 6;
     const int words = F >> 6;
+    const int64_t s_first = (int64_t)blockIdx.x * K1W_WARPS + warp, s_step = (int64_t)gridDim.x * K1W_WARPS;
     for (int c = 0; c < nchunks; ++c) {
         __syncthreads();
+        if (sketch != nullptr) {
+            for (int e = threadIdx.x; e < 64 * 32; e += K1W_THREADS) {
+                const int fl = e >> 5, w = e & 31, fn = (c << 6) + fl;
+                bm_s[fl * 33 + w] = fn < F ? bitmask[(size_t)fn * 32 + w] : 0u;
+            }
+        }
         for (int e = threadIdx.x; e < L * 256 * 32; e += K1W_THREADS) {
             const int k = e >> 13, b = (e >> 5) & 255, ln = e & 31;
             uint2 v = make_uint2(0u, 0u);
@@ -348,8 +384,19 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_keyed(
         }
         __syncthreads();
         const int fn0 = (c << 6) + lane, fn1 = fn0 + 32;
-        for (int64_t s = (int64_t)blockIdx.x * K1W_WARPS + warp; s < n; s += (int64_t)gridDim.x * K1W_WARPS) {
-            const int64_t beg = offsets[s], end = offsets[s + 1];
+        // software-pipelined set loop: the next set's offsets are in flight
+        // while the current set is hashed
+        int64_t nbeg = 0, nend = 0;
+        if (s_first < n) {
+            nbeg = offsets[s_first];
+            nend = offsets[s_first + 1];
+        }
+        for (int64_t s = s_first; s < n; s += s_step) {
+            const int64_t beg = nbeg, end = nend;
+            if (s + s_step < n) {
+                nbeg = offsets[s + s_step];
+                nend = offsets[s + s_step + 1];
+            }
             const int len = (int)(end - beg);
             uint32_t t0 = 0, t1 = 0;
             if (len > (int)KEY_MASK + 1) {
@@ -366,27 +413,32 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_keyed(
                     for (int j = 0; j < cnt; ++j) {
                         const uint32_t tok = __shfl_sync(0xffffffffu, mine, j);
                         const uint2 h = key_pair<L>(tok, lane_base);
+                        // the hash words have their low KEY_BITS cleared, so
+                        // "| p" == "+ p"; IMADs keep the key formation off
+                        // the ALU pipe, this loop's bottleneck (ncu: alu 83%)
                         const uint32_t p = (uint32_t)(base + j);
-                        key_update(k0, h.x | p);
-                        key_update(k1, h.y | p);
+                        const uint32_t q = KEY_MASK - p;
+                        key_update(k0, h.x, p, q);
+                        key_update(k1, h.y, p, q);
                     }
                 }
-                if ((k0.m1 >> KEY_BITS) == (k0.m2 >> KEY_BITS) && fn0 < F)
+                if (key_tie(k0) && fn0 < F)
                     t0 = resolve_tie(hi, lo, fn0, tokens, beg, end);
                 else
-                    t0 = __ldg(tokens + beg + (k0.m1 & KEY_MASK));
-                if ((k1.m1 >> KEY_BITS) == (k1.m2 >> KEY_BITS) && fn1 < F)
+                    t0 = __ldg(tokens + beg + (k0.first & KEY_MASK));
+                if (key_tie(k1) && fn1 < F)
                     t1 = resolve_tie(hi, lo, fn1, tokens, beg, end);
                 else
-                    t1 = __ldg(tokens + beg + (k1.m1 & KEY_MASK));
+                    t1 = __ldg(tokens + beg + (k1.first & KEY_MASK));
             }
             if (values != nullptr) {
                 if (fn0 < F) values[s * F + fn0] = t0;
                 if (fn1 < F) values[s * F + fn1] = t1;
             }
             if (sketch != nullptr) {
-                const uint32_t w0 = __ballot_sync(0xffffffffu, len > 0 && fn0 < F && sketch_bit(bitmask, fn0, t0));
-                const uint32_t w1 = __ballot_sync(0xffffffffu, len > 0 && fn1 < F && sketch_bit(bitmask, fn1, t1));
+                const uint32_t w0 = __ballot_sync(0xffffffffu, len > 0 && fn0 < F && sketch_bit_s(bm_s, lane, t0));
+                const uint32_t w1 = __ballot_sync(0xffffffffu, len > 0 && fn1 < F &&
+                                                                   sketch_bit_s(bm_s, lane + 32, t1));
                 if (lane == 0) sketch[s * words + c] = ((uint64_t)w1 << 32) | w0;
             }
         }
@@ -396,7 +448,7 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_keyed(
 template <int L>
 static void launch_minhash_keyed(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
                                  int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
-    const int smem = L * 256 * 32 * 8;
+    const int smem = L * 256 * 32 * 8 + (sketch != nullptr ? 64 * 33 * 4 : 0);
     CPSJ_CUDA(cudaFuncSetAttribute(k_minhash_keyed<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
