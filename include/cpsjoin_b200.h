@@ -101,6 +101,8 @@ typedef struct {
     double split_p;          /* 1.0 / (lambda_ * t) (cpsjoin.py:234)           */
     const uint64_t *h_rep_seeds;  /* repetition tree seeds (cpsjoin.py:346) */
     int32_t n_reps;
+    int32_t value_bits;      /* every MinHash value < 2^value_bits (0 = 32);
+                                narrows the split's radix-sort keys          */
 } cpsj_plan;
 
 typedef struct {

@@ -133,7 +133,7 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinA
     seeds = plan.rep_seeds if rep_indices is None else plan.rep_seeds[np.asarray(rep_indices, dtype=np.int64)]
     seeds = np.ascontiguousarray(seeds)
     cplan = Plan(float(params.lambda_), int(params.limit), int(params.depth_cap), plan.accept_dist,
-                 plan.flag_dist, float(plan.split_p), seeds.ctypes.data, int(len(seeds)))
+                 plan.flag_dist, float(plan.split_p), seeds.ctypes.data, int(len(seeds)), _value_bits(emb))
     st = JoinStats()
     ctx.check(ctx.lib.cpsj_self_join(ctx.handle, ctypes.byref(inputs), ctypes.byref(cplan), ctypes.byref(st),
                                      stream))
@@ -156,6 +156,22 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinA
                         int(st.peak_live_members))
     stats = {f: int(getattr(st, f)) for f, _ in JoinStats._fields_}
     return JoinArrays(a, b, sims, counters, caps, stats)
+
+
+def _value_bits(emb: EmbeddedDataset) -> int:
+    """Bits of the largest MinHash value: every value is a token of the
+    CSR, so the token universe bounds it; host-provided values are checked
+    directly.  0 means "use all 32 bits"."""
+    if emb._width and "values" in emb._dev and not getattr(emb, "_values_host_set", False):
+        vmax = int(emb._width) - 1          # values computed by K1 from this CSR
+    elif emb._values is not None:
+        key = id(emb._values)
+        if getattr(emb, "_vmax_key", None) != key:
+            emb._vmax_key, emb._vmax = key, (int(emb._values.max()) if emb._values.size else 0)
+        vmax = emb._vmax
+    else:
+        return 0
+    return max(1, vmax.bit_length())
 
 
 def _emit_warnings(res: JoinArrays, params: CPSJoinParams, n: int) -> None:

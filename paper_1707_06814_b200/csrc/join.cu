@@ -138,12 +138,18 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
         int dist = 0;
         if (ELL >= 8) {
             // the distance only grows word by word: once no lane of the warp
-            // can still pass after half the words, the row is done
+            // can still pass, the row is done.  Unrelated pairs sit near
+            // 32 bits per word, so checkpoints at 5/8 and 6/8 of the words
+            // (dist ~160 and ~192 of accept ~144 at l=8) end most rows early.
+            constexpr int C1 = EL * 5 / 8, C2 = EL * 6 / 8;
 #pragma unroll
-            for (int k = 0; k < EL / 2; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+            for (int k = 0; k < C1; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
             if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
 #pragma unroll
-            for (int k = EL / 2; k < EL; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+            for (int k = C1; k < C2; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+            if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
+#pragma unroll
+            for (int k = C2; k < EL; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
         } else if (ELL > 0) {
 #pragma unroll
             for (int k = 0; k < EL; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
@@ -197,17 +203,32 @@ __global__ void __launch_bounds__(TPB) k_leaf_pairs(
         const int32_t *mem = members + nd_off[node];
         a = mem[i];
         b = mem[j];
-        const int ell = ELL > 0 ? ELL : ell_rt;
-        const uint64_t *sa = sketch + (size_t)a * ell, *sb = sketch + (size_t)b * ell;
-        int dist = 0;
-        if (ELL > 0) {
-#pragma unroll
-            for (int k = 0; k < (ELL > 0 ? ELL : 1); ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
-        } else {
-            for (int k = 0; k < ell; ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
-        }
-        pass = dist <= accept && size_filter(sizes[a], sizes[b], lam);
     }
+    const int ell = ELL > 0 ? ELL : ell_rt;
+    const uint64_t *sa = sketch + (size_t)a * ell, *sb = sketch + (size_t)b * ell;
+    int dist = 0;
+    bool alive = valid;
+    if (ELL >= 8) {
+        // warp-wide early exit at 5/8 and 6/8 of the words (see k_leaf_tiles)
+        constexpr int EL = ELL > 0 ? ELL : 8, C1 = EL * 5 / 8, C2 = EL * 6 / 8;
+#pragma unroll
+        for (int k = 0; k < C1; ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
+        alive = alive && dist <= accept;
+        if (__any_sync(0xffffffffu, alive)) {
+#pragma unroll
+            for (int k = C1; k < C2; ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
+            alive = alive && dist <= accept;
+            if (__any_sync(0xffffffffu, alive)) {
+#pragma unroll
+                for (int k = C2; k < EL; ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
+                alive = alive && dist <= accept;
+            }
+        }
+    } else {
+        for (int k = 0; k < ell; ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
+        alive = alive && dist <= accept;
+    }
+    if (alive) pass = size_filter(sizes[a], sizes[b], lam);
     const unsigned mask = __ballot_sync(0xffffffffu, pass);
     if (mask) {
         unsigned long long base = 0;
@@ -384,13 +405,15 @@ __global__ void k_select(int64_t n_int, const int64_t *__restrict__ ilist, const
 }
 
 // one entry per (node, selected position, survivor) in that order; the key
-// (segment << 32 | minhash value) sorts stably into the groups of
+// (segment << vbits | minhash value) sorts stably into the groups of
 // split_buckets: position ascending, value ascending, members ascending.
+// vbits = bits of the largest value (from the token universe), so the radix
+// sort only runs over vbits + bits(#segments) key bits.
 __global__ void k_build_keys(int64_t E, const int64_t *__restrict__ e_off, int64_t n_int,
                              const int64_t *__restrict__ seg_off, const int64_t *__restrict__ nsel,
                              const int64_t *__restrict__ im_off, const int64_t *__restrict__ fscan,
                              const int16_t *__restrict__ sel_pos, int t, const int32_t *__restrict__ surv,
-                             const uint32_t *__restrict__ values, uint64_t *__restrict__ keys,
+                             const uint32_t *__restrict__ values, int vbits, uint64_t *__restrict__ keys,
                              int32_t *__restrict__ vals) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
@@ -400,7 +423,7 @@ __global__ void k_build_keys(int64_t E, const int64_t *__restrict__ e_off, int64
     const int64_t r = local / s, p = local - r * s;
     const int pos = sel_pos[k * t + r];
     const int32_t x = surv[(im_off[k] - fscan[im_off[k]]) + p];
-    keys[e] = ((uint64_t)(seg_off[k] + r) << 32) | values[(size_t)x * t + pos];
+    keys[e] = ((uint64_t)(seg_off[k] + r) << vbits) | values[(size_t)x * t + pos];
     vals[e] = x;
 }
 
@@ -444,14 +467,15 @@ __global__ void k_children(const int64_t *__restrict__ Gp, int64_t E, const int6
                            const int64_t *__restrict__ ilist, const uint64_t *__restrict__ nd_seed,
                            const int64_t *__restrict__ nd_S, uint64_t child_off,
                            int64_t *__restrict__ c_off, int32_t *__restrict__ c_cnt,
-                           uint64_t *__restrict__ c_seed, int64_t *__restrict__ c_S, DevCounters *ctr) {
+                           uint64_t *__restrict__ c_seed, int64_t *__restrict__ c_S, int vbits,
+                           DevCounters *ctr) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t G = *Gp;
     long long cand_peak = 0;
     if (g < G && keep[g]) {
         const int64_t st = gstart[g];
         const int64_t sz = (g + 1 < G ? gstart[g + 1] : E) - st;
-        const int64_t seg = (int64_t)(keys[st] >> 32);
+        const int64_t seg = (int64_t)(keys[st] >> vbits);
         const int64_t k = upper_bound_i64(seg_off, n_int + 1, seg) - 1;
         const int64_t node = ilist[k];
         const int64_t g0 = hscan[e_off[k]];  // parent's first group
@@ -689,6 +713,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         CPSJ_CUDA(cudaStreamSynchronize(st));  // host vectors above go out of scope
     }
     const uint64_t child_off = (uint64_t)t + 64ull * (uint64_t)ell;
+    const int vbits = plan->value_bits > 0 && plan->value_bits < 32 ? plan->value_bits : 32;
     unsigned long long res_bound = 0;  // host upper bound of result slots used
 
     // K5 on `nc` candidates emitted since the last reset; `regen` re-emits
@@ -859,10 +884,10 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             vals.alloc(E, st);
             vals2.alloc(E, st);
             k_build_keys<<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p, im_off_c.p, fscan.p,
-                                                        sel_pos.p, t, surv.p, in->d_values, keys.p, vals.p);
+                                                        sel_pos.p, t, surv.p, in->d_values, vbits, keys.p, vals.p);
             CPSJ_LAUNCH_CHECK();
-            int end_bit = 32;
-            while (end_bit < 64 && ((uint64_t)n_seg >> (end_bit - 32)) > 0) ++end_bit;
+            int end_bit = vbits;
+            while (end_bit < 64 && ((uint64_t)n_seg >> (end_bit - vbits)) > 0) ++end_bit;
             size_t bytes = 0;
             CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0, end_bit,
                                                       st));
@@ -908,7 +933,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             nx.members.alloc(nx.M, st);
             k_children<<<blocks_for(E), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p,
                                                       keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p, lv.S.p,
-                                                      child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, ctr.p);
+                                                      child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, vbits,
+                                                      ctr.p);
             CPSJ_LAUNCH_CHECK();
             k_scatter_children<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p, keep.p, mscan.p, vals2.p,
                                                               nx.members.p);

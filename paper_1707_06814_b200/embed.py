@@ -134,6 +134,7 @@ class EmbeddedDataset:
     @values.setter
     def values(self, v):
         self._values = np.asarray(v, dtype=np.uint32)
+        self._values_host_set = True
         self._dev.pop("values", None)
         self._dense = None
         self._d = None
