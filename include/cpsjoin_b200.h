@@ -86,6 +86,9 @@ typedef struct {
     int32_t t;
     const uint64_t *d_sketch;   /* emb.sketches(ell, seed)  (n, ell)    */
     int32_t ell;
+    const int8_t *d_side;       /* emb.side (n) or NULL: R x S join over a
+                                   tagged union suppresses same-side pairs
+                                   before verification (cpsjoin.py:135-136) */
 } cpsj_inputs;
 
 /* host-derived plan; every float rule is pre-reduced to an integer

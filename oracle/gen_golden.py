@@ -167,8 +167,69 @@ def synthetic_fixture(name, values, lists, d_origin, joins, patch_rows=None):
     save(name, **out)
 
 
+def rs_fixture(name, r_lists, s_lists, d, t, emb_seed, joins):
+    """join_rs (cpsjoin.py:354-385) on two datasets over a shared universe."""
+    from simjoin.cpsjoin import join_rs
+    ds_r = Dataset.from_token_lists(r_lists, d=d)
+    ds_s = Dataset.from_token_lists(s_lists, d=d)
+    params = EmbeddingParams(t=t, seed=emb_seed)
+    er, es = embed_dataset(params, ds_r), embed_dataset(params, ds_s)
+    out = {}
+    for side, ds in (("r", ds_r), ("s", ds_s)):
+        c = csr_of(ds)
+        for k, v in c.items():
+            out[f"{side}_{k}"] = v
+    out.update(t=np.int64(t), emb_seed=np.int64(emb_seed))
+    for k, kw in enumerate(joins):
+        h = _Count()
+        lg = logging.getLogger("simjoin.cpsjoin")
+        lg.addHandler(h)
+        try:
+            pairs, c = join_rs(er, es, CPSJoinParams(lambda_=kw["lam"], seed=kw["seed"],
+                                                     repetitions=kw.get("reps", 10), ell=kw.get("ell", 8)))
+        finally:
+            lg.removeHandler(h)
+        out[f"j{k}_pair_a"] = np.array([p.a for p in pairs], dtype=np.int64)
+        out[f"j{k}_pair_b"] = np.array([p.b for p in pairs], dtype=np.int64)
+        out[f"j{k}_pair_sim"] = np.array([p.similarity for p in pairs], dtype=np.float64)
+        out[f"j{k}_counters"] = np.array([c.pre_candidates, c.candidates, c.results, c.max_depth,
+                                          c.peak_live_members], dtype=np.int64)
+        out[f"j{k}_params"] = np.array([kw["lam"], kw.get("ell", 8), kw["seed"], kw.get("reps", 10), 250, 0.1,
+                                        0.05, 64], dtype=np.float64)
+    out["n_joins"] = np.int64(len(joins))
+    save(name, **out)
+
+
+def rs_main():
+    # planted halves (tests/test_cpsjoin.py:434-452 shape)
+    size, overlap = 17, 14
+    r_lists, s_lists = [], []
+    for k in range(40):
+        lo = k * (2 * size - overlap)
+        common = list(range(lo, lo + overlap))
+        r_lists.append(common + list(range(lo + overlap, lo + size)))
+        s_lists.append(common + list(range(lo + size, lo + 2 * size - overlap)))
+    rng = np.random.default_rng(12)
+    r_lists += [rng.choice(np.arange(2000, 6000), size=17, replace=False) for _ in range(300)]
+    s_lists += [rng.choice(np.arange(2000, 6000), size=17, replace=False) for _ in range(250)]
+    rs_fixture("rs_planted", r_lists, s_lists, 6000, 128, 4, [dict(lam=0.5, seed=4), dict(lam=0.6, seed=9, reps=3)])
+    # same input on both sides (tests/test_cpsjoin.py:412-424 shape)
+    lists = planted_lists(100, 10, 81)
+    ds = Dataset.from_token_lists(lists)
+    rows = [ds.records[i].tokens.tolist() for i in range(len(ds))]
+    rs_fixture("rs_same", rows, rows, ds.d, 128, 15, [dict(lam=0.5, seed=15)])
+    # a config-1 sample split into halves
+    w1 = generate(1, scale=0.05)
+    rows = [w1.tokens[w1.offsets[i]:w1.offsets[i + 1]].tolist() for i in range(w1.n)]
+    rs_fixture("rs_c1_sample", rows[::2], rows[1::2], w1.d, 128, 7, [dict(lam=0.5, seed=7, reps=3)])
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--rs-only" in sys.argv:
+        rs_main()
+        return
+    rs_main()
     kat_minhash()
     # reference-fixture shapes (planted J = 0.7 pairs)
     emb_fixture("planted_small", Dataset.from_token_lists(planted_lists(60, 12, 31)), 128, 3,

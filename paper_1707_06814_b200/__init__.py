@@ -11,8 +11,8 @@ fallback: without the built library and a CUDA device the entry points
 raise.
 """
 from .core import Counters, Dataset, Record, ResultPair, check_threshold, jaccard  # noqa: F401
-from .cpsjoin import CPSJoinParams, cpsjoin_self, cpsjoin_self_arrays, join_rs  # noqa: F401
-from .embed import EmbeddedDataset, EmbeddingParams, embed_dataset  # noqa: F401
+from .cpsjoin import CPSJoinParams, cpsjoin_self, cpsjoin_self_arrays, join_rs, join_rs_arrays  # noqa: F401
+from .embed import EmbeddedDataset, EmbeddingParams, embed_dataset, union_embedded  # noqa: F401
 from .hashing import SketchFamily, match_threshold  # noqa: F401
 
 __version__ = "0.1.0"

@@ -19,7 +19,7 @@ CPSJ_E_ARG, CPSJ_E_CUDA, CPSJ_E_OOM, CPSJ_E_PICK = -1, -2, -3, -4
 
 class Inputs(ctypes.Structure):
     _fields_ = [("d_tokens", P), ("d_offsets", P), ("d_sizes", P), ("n", i64),
-                ("d_values", P), ("t", i32), ("d_sketch", P), ("ell", i32)]
+                ("d_values", P), ("t", i32), ("d_sketch", P), ("ell", i32), ("d_side", P)]
 
 
 class Plan(ctypes.Structure):

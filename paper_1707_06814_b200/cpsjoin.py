@@ -106,7 +106,7 @@ class JoinArrays:
     stats: dict
 
 
-def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinArrays:
+def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None, map_ids: bool = True) -> JoinArrays:
     import torch
 
     from ._native import Context, Inputs, JoinStats, Plan
@@ -126,10 +126,11 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinA
         if dvals.shape[1] != t:
             raise ValueError("embedded dataset is inconsistent")
         sk = emb.sketches_device(params.ell, params.seed)
+        side = emb.device_side(ctx)
         inputs = Inputs(tok.data_ptr(), off.data_ptr(), sizes.data_ptr(), n, dvals.data_ptr(), t,
-                        sk.data_ptr(), params.ell)
+                        sk.data_ptr(), params.ell, None if side is None else side.data_ptr())
     else:
-        inputs = Inputs(None, None, None, n, None, t, None, params.ell)
+        inputs = Inputs(None, None, None, n, None, t, None, params.ell, None)
     seeds = plan.rep_seeds if rep_indices is None else plan.rep_seeds[np.asarray(rep_indices, dtype=np.int64)]
     seeds = np.ascontiguousarray(seeds)
     cplan = Plan(float(params.lambda_), int(params.limit), int(params.depth_cap), plan.accept_dist,
@@ -145,7 +146,7 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinA
     a = (keys >> np.uint64(32)).astype(np.int64)
     b = (keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
     src = emb.source_ids
-    if src is not None and not emb.ids_are_rows():
+    if map_ids and src is not None and not emb.ids_are_rows():
         # map rows to source ids, re-orient and re-dedup (cpsjoin.py:313-318)
         ia, ib = np.asarray(src)[a], np.asarray(src)[b]
         lo, hi = np.minimum(ia, ib).astype(np.uint64), np.maximum(ia, ib).astype(np.uint64)
@@ -203,7 +204,34 @@ def cpsjoin_self(emb: EmbeddedDataset, params: CPSJoinParams) -> tuple[list[Resu
     return pairs, res.counters
 
 
-def join_rs(r: EmbeddedDataset, s: EmbeddedDataset, params: CPSJoinParams):
-    """R x S cross join (cpsjoin.py:354-385): the next row of SURVEY.md 8(f);
-    not built yet on the GPU path."""
-    raise NotImplementedError("join_rs is not implemented on the GPU path yet (SURVEY.md 8(f) rank 1)")
+def join_rs_arrays(r: EmbeddedDataset, s: EmbeddedDataset, params: CPSJoinParams) -> JoinArrays:
+    """join_rs returning arrays: a = record id in r, b = record id in s."""
+    from .embed import union_embedded
+    union = union_embedded(r, s)
+    res = _run(union, params, map_ids=False)
+    n = len(union)
+    _emit_warnings(res, params, n)
+    if len(res.a):
+        # same-side pairs never reach verification, and r rows precede s
+        # rows, so the smaller row of every pair is the r side
+        src = np.asarray(union.source_ids)
+        ids_r = src[res.a].astype(np.uint64)
+        ids_s = src[res.b].astype(np.uint64)
+        keys = (ids_r << np.uint64(32)) | ids_s
+        _, first = np.unique(keys, return_index=True)      # cpsjoin.py:381-384
+        res.a = ids_r[first].astype(np.int64)
+        res.b = ids_s[first].astype(np.int64)
+        res.similarity = res.similarity[first]
+    return res
+
+
+def join_rs(r: EmbeddedDataset, s: EmbeddedDataset, params: CPSJoinParams
+            ) -> tuple[list[ResultPair], Counters]:
+    """Cross join of two embeddings sharing a function family
+    (cpsjoin.py:354-385): a self-join over the tagged union whose BruteForce
+    suppresses same-side pairs before verification; ``a`` is a record id of
+    r and ``b`` one of s."""
+    res = join_rs_arrays(r, s, params)
+    pairs = [ResultPair(int(x), int(y), float(v))
+             for x, y, v in zip(res.a.tolist(), res.b.tolist(), res.similarity.tolist())]
+    return pairs, res.counters

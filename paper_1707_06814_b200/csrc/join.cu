@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
     int64_t total_tiles, const int64_t *__restrict__ tile_off, int64_t N,
     const int64_t *__restrict__ nd_off, const int32_t *__restrict__ nd_cnt,
     const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch, int ell_rt,
-    const int32_t *__restrict__ sizes, int32_t accept, double lam, int2 *__restrict__ cand,
+    const int32_t *__restrict__ sizes, const int8_t *__restrict__ side, int32_t accept, double lam,
+    int2 *__restrict__ cand,
     unsigned long long cap, DevCounters *ctr) {
     const int lane = threadIdx.x & 31;
     const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
             for (int k = 0; k < ell; ++k) dist += __popcll(__ldg(rs + k) ^ (jvalid ? __ldg(csp + k) : 0));
         }
         bool pass = active && dist <= accept;
-        if (pass) pass = size_filter(sizes[row], col_size, lam);
+        if (pass) pass = size_filter(sizes[row], col_size, lam) && (side == nullptr || side[row] != side[col]);
         const unsigned mask = __ballot_sync(0xffffffffu, pass);
         if (mask) {
             unsigned long long base = 0;
@@ -181,7 +182,8 @@ __global__ void __launch_bounds__(TPB) k_leaf_pairs(
     int64_t total_pairs, const int64_t *__restrict__ pair_off, int64_t N,
     const int64_t *__restrict__ nd_off, const int32_t *__restrict__ nd_cnt,
     const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch, int ell_rt,
-    const int32_t *__restrict__ sizes, int32_t accept, double lam, int2 *__restrict__ cand,
+    const int32_t *__restrict__ sizes, const int8_t *__restrict__ side, int32_t accept, double lam,
+    int2 *__restrict__ cand,
     unsigned long long cap, DevCounters *ctr) {
     const int lane = threadIdx.x & 31;
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(TPB) k_leaf_pairs(
         for (int k = 0; k < ell; ++k) dist += __popcll(__ldg(sa + k) ^ __ldg(sb + k));
         alive = alive && dist <= accept;
     }
-    if (alive) pass = size_filter(sizes[a], sizes[b], lam);
+    if (alive) pass = size_filter(sizes[a], sizes[b], lam) && (side == nullptr || side[a] != side[b]);
     const unsigned mask = __ballot_sync(0xffffffffu, pass);
     if (mask) {
         unsigned long long base = 0;
@@ -304,8 +306,8 @@ __global__ void k_point(int64_t n_flag, const int64_t *__restrict__ flist, const
                         const int64_t *__restrict__ ilist, const int64_t *__restrict__ nd_off,
                         const int32_t *__restrict__ nd_cnt, const int32_t *__restrict__ members,
                         const uint64_t *__restrict__ sketch, int ell, const int32_t *__restrict__ sizes,
-                        int32_t accept, double lam, int2 *__restrict__ cand, unsigned long long cap,
-                        int count_pre, DevCounters *ctr) {
+                        const int8_t *__restrict__ side, int32_t accept, double lam, int2 *__restrict__ cand,
+                        unsigned long long cap, int count_pre, DevCounters *ctr) {
     const int lane = threadIdx.x & 31;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (w >= n_flag) return;
@@ -332,7 +334,8 @@ __global__ void k_point(int64_t n_flag, const int64_t *__restrict__ flist, const
                 const uint64_t *sy = sketch + (size_t)y * ell;
                 int dist = 0;
                 for (int q = 0; q < ell; ++q) dist += __popcll(sx[q] ^ sy[q]);
-                pass = dist <= accept && size_filter(size_x, sizes[y], lam);
+                pass = dist <= accept && size_filter(size_x, sizes[y], lam) &&
+                       (side == nullptr || side[x] != side[y]);
             }
         }
         const unsigned mask = __ballot_sync(0xffffffffu, pass);
@@ -631,14 +634,15 @@ void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level
     if (wk.tiles > 0) {
         k_leaf_tiles<ELL><<<blocks_for(wk.tiles * 32), TPB, 0, st>>>(wk.tiles, wk.tile_off, lv.N, lv.off.p,
                                                                      lv.cnt.p, lv.members.p, in->d_sketch, in->ell,
-                                                                     in->d_sizes, accept, lam, cand, cap, ctr);
+                                                                     in->d_sizes, in->d_side, accept, lam, cand, cap,
+                                                                     ctr);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
     }
     if (wk.pairs > 0) {
         k_leaf_pairs<ELL><<<blocks_for(wk.pairs), TPB, 0, st>>>(wk.pairs, wk.pair_off, lv.N, lv.off.p, lv.cnt.p,
                                                                 lv.members.p, in->d_sketch, in->ell, in->d_sizes,
-                                                                accept, lam, cand, cap, ctr);
+                                                                in->d_side, accept, lam, cand, cap, ctr);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
     }
@@ -860,7 +864,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             ProfScope prof(ctx, PROF_POINT, st);
             k_point<<<blocks_for(n_flag * 32), TPB, 0, st>>>(
                 n_flag, flist.p, fscan.p, flags.p, im_off_c.p, n_int, ilist.p, lv.off.p, lv.cnt.p, lv.members.p,
-                in->d_sketch, ell, in->d_sizes, plan->accept_dist, lam, cand.p, cand_cap, count_pre, ctr.p);
+                in->d_sketch, ell, in->d_sizes, in->d_side, plan->accept_dist, lam, cand.p, cand_cap, count_pre,
+                ctr.p);
             CPSJ_LAUNCH_CHECK();
             ctx->launches++;
             count_pre = 0;  // a regeneration must not count twice

@@ -109,6 +109,18 @@ class EmbeddedDataset:
             self._dev["values"] = torch.from_numpy(v.view(np.int32)).to(dev, non_blocking=True)
         return self._dev["tokens"], self._dev["offsets"], self._dev["sizes"], self._dev["values"]
 
+    def device_side(self, ctx):
+        """emb.side as a device int8 tensor (None for a self-join dataset)."""
+        if self.side is None:
+            return None
+        key = id(self.side)
+        if self._dev.get("side_key") != key:
+            torch = _torch()
+            self._dev["side"] = torch.from_numpy(np.ascontiguousarray(self.side, dtype=np.int8)).to(
+                torch.device("cuda", ctx.device))
+            self._dev["side_key"] = key
+        return self._dev["side"]
+
     def ids_are_rows(self) -> bool:
         """True when source_ids == arange(n) (checked once per array)."""
         src = self.source_ids
@@ -272,6 +284,36 @@ def embed_device_csr(params: EmbeddingParams, d_tokens, d_offsets, d: int, host_
     obj._ids_checked, obj._ids_ok = (id(obj.source_ids), n), True
     obj._sizes_fn = lambda: obj._dev["sizes"].cpu().numpy().astype(np.int64)
     return obj
+
+
+def union_embedded(r: EmbeddedDataset, s: EmbeddedDataset) -> EmbeddedDataset:
+    """Tagged union of two embeddings sharing a function family (reference
+    embed.py:142-169): rows of r first with side 0, rows of s after with
+    side 1.  The device arrays are concatenated on the GPU."""
+    if r.t != s.t:
+        raise ValueError(f"embedding size mismatch: {r.t} vs {s.t}")
+    if r.seed != s.seed:
+        raise ValueError("inputs were embedded with different seeds")
+    torch = _torch()
+    from ._native import Context
+    ctx = Context.get()
+    tr, or_, zr, vr = r.device_inputs(ctx)
+    ts, os_, zs, vs = s.device_inputs(ctx)
+    n_r, n_s = len(r), len(s)
+    wr = r._width if r._width is not None else r._csr_host()[2]
+    ws = s._width if s._width is not None else s._csr_host()[2]
+    u = EmbeddedDataset(None, None, None, r.t, r.seed, None, np.concatenate([r.sizes, s.sizes]),
+                        np.concatenate([np.asarray(r.source_ids), np.asarray(s.source_ids)]),
+                        side=np.concatenate([np.zeros(n_r, dtype=np.int8), np.ones(n_s, dtype=np.int8)]))
+    u._dev.update(tokens=torch.cat([tr, ts]), offsets=torch.cat([or_, os_[1:] + or_[-1]]),
+                  sizes=torch.cat([zr, zs]), values=torch.cat([vr, vs]))
+    u._n = n_r + n_s
+    u._width = max(int(wr), int(ws))
+    if r._csr_arrays is not None and s._csr_arrays is not None or (r._csr is not None and s._csr is not None):
+        rt, ro, _ = r._csr_host()
+        st, so, _ = s._csr_host()
+        u._csr_arrays = (np.concatenate([rt, st]), np.concatenate([ro, so[1:] + ro[-1]]), u._width)
+    return u
 
 
 _PIPELINE_MIN_SETS = 1 << 16

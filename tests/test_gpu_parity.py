@@ -279,3 +279,45 @@ def test_pipelined_embed_with_sketch_hint_matches_oracle(chunks):
     assert np.array_equal(emb.sketches(8, 7), sk)
     res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=0.5, seed=7, repetitions=2))
     assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)
+
+
+# ---- R x S join, against reference-made fixtures
+
+@pytest.mark.parametrize("name", ["rs_planted", "rs_same", "rs_c1_sample"])
+def test_join_rs_matches_reference_golden(name):
+    from paper_1707_06814_b200 import Dataset, EmbeddingParams, embed_dataset, join_rs_arrays
+    z = load(name)
+    params = EmbeddingParams(t=int(z["t"]), seed=int(z["emb_seed"]))
+    er = embed_dataset(params, Dataset.from_csr(z["r_tokens"], z["r_offsets"], int(z["r_d"])))
+    es = embed_dataset(params, Dataset.from_csr(z["s_tokens"], z["s_offsets"], int(z["s_d"])))
+    for k in range(int(z["n_joins"])):
+        res = join_rs_arrays(er, es, _params(z, k))
+        assert np.array_equal(res.a, z[f"j{k}_pair_a"])
+        assert np.array_equal(res.b, z[f"j{k}_pair_b"])
+        assert np.array_equal(res.similarity, z[f"j{k}_pair_sim"])
+        c = res.counters
+        assert [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members] == \
+            z[f"j{k}_counters"].tolist()
+
+
+def test_join_rs_same_input_is_self_join_plus_diagonal():
+    from paper_1707_06814_b200 import CPSJoinParams, EmbeddingParams, cpsjoin_self, embed_dataset, join_rs
+    ds = _planted(100, 10, 81)
+    params = EmbeddingParams(t=128, seed=15)
+    jp = CPSJoinParams(lambda_=0.5, seed=15)
+    cross, _ = join_rs(embed_dataset(params, ds), embed_dataset(params, ds), jp)
+    self_pairs, _ = cpsjoin_self(embed_dataset(params, ds), jp)
+    cross_keys = {(min(p.a, p.b), max(p.a, p.b)) for p in cross}
+    assert cross_keys == {p.key() for p in self_pairs} | {(i, i) for i in range(len(ds))}
+
+
+def test_join_rs_rejects_mismatched_embeddings():
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, embed_dataset, join_rs
+    ds = Dataset.from_token_lists([[0, 1], [1, 2]], d=10)
+    a = embed_dataset(EmbeddingParams(t=16, seed=1), ds)
+    b = embed_dataset(EmbeddingParams(t=32, seed=1), ds)
+    c = embed_dataset(EmbeddingParams(t=16, seed=2), ds)
+    with pytest.raises(ValueError):
+        join_rs(a, b, CPSJoinParams(lambda_=0.5, seed=1))
+    with pytest.raises(ValueError):
+        join_rs(a, c, CPSJoinParams(lambda_=0.5, seed=1))
