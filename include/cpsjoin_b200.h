@@ -106,6 +106,11 @@ typedef struct {
     int32_t n_reps;
     int32_t value_bits;      /* every MinHash value < 2^value_bits (0 = 32);
                                 narrows the split's radix-sort keys          */
+    int32_t use_count_table; /* flag rule from exact embedded token counts
+                                (_count_table_estimates, cpsjoin.py:209-219)
+                                instead of the node sketch                    */
+    double count_threshold;  /* (1 - epsilon) * lambda_, compared as
+                                (double)(sum - t) / (double)(t (m - 1)) > it */
 } cpsj_plan;
 
 typedef struct {

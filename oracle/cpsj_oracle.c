@@ -171,6 +171,7 @@ typedef struct {
     int32_t ell;
     double lam, eps;
     int32_t limit, kstar, depth_cap;
+    int use_ct;             /* CPSJoinParams.use_count_table */
 } Ctx;
 
 typedef struct {
@@ -252,31 +253,63 @@ static void brute_force_point(const Ctx *c, Acc *acc, int64_t x, const int64_t *
     }
 }
 
+static int cmp_u32_first(const void *a, const void *b) {
+    uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+    return x < y ? -1 : (x > y);
+}
+
 /* pre-split pruning, returns survivors in member order: cps:248-275,
  * node sketch cps:182-198, estimates cps:201-206 */
 static int64_t brute_force_step(const Ctx *c, Acc *acc, const int64_t *mem, int64_t m,
                                 uint64_t seed, int64_t *surv) {
     if (m <= c->limit) { brute_force_pairs(c, acc, mem, m); return 0; }
-    int32_t mbits = 64 * c->ell;
-    uint64_t nsk[64];
-    memset(nsk, 0, sizeof(nsk));
-    for (int32_t i = 0; i < mbits; i++) {
-        double u = stream_uniform(seed, (uint64_t)c->t + (uint64_t)i);
-        int64_t idx = (int64_t)(u * (double)m);
-        if (idx >= m) { acc->error = 1; idx = m - 1; }
-        uint64_t w = c->sketch[mem[idx] * c->ell + (i >> 6)];
-        nsk[i >> 6] |= ((w >> (i & 63)) & 1ULL) << (i & 63);
-    }
     double thr = (1.0 - c->eps) * c->lam;
     uint8_t *flag = malloc(m);
     int64_t nflag = 0;
-    for (int64_t k = 0; k < m; k++) {
-        const uint64_t *s = c->sketch + mem[k] * c->ell;
-        int64_t dist = 0;
-        for (int w = 0; w < c->ell; w++) dist += __builtin_popcountll(s[w] ^ nsk[w]);
-        double est = 2.0 * (double)(mbits - dist) / (double)mbits - 1.0;
-        flag[k] = est > thr;
-        nflag += flag[k];
+    if (c->use_ct) {
+        /* exact embedded average similarity: cps:209-219.  count[dense id]
+         * over the node, summed over each member's t tokens, minus t;
+         * dense ids are equal exactly when (position, value) are */
+        int64_t *sum = calloc(m, sizeof(int64_t));
+        typedef struct { uint32_t v; int64_t k; } VK;
+        VK *tmp = malloc(m * sizeof(VK));
+        for (int32_t i = 0; i < c->t; i++) {
+            for (int64_t k = 0; k < m; k++) { tmp[k].v = c->values[mem[k] * c->t + i]; tmp[k].k = k; }
+            qsort(tmp, m, sizeof(VK), cmp_u32_first);
+            int64_t g = 0;
+            while (g < m) {
+                int64_t e = g + 1;
+                while (e < m && tmp[e].v == tmp[g].v) e++;
+                for (int64_t q = g; q < e; q++) sum[tmp[q].k] += e - g;
+                g = e;
+            }
+        }
+        for (int64_t k = 0; k < m; k++) {
+            double est = (double)(sum[k] - c->t) / (double)((int64_t)c->t * (m - 1));
+            flag[k] = est > thr;
+            nflag += flag[k];
+        }
+        free(tmp);
+        free(sum);
+    } else {
+        int32_t mbits = 64 * c->ell;
+        uint64_t nsk[64];
+        memset(nsk, 0, sizeof(nsk));
+        for (int32_t i = 0; i < mbits; i++) {
+            double u = stream_uniform(seed, (uint64_t)c->t + (uint64_t)i);
+            int64_t idx = (int64_t)(u * (double)m);
+            if (idx >= m) { acc->error = 1; idx = m - 1; }
+            uint64_t w = c->sketch[mem[idx] * c->ell + (i >> 6)];
+            nsk[i >> 6] |= ((w >> (i & 63)) & 1ULL) << (i & 63);
+        }
+        for (int64_t k = 0; k < m; k++) {
+            const uint64_t *s = c->sketch + mem[k] * c->ell;
+            int64_t dist = 0;
+            for (int w = 0; w < c->ell; w++) dist += __builtin_popcountll(s[w] ^ nsk[w]);
+            double est = 2.0 * (double)(mbits - dist) / (double)mbits - 1.0;
+            flag[k] = est > thr;
+            nflag += flag[k];
+        }
     }
     if (nflag) {
         uint8_t *alive = malloc(m);
@@ -384,14 +417,33 @@ static int cmp_ks(const void *a, const void *b) { return cmp_key(a, b); }
  * is sorted, so the output is independent of the thread count.
  * Returns 0, or 1 when a node-sketch pick fell out of range (the
  * reference raises IndexError there, cps:193). */
+int orc_self_join_ct(const uint32_t *tok, const int64_t *off, const int64_t *sizes, int64_t n,
+                     const uint32_t *values, int32_t t, const uint64_t *sketch, int32_t ell,
+                     double lam, double eps, int32_t limit, int32_t kstar, int32_t depth_cap,
+                     const uint64_t *rep_seeds, int32_t reps, int nthreads,
+                     uint64_t **out_keys, double **out_sims, int64_t *out_n,
+                     int64_t *counters /* pre, cand, res, max_depth, peak */,
+                     int64_t **cap_events, int64_t *n_cap_events, int use_count_table);
+
 int orc_self_join(const uint32_t *tok, const int64_t *off, const int64_t *sizes, int64_t n,
                   const uint32_t *values, int32_t t, const uint64_t *sketch, int32_t ell,
                   double lam, double eps, int32_t limit, int32_t kstar, int32_t depth_cap,
                   const uint64_t *rep_seeds, int32_t reps, int nthreads,
                   uint64_t **out_keys, double **out_sims, int64_t *out_n,
-                  int64_t *counters /* pre, cand, res, max_depth, peak */,
-                  int64_t **cap_events, int64_t *n_cap_events) {
-    Ctx c = {tok, off, sizes, n, values, t, sketch, ell, lam, eps, limit, kstar, depth_cap};
+                  int64_t *counters, int64_t **cap_events, int64_t *n_cap_events) {
+    return orc_self_join_ct(tok, off, sizes, n, values, t, sketch, ell, lam, eps, limit, kstar, depth_cap,
+                            rep_seeds, reps, nthreads, out_keys, out_sims, out_n, counters, cap_events,
+                            n_cap_events, 0);
+}
+
+int orc_self_join_ct(const uint32_t *tok, const int64_t *off, const int64_t *sizes, int64_t n,
+                     const uint32_t *values, int32_t t, const uint64_t *sketch, int32_t ell,
+                     double lam, double eps, int32_t limit, int32_t kstar, int32_t depth_cap,
+                     const uint64_t *rep_seeds, int32_t reps, int nthreads,
+                     uint64_t **out_keys, double **out_sims, int64_t *out_n,
+                     int64_t *counters /* pre, cand, res, max_depth, peak */,
+                     int64_t **cap_events, int64_t *n_cap_events, int use_count_table) {
+    Ctx c = {tok, off, sizes, n, values, t, sketch, ell, lam, eps, limit, kstar, depth_cap, use_count_table};
     Acc *accs = calloc(reps > 0 ? reps : 1, sizeof(Acc));
     if (n >= 2) {
         TreeArgs ta = {&c, accs, rep_seeds};

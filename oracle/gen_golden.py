@@ -48,7 +48,7 @@ class _Count(logging.Handler):
         self.msgs.append(record.getMessage())
 
 
-def run_join(emb, lam, *, ell=8, seed=0, reps=10, limit=250, eps=0.1, delta=0.05, depth_cap=64):
+def run_join(emb, lam, *, ell=8, seed=0, reps=10, limit=250, eps=0.1, delta=0.05, depth_cap=64, ct=False):
     h = _Count()
     lg = logging.getLogger("simjoin.cpsjoin")
     lg.addHandler(h)
@@ -56,7 +56,7 @@ def run_join(emb, lam, *, ell=8, seed=0, reps=10, limit=250, eps=0.1, delta=0.05
     try:
         pairs, c = cpsjoin_self(emb, CPSJoinParams(lambda_=lam, ell=ell, seed=seed, repetitions=reps,
                                                    limit=limit, epsilon=eps, delta=delta,
-                                                   depth_cap=depth_cap))
+                                                   depth_cap=depth_cap, use_count_table=ct))
     finally:
         lg.removeHandler(h)
     cap_msgs = [m for m in h.msgs if "depth cap" in m]
@@ -140,6 +140,7 @@ def emb_fixture(name, ds, t, emb_seed, joins):
         sk = emb.sketches(kw.get("ell", 8), kw.get("seed", 0))
         res["sketch_sha"] = np.array(sha(sk))
         res["sketch_head"] = sk[:8].copy()
+        res["use_count_table"] = np.int64(1 if kw.get("ct") else 0)
         for key, v in res.items():
             out[f"j{k}_{key}"] = v
     out["n_joins"] = np.int64(len(joins))
@@ -224,12 +225,31 @@ def rs_main():
     rs_fixture("rs_c1_sample", rows[::2], rows[1::2], w1.d, 128, 7, [dict(lam=0.5, seed=7, reps=3)])
 
 
+def ct_main():
+    """use_count_table=True (cpsjoin.py:209-219,262-263): exact token-count
+    flag rule; the dense cluster and a small limit make it fire."""
+    emb_fixture("ct_planted", Dataset.from_token_lists(planted_lists(420, 40, 41)), 128, 7,
+                [dict(lam=0.5, seed=7, ct=True, reps=4), dict(lam=0.5, seed=11, limit=40, reps=3, ct=True)])
+    rng = np.random.default_rng(5)
+    dense = [list(range(180)) + list(range(1000 + 10 * i, 1010 + 10 * i)) for i in range(300)]
+    dense += [rng.choice(np.arange(5000, 20000), size=30, replace=False) for _ in range(300)]
+    emb_fixture("ct_dense", Dataset.from_token_lists(dense), 128, 8,
+                [dict(lam=0.5, seed=8, reps=3, ct=True), dict(lam=0.8, seed=4, reps=2, eps=0.3, ct=True)])
+    w1 = generate(1, scale=0.1)
+    ds1 = Dataset.from_token_lists([w1.tokens[w1.offsets[i]:w1.offsets[i + 1]] for i in range(w1.n)], d=w1.d)
+    emb_fixture("ct_c1_sample", ds1, 128, 7, [dict(lam=0.5, seed=7, reps=3, ct=True)])
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     if "--rs-only" in sys.argv:
         rs_main()
         return
+    if "--ct-only" in sys.argv:
+        ct_main()
+        return
     rs_main()
+    ct_main()
     kat_minhash()
     # reference-fixture shapes (planted J = 0.7 pairs)
     emb_fixture("planted_small", Dataset.from_token_lists(planted_lists(60, 12, 31)), 128, 3,

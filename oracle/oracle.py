@@ -46,6 +46,8 @@ def lib():
                                     P, i32, ctypes.c_int,
                                     ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64),
                                     P, ctypes.POINTER(P), ctypes.POINTER(i64)]
+        L.orc_self_join_ct.restype = ctypes.c_int
+        L.orc_self_join_ct.argtypes = L.orc_self_join.argtypes + [ctypes.c_int]
         L.orc_exact_join.restype = ctypes.c_int
         L.orc_exact_join.argtypes = [P, P, i64, ctypes.c_uint32, dbl, ctypes.c_int,
                                      ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)]
@@ -159,7 +161,8 @@ def _take(ptr, n, dtype):
 
 
 def self_join(tokens, offsets, sizes, values, sketches, lam: float, *, epsilon=0.1, limit=250,
-              delta=0.05, repetitions=10, seed=0, depth_cap=64, threads: int = 0) -> JoinOut:
+              delta=0.05, repetitions=10, seed=0, depth_cap=64, threads: int = 0,
+              use_count_table: bool = False) -> JoinOut:
     """cpsjoin.py:331-351 on explicit arrays (self-join, source_ids = arange)."""
     tok, off = _csr(tokens, offsets)
     sizes = np.ascontiguousarray(sizes, dtype=np.int64)
@@ -172,11 +175,11 @@ def self_join(tokens, offsets, sizes, values, sketches, lam: float, *, epsilon=0
     kp, sp, cp = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
     nk, nc = ctypes.c_int64(), ctypes.c_int64()
     counters = np.zeros(5, dtype=np.int64)
-    err = lib().orc_self_join(_p(tok), _p(off), _p(sizes), n, _p(values), t, _p(sk), ell,
-                              float(lam), float(epsilon), int(limit), ks, int(depth_cap),
-                              _p(seeds), int(repetitions), threads,
-                              ctypes.byref(kp), ctypes.byref(sp), ctypes.byref(nk),
-                              _p(counters), ctypes.byref(cp), ctypes.byref(nc))
+    err = lib().orc_self_join_ct(_p(tok), _p(off), _p(sizes), n, _p(values), t, _p(sk), ell,
+                                 float(lam), float(epsilon), int(limit), ks, int(depth_cap),
+                                 _p(seeds), int(repetitions), threads,
+                                 ctypes.byref(kp), ctypes.byref(sp), ctypes.byref(nk),
+                                 _p(counters), ctypes.byref(cp), ctypes.byref(nc), int(bool(use_count_table)))
     keys = _take(kp, nk.value, np.uint64)
     sims = _take(sp, nk.value, np.float64)
     ev = _take(cp, nc.value, np.int64)

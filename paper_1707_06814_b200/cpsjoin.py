@@ -110,8 +110,6 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None, map_ids:
     import torch
 
     from ._native import Context, Inputs, JoinStats, Plan
-    if params.use_count_table:
-        raise NotImplementedError("use_count_table=True (cpsjoin.py:209-219) is not implemented on the GPU path")
     vals = emb.values if emb._values is not None else None
     t = emb.t
     if vals is not None and vals.shape[1] != t:
@@ -134,7 +132,8 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None, map_ids:
     seeds = plan.rep_seeds if rep_indices is None else plan.rep_seeds[np.asarray(rep_indices, dtype=np.int64)]
     seeds = np.ascontiguousarray(seeds)
     cplan = Plan(float(params.lambda_), int(params.limit), int(params.depth_cap), plan.accept_dist,
-                 plan.flag_dist, float(plan.split_p), seeds.ctypes.data, int(len(seeds)), _value_bits(emb))
+                 plan.flag_dist, float(plan.split_p), seeds.ctypes.data, int(len(seeds)), _value_bits(emb),
+                 1 if params.use_count_table else 0, (1.0 - params.epsilon) * params.lambda_)
     st = JoinStats()
     ctx.check(ctx.lib.cpsj_self_join(ctx.handle, ctypes.byref(inputs), ctypes.byref(cplan), ctypes.byref(st),
                                      stream))

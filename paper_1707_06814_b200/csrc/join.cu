@@ -648,6 +648,86 @@ void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level
     }
 }
 
+// ------------------------------------- count-table flag rule (test flag)
+//
+// _count_table_estimates (cpsjoin.py:209-219): for member x of a node with
+// m members, est = (sum_i count_i(x) - t) / (t (m - 1)) where count_i(x) is
+// the number of members whose embedded token at position i equals x's --
+// the dense id of (i, value) is equal exactly when (i, value) is, so the
+// dense remap is not needed.  One entry per (member, position), keyed
+// (node, position, value), radix-sorted; every entry adds its group size
+// to its member's sum.
+
+__global__ void k_ct_keys(int64_t EN, int t, const int64_t *__restrict__ im_off, int64_t n_int,
+                          const int64_t *__restrict__ ilist, const int64_t *__restrict__ nd_off,
+                          const int32_t *__restrict__ members, const uint32_t *__restrict__ values, int vbits,
+                          uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= EN) return;
+    const int64_t q = e / t, i = e - q * t;
+    const int64_t k = upper_bound_i64(im_off, n_int + 1, q) - 1;
+    const int32_t x = members[nd_off[ilist[k]] + (q - im_off[k])];
+    keys[e] = ((uint64_t)(k * t + i) << vbits) | values[(size_t)x * t + i];
+    vals[e] = (int32_t)q;
+}
+
+__global__ void k_ct_accumulate(int64_t EN, const int64_t *__restrict__ Gp, const int64_t *__restrict__ head,
+                                const int64_t *__restrict__ hscan, const int64_t *__restrict__ gstart,
+                                const int32_t *__restrict__ vals, unsigned long long *__restrict__ acc) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= EN) return;
+    const int64_t G = *Gp;
+    const int64_t g = hscan[e] + head[e] - 1;
+    const int64_t sz = (g + 1 < G ? gstart[g + 1] : EN) - gstart[g];
+    atomicAdd(acc + vals[e], (unsigned long long)sz);
+}
+
+__global__ void k_ct_flags(int64_t Mi, int t, const int64_t *__restrict__ im_off, int64_t n_int,
+                           const int64_t *__restrict__ ilist, const int32_t *__restrict__ nd_cnt,
+                           const unsigned long long *__restrict__ acc, double thr, int64_t *__restrict__ flags) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q > Mi) return;
+    if (q == Mi) { flags[q] = 0; return; }
+    const int64_t k = upper_bound_i64(im_off, n_int + 1, q) - 1;
+    const int64_t m = nd_cnt[ilist[k]];
+    const int64_t per = (int64_t)acc[q] - t;
+    const double est = (double)per / (double)((int64_t)t * (m - 1));
+    flags[q] = est > thr ? 1 : 0;
+}
+
+void count_table_flags(cpsj_ctx *ctx, Driver &drv, const cpsj_inputs *in, const cpsj_plan *plan, int vbits,
+                       int64_t n_int, int64_t Mi, const int64_t *ilist, const int64_t *im_off, const Level &lv,
+                       int64_t *flags, cudaStream_t st) {
+    const int t = in->t;
+    const int64_t EN = Mi * t;
+    DevBuf<uint64_t> keys(EN, st), keys2(EN, st);
+    DevBuf<int32_t> vals(EN, st), vals2(EN, st);
+    k_ct_keys<<<blocks_for(EN), TPB, 0, st>>>(EN, t, im_off, n_int, ilist, lv.off.p, lv.members.p, in->d_values,
+                                              vbits, keys.p, vals.p);
+    CPSJ_LAUNCH_CHECK();
+    int end_bit = vbits;
+    while (end_bit < 64 && ((uint64_t)(n_int * t) >> (end_bit - vbits)) > 0) ++end_bit;
+    size_t bytes = 0;
+    CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, EN, 0, end_bit, st));
+    if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+    CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, EN, 0, end_bit,
+                                              st));
+    ctx->lib_calls++;
+    DevBuf<int64_t> head(EN + 1, st), hscan(EN + 1, st), gstart(EN, st);
+    k_heads<<<blocks_for(EN + 1), TPB, 0, st>>>(EN, keys2.p, head.p);
+    CPSJ_LAUNCH_CHECK();
+    drv.scan(head.p, hscan.p, EN + 1);
+    k_group_start<<<blocks_for(EN), TPB, 0, st>>>(EN, head.p, hscan.p, gstart.p);
+    CPSJ_LAUNCH_CHECK();
+    DevBuf<unsigned long long> acc(std::max<int64_t>(1, Mi), st);
+    CPSJ_CUDA(cudaMemsetAsync(acc.p, 0, std::max<int64_t>(1, Mi) * sizeof(unsigned long long), st));
+    k_ct_accumulate<<<blocks_for(EN), TPB, 0, st>>>(EN, hscan.p + EN, head.p, hscan.p, gstart.p, vals2.p, acc.p);
+    CPSJ_LAUNCH_CHECK();
+    k_ct_flags<<<blocks_for(Mi + 1), TPB, 0, st>>>(Mi, t, im_off, n_int, ilist, lv.cnt.p, acc.p,
+                                                   plan->count_threshold, flags);
+    ctx->launches += 5;
+}
+
 void leaf_dispatch(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level &lv, const cpsj_inputs *in,
                    int32_t accept, double lam, int2 *cand, unsigned long long cap, DevCounters *ctr) {
     switch (in->ell) {
@@ -804,14 +884,20 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 drv.scan(icnt.p, im_off_c.p, n_int + 1);
             }
             nsk.alloc(n_int * ell, st);
-            k_node_sketch<<<(unsigned)n_int, TPB, 0, st>>>(ilist.p, lv.off.p, lv.cnt.p, lv.seed.p, lv.members.p,
-                                                           in->d_sketch, ell, t,
-                                                           reinterpret_cast<uint32_t *>(nsk.p), ctr.p);
-            CPSJ_LAUNCH_CHECK();
+            if (!plan->use_count_table) {
+                k_node_sketch<<<(unsigned)n_int, TPB, 0, st>>>(ilist.p, lv.off.p, lv.cnt.p, lv.seed.p,
+                                                               lv.members.p, in->d_sketch, ell, t,
+                                                               reinterpret_cast<uint32_t *>(nsk.p), ctr.p);
+                CPSJ_LAUNCH_CHECK();
+            }
             flags.alloc(Mi + 1, st);
             fscan.alloc(Mi + 1, st);
-            k_flags<<<blocks_for(Mi + 1), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p, lv.members.p,
-                                                        in->d_sketch, ell, nsk.p, plan->flag_dist, flags.p);
+            if (plan->use_count_table)
+                count_table_flags(ctx, drv, in, plan, vbits, n_int, Mi, ilist.p, im_off_c.p, lv, flags.p, st);
+            else
+                k_flags<<<blocks_for(Mi + 1), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p,
+                                                            lv.members.p, in->d_sketch, ell, nsk.p, plan->flag_dist,
+                                                            flags.p);
             CPSJ_LAUNCH_CHECK();
             drv.scan(flags.p, fscan.p, Mi + 1);
             surv.alloc(std::max<int64_t>(1, Mi), st);

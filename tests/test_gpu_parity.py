@@ -33,8 +33,10 @@ def _cuda():
 def _params(z, k):
     from paper_1707_06814_b200 import CPSJoinParams
     lam, ell, seed, reps, limit, eps, delta, cap = z[f"j{k}_params"].tolist()
+    ct_key = f"j{k}_use_count_table"
+    ct = bool(int(z[ct_key])) if ct_key in z.files else False
     return CPSJoinParams(lambda_=lam, ell=int(ell), seed=int(seed), repetitions=int(reps), limit=int(limit),
-                         epsilon=eps, delta=delta, depth_cap=int(cap))
+                         epsilon=eps, delta=delta, depth_cap=int(cap), use_count_table=ct)
 
 
 def _check_join(res, z, k):
@@ -91,7 +93,8 @@ def test_minhash_high_word_ties_resolved_on_full_hash():
     assert np.array_equal(got, O.minhash(tok, off, tables))
 
 
-EMB_FIXTURES = ["planted_small", "planted_880", "dense_cluster", "c1_sample", "c3_sample", "c4_sample"]
+EMB_FIXTURES = ["planted_small", "planted_880", "dense_cluster", "c1_sample", "c3_sample", "c4_sample",
+                "ct_planted", "ct_dense", "ct_c1_sample"]
 
 
 @pytest.mark.parametrize("name", EMB_FIXTURES)
@@ -236,16 +239,33 @@ def test_no_pairs_and_degenerate_sizes():
     assert pairs == []
 
 
-def test_deterministic_and_count_table_gap():
+def test_deterministic_given_seed():
     from paper_1707_06814_b200 import CPSJoinParams, EmbeddingParams, cpsjoin_self, embed_dataset
     ds = _planted(300, 25, 51)
-    p1, c1 = cpsjoin_self(embed_dataset(EmbeddingParams(seed=9), ds), CPSJoinParams(lambda_=0.6, seed=9))
-    p2, c2 = cpsjoin_self(embed_dataset(EmbeddingParams(seed=9), ds), CPSJoinParams(lambda_=0.6, seed=9))
-    assert [(p.a, p.b, p.similarity) for p in p1] == [(p.a, p.b, p.similarity) for p in p2]
-    assert c1 == c2
-    with pytest.raises(NotImplementedError):
-        cpsjoin_self(embed_dataset(EmbeddingParams(seed=9), ds),
-                     CPSJoinParams(lambda_=0.6, seed=9, use_count_table=True))
+    for ct in (False, True):
+        p1, c1 = cpsjoin_self(embed_dataset(EmbeddingParams(seed=9), ds),
+                              CPSJoinParams(lambda_=0.6, seed=9, use_count_table=ct))
+        p2, c2 = cpsjoin_self(embed_dataset(EmbeddingParams(seed=9), ds),
+                              CPSJoinParams(lambda_=0.6, seed=9, use_count_table=ct))
+        assert [(p.a, p.b, p.similarity) for p in p1] == [(p.a, p.b, p.similarity) for p in p2]
+        assert c1 == c2
+
+
+@pytest.mark.parametrize("cfg,scale,limit", [(1, 0.2, 250), (3, 0.01, 60), (1, 0.05, 20)])
+def test_count_table_flag_rule_matches_oracle(cfg, scale, limit):
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    from paper_1707_06814_b200.workloads import generate
+    w = generate(cfg, scale=scale)
+    emb = embed_dataset(EmbeddingParams(t=128, seed=7), Dataset.from_csr(w.tokens, w.offsets, w.d))
+    p = CPSJoinParams(lambda_=0.5, seed=3, repetitions=3, limit=limit, use_count_table=True)
+    res = cpsjoin_self_arrays(emb, p)
+    ref = O.self_join(w.tokens, w.offsets, w.sizes, emb.values, emb.sketches(8, 3), 0.5, limit=limit,
+                      repetitions=3, seed=3, use_count_table=True)
+    assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)
+    c = res.counters
+    assert [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members] == \
+        [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members]
 
 
 def test_full_config1_against_oracle_and_exact_truth():

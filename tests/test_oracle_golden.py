@@ -54,7 +54,13 @@ def test_kstar_table(lam, m, expect):
     assert O.kstar(lam, 0.05, m) == expect
 
 
-EMB_FIXTURES = ["planted_small", "planted_880", "dense_cluster", "c1_sample", "c3_sample", "c4_sample"]
+EMB_FIXTURES = ["planted_small", "planted_880", "dense_cluster", "c1_sample", "c3_sample", "c4_sample",
+                "ct_planted", "ct_dense", "ct_c1_sample"]
+
+
+def use_ct(z, k):
+    key = f"j{k}_use_count_table"
+    return bool(int(z[key])) if key in z.files else False
 
 
 def fixture_joins(name):
@@ -76,7 +82,7 @@ def test_oracle_matches_reference_join(name):
         sk = O.sketch(tok, off, mh, bt)
         assert sha(sk) == str(z[f"j{k}_sketch_sha"])
         out = O.self_join(tok, off, sizes, values, sk, lam, epsilon=eps, limit=int(limit), delta=delta,
-                          repetitions=int(reps), seed=int(seed), depth_cap=int(cap))
+                          repetitions=int(reps), seed=int(seed), depth_cap=int(cap), use_count_table=use_ct(z, k))
         assert np.array_equal(out.a, z[f"j{k}_pair_a"])
         assert np.array_equal(out.b, z[f"j{k}_pair_b"])
         assert np.array_equal(out.sims, z[f"j{k}_pair_sim"])  # bit-exact f64
