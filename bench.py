@@ -147,33 +147,64 @@ def workload_dict(w, cfg, R, rec, lam, extra=None):
 
 # -------------------------------------------------------------- CPU (oracle)
 
-def cpu_pipeline_time(cfg_id: int, scale: float, threads: int, reps=None):
-    """Oracle (C port of the reference) on a sample: (sets, seconds, R, recall)."""
-    from oracle import oracle as O
-    from paper_1707_06814_b200.workloads import CONFIGS, generate
-    cfg = CONFIGS[cfg_id]
-    lam = cfg.lambdas[0]
-    w = generate(cfg_id, scale=scale)
-    truth = None
-    if reps is None:
-        truth, _ = O.exact_join(w.tokens, w.offsets, w.d, lam, threads)
-        R, rec = 1, 0.0
-        values = O.minhash(w.tokens, w.offsets, O.embedding_tables(128, cfg.emb_seed), threads)
+def recall_truth(cfg_id: int, scale: float, w, lam: float):
+    """Recall denominator: the exact-join truth file for this workload if one
+    was generated (oracle/make_truth.py), else the planted pairs whose exact
+    Jaccard is >= lambda (a proxy; stated in the output)."""
+    t = load_truth(cfg_id, scale, lam, w.tokens, w.offsets)
+    if t is not None:
+        return t, "exact join (oracle/make_truth.py)"
+    keys = []
+    for a, b in w.planted_pairs.tolist():
+        x = w.tokens[w.offsets[a]:w.offsets[a + 1]]
+        y = w.tokens[w.offsets[b]:w.offsets[b + 1]]
+        inter = len(np.intersect1d(x, y, assume_unique=True))
+        if inter / (len(x) + len(y) - inter) >= lam:
+            keys.append((min(a, b) << 32) | max(a, b))
+    return np.unique(np.array(keys, dtype=np.uint64)), "planted pairs with J >= lambda (proxy, no truth file)"
+
+
+class CpuArm:
+    """The C oracle (port of the reference path) on one workload, all threads."""
+
+    def __init__(self, w, cfg, threads: int):
+        from oracle import oracle as O
+        self.O, self.w, self.cfg, self.threads = O, w, cfg, threads
+        self.lam = cfg.lambdas[0]
+
+    def pipeline(self, reps: int):
+        """embed_dataset + sketches + cpsjoin_self, timed: (seconds, JoinOut)."""
+        t0 = time.perf_counter()
+        _, _, out = self.O.full_pipeline(self.w.tokens, self.w.offsets, self.w.sizes, lam=self.lam, t=128,
+                                         emb_seed=self.cfg.emb_seed, ell=self.cfg.ell, seed=self.cfg.join_seed,
+                                         repetitions=reps, threads=self.threads)
+        return time.perf_counter() - t0, out
+
+    def choose_reps(self, truth):
+        O, w, cfg = self.O, self.w, self.cfg
+        values = O.minhash(w.tokens, w.offsets, O.embedding_tables(128, cfg.emb_seed), self.threads)
         mh, bt = O.sketch_tables(cfg.ell, cfg.join_seed)
-        sk = O.sketch(w.tokens, w.offsets, mh, bt, threads)
+        sk = O.sketch(w.tokens, w.offsets, mh, bt, self.threads)
+        rec = 0.0
         for R in range(1, 11):
-            out = O.self_join(w.tokens, w.offsets, w.sizes, values, sk, lam, repetitions=R, seed=cfg.join_seed,
-                              threads=threads)
+            out = O.self_join(w.tokens, w.offsets, w.sizes, values, sk, self.lam, repetitions=R,
+                              seed=cfg.join_seed, threads=self.threads)
             rec = float(np.isin(truth, out.keys).mean()) if len(truth) else 1.0
             if rec >= cfg.recall:
                 break
-        reps = R
-    t0 = time.perf_counter()
-    values, sk, out = O.full_pipeline(w.tokens, w.offsets, w.sizes, lam=lam, t=128, emb_seed=cfg.emb_seed,
-                                      ell=cfg.ell, seed=cfg.join_seed, repetitions=reps, threads=threads)
-    dt = time.perf_counter() - t0
-    rec = float(np.isin(truth, out.keys).mean()) if truth is not None and len(truth) else None
-    return w.n, dt, reps, rec
+        return R, rec
+
+
+def cpu_sample_scale(cfg_id: int, threads: int, budget_s: float = 15.0) -> float:
+    """Largest workload fraction whose oracle pipeline should take about
+    `budget_s` seconds, from a timed 10k-set calibration run (1.0 = full)."""
+    from paper_1707_06814_b200.workloads import CONFIGS, generate
+    cfg = CONFIGS[cfg_id]
+    n_full = cfg.n_background + cfg.n_planted
+    s0 = min(1.0, 10_000 / n_full)
+    w0 = generate(cfg_id, scale=s0)
+    dt, _ = CpuArm(w0, cfg, threads).pipeline(3)
+    return min(1.0, s0 * budget_s / max(dt, 1e-3))
 
 
 def cpu_threads() -> int:
@@ -184,27 +215,31 @@ def cpu_threads() -> int:
 
 
 def run_reference(args, rank: int, world: int):
-    from paper_1707_06814_b200.workloads import CONFIGS
+    from paper_1707_06814_b200.workloads import CONFIGS, generate
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
     threads = cpu_threads()
-    scale = args.cpu_scale or min(1.0, 25_000 / (cfg.n_background + cfg.n_planted)) * args.scale
-    n, _, R, rec = cpu_pipeline_time(args.config, scale, threads)  # warm-up run also fixes R
-    for _ in range(max(0, args.warmup - 1)):
-        cpu_pipeline_time(args.config, scale, threads, reps=R)
-    times = []
-    for _ in range(args.steps):
-        times.append(cpu_pipeline_time(args.config, scale, threads, reps=R)[1])
+    scale = args.cpu_scale or cpu_sample_scale(args.config, threads) * args.scale
+    if scale > 0.8 * args.scale:
+        scale = args.scale  # the whole workload fits the time budget
+    w = generate(args.config, scale=scale)
+    truth, truth_src = recall_truth(args.config, scale, w, cfg.lambdas[0])
+    arm = CpuArm(w, cfg, threads)
+    R, rec = arm.choose_reps(truth)
+    for _ in range(max(0, min(args.warmup, 1))):  # one warm-up: the port has no JIT or caches to warm
+        arm.pipeline(R)
+    times = [arm.pipeline(R)[0] for _ in range(args.steps)]
     total = sum(times)
-    value = n * len(times) / total
-    sample = f"{cfg.name} scaled x{scale:g}: {n} sets, R={R} (recall {rec:.3f} on the sample's exact join)"
+    value = w.n * len(times) / total
+    sample = (f"{cfg.name} x{scale:g}: {w.n} sets, embed+sketch+join R={R} (recall {rec:.3f} vs {truth_src}), "
+              f"{total / len(times):.2f} s per step, {threads} threads")
     line = {"metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64 integer hashing, f64 verify",
-            "data": "synthetic (seeded generator for BASELINE.json config, sampled)",
-            "config": {"workload": f"{cfg.name} sample", "n_sets": n, "repetitions": R, "recall": rec,
-                       "lambda": cfg.lambdas[0], "ell": cfg.ell, "t": 128},
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded generator for the BASELINE.json config)",
+            "config": {"workload": f"{cfg.name} x{scale:g}", "n_sets": int(w.n), "repetitions": R, "recall": rec,
+                       "recall_truth": truth_src, "lambda": cfg.lambdas[0], "ell": cfg.ell, "t": 128},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "sets/s", "cores": threads, "kind": "port",
                              "sample": sample},
@@ -241,15 +276,12 @@ def run_ours(args, rank: int, world: int):
     eparams = EmbeddingParams(t=128, seed=cfg.emb_seed)
 
     # repetitions: smallest R reaching the target recall (prefix-stable seeds)
-    truth = load_truth(args.config, args.scale, lam, w.tokens, w.offsets)
+    truth, truth_src = recall_truth(args.config, args.scale, w, lam)
     emb0 = embed_device_csr(eparams, d_tok, d_off, w.d, host_csr=(w.tokens, w.offsets))
     if args.reps != "auto":
         R = int(args.reps)
         res = cpsjoin_self_arrays(emb0, CPSJoinParams(lambda_=lam, ell=cfg.ell, seed=cfg.join_seed, repetitions=R))
         rec = recall_of(res.a, res.b, truth)
-    elif truth is None:
-        R, rec = 3, float("nan")
-        log("no exact-join truth for this workload: R fixed at 3, recall unmeasured")
     else:
         for R in range(1, 11):
             res = cpsjoin_self_arrays(emb0, CPSJoinParams(lambda_=lam, ell=cfg.ell, seed=cfg.join_seed,
@@ -344,18 +376,26 @@ def run_ours(args, rank: int, world: int):
     d2h = int(len(res_e2e.a) * 16)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the same algorithm on the host: the oracle port, all threads, same
+        # R (bit-identical output, so the same recall) on the whole workload
+        # when it fits the ~15 s budget, else on a scaled sample
         threads = cpu_threads()
-        scale = args.cpu_scale or min(1.0, 25_000 / (cfg.n_background + cfg.n_planted)) * args.scale
-        cn, cdt, cR, crec = cpu_pipeline_time(args.config, scale, threads)
-        cpu = {"value": cn / cdt, "unit": "sets/s", "cores": threads, "kind": "port",
-               "sample": f"{cfg.name} scaled x{scale:g}: {cn} sets, embed+sketch+join R={cR} "
-                         f"(recall {crec:.3f} on the sample's exact join), {cdt:.1f} s"}
+        cscale = args.cpu_scale or cpu_sample_scale(args.config, threads) * args.scale
+        if cscale > 0.8 * args.scale:
+            cscale = args.scale
+        cw = w if cscale == args.scale else generate(args.config, scale=cscale)
+        cdt, cout = CpuArm(cw, cfg, threads).pipeline(R)
+        crec = recall_of(cout.a, cout.b, truth) if cw is w else None
+        cpu = {"value": cw.n / cdt, "unit": "sets/s", "cores": threads, "kind": "port",
+               "sample": f"{cfg.name} x{cscale:g}: {cw.n} sets, embed+sketch+join R={R}"
+                         + (f" (recall {crec:.3f})" if crec is not None else "") + f", {cdt:.2f} s"}
     line = {
         "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded generator for BASELINE.json config; Mann et al. datasets unavailable)",
-        "config": workload_dict(w, cfg, R, rec, lam, {"parallelism": f"reps sharded over {world} GPU(s)"}),
+        "config": workload_dict(w, cfg, R, rec, lam, {"parallelism": f"reps sharded over {world} GPU(s)",
+                                                     "recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
                      "frac": achieved / float(peaks["hbm_gbs"]), "traffic": None,
                      "kernel": "k_minhash<L> sketch launch (K1, 64*ell functions)",
