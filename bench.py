@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--reps", default="auto")
     ap.add_argument("--cpu-scale", type=float, default=None, help="CPU sample scale (default: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # nvidia-smi in its own process at 500 ms; an in-process NVML thread
+    # contends for the GIL with the launch path and slows the step (measured)
+    ap.add_argument("--clock-source", default="smi", choices=["nvml", "smi"])
+    ap.add_argument("--clock-ms", type=int, default=500)
     return ap.parse_args()
 
 
@@ -55,19 +59,72 @@ def log(*a):
 
 # ------------------------------------------------------------ clock sampling
 
+class NvmlClockSampler:
+    """SM clock + clock-event reasons polled in-process through NVML (the
+    recipe's nvidia-smi fields) -- much lighter on the device than a polling
+    nvidia-smi process, whose queries stall a busy GPU measurably."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, gpu: int, interval_s: float = 0.25):
+        self.gpu, self.interval = gpu, interval_s
+        self.samples = []
+        self._stop = None
+
+    def __enter__(self):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+        except Exception:
+            self.nv = None
+            return self
+        self._stop = threading.Event()
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append((self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM),
+                                         self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+                except Exception:
+                    pass
+                self._stop.wait(self.interval)
+
+        self.th = threading.Thread(target=loop, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._stop is not None:
+            self._stop.set()
+            self.th.join(timeout=5)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": "unavailable"}
+        reasons = sorted({k for _, r in self.samples for k, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "NVML (in-process, 250 ms)"}
+
+
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, interval_ms: int = 200):
         self.gpu = gpu
         self.proc = None
+        self.interval_ms = interval_ms
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -334,10 +391,11 @@ def run_ours(args, rank: int, world: int):
         step_e2e()
     k1_events.clear()
     launches0 = ctx_launch_count(ctx)
-    with ClockSampler(dev.index) as clk:
-        # let nvidia-smi finish initialising NVML before the timed region;
-        # its start-up stalls the device for a few hundred ms
-        time.sleep(1.5)
+    sampler = ClockSampler(dev.index, args.clock_ms) if args.clock_source == "smi" else \
+        NvmlClockSampler(dev.index, args.clock_ms / 1e3)
+    with sampler as clk:
+        # let the sampler finish initialising before the timed region
+        time.sleep(1.0)
         step_device()
         ms_dev, res = timed(step_device, args.steps)
         launches = ctx_launch_count(ctx) - launches0
