@@ -112,7 +112,9 @@ class NvmlClockSampler:
 
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    # the recipe's clock fields minus power.draw (whose query was the one
+    # that stalled the device mid-step in our measurements)
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks.mem,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
