@@ -279,9 +279,17 @@ def run_reference(args, rank: int, world: int):
         return
     cfg = CONFIGS[args.config]
     threads = cpu_threads()
-    scale = args.cpu_scale or cpu_sample_scale(args.config, threads) * args.scale
-    if scale > 0.8 * args.scale:
-        scale = args.scale  # the whole workload fits the time budget
+    # the GPU arm's exact workload when its recall truth is on file (c2: ~10 s
+    # per step on 16 host threads), else a sample sized to ~15 s per step
+    from oracle.make_truth import truth_path
+    if args.cpu_scale:
+        scale = args.cpu_scale
+    elif os.path.exists(truth_path(args.config, args.scale, cfg.lambdas[0])):
+        scale = args.scale
+    else:
+        scale = cpu_sample_scale(args.config, threads) * args.scale
+        if scale > 0.8 * args.scale:
+            scale = args.scale
     w = generate(args.config, scale=scale)
     truth, truth_src = recall_truth(args.config, scale, w, cfg.lambdas[0])
     arm = CpuArm(w, cfg, threads)
