@@ -459,6 +459,204 @@ static void launch_minhash_keyed(cpsj_ctx *ctx, const cpsj_family *fam, const ui
     ctx->launches++;
 }
 
+// ---------------------------------------------------------------------
+// 16-bit keyed variant (key bytes L <= 3, sets <= 65536 tokens): the
+// shared tables keep only the top 16 bits of each hash, so one LDS.64 per
+// lane fetches FOUR functions' entries (f = lane, +32, +64, +96 of a
+// 128-function chunk) and both the shared-memory traffic and the per-token
+// address work per evaluation halve.  Keys are (hash16 << 16) | position;
+// first/last minimum tie detection as in k_minhash_keyed.  A tie on the
+// 16 compared bits (p ~ |x| / 2^16 per set and function) re-resolves that
+// function on the full 64-bit hash, so the result stays bit-exact.
+constexpr uint32_t K16_MASK = 0xFFFFu;
+
+template <int L>
+__device__ __forceinline__ uint2 key_quad(uint32_t tok, uint32_t lane_base) {
+    uint2 h = lds64(lane_base + __byte_perm(tok, 0u, 0x4404));
+    if (L > 1) {
+        const uint2 v = lds64(lane_base + 65536u + (tok & 0xFF00u));
+        h.x ^= v.x;
+        h.y ^= v.y;
+    }
+    if (L > 2) {
+        const uint2 v = lds64(lane_base + 131072u + __byte_perm(tok, 0u, 0x4424));
+        h.x ^= v.x;
+        h.y ^= v.y;
+    }
+    return h;
+}
+
+__device__ __forceinline__ bool key16_tie(const KeyMin &k) {
+    return (k.first & K16_MASK) != K16_MASK - (k.last & K16_MASK);
+}
+
+// exact argmin of function f over a set whose minimal top-16 hash bits are
+// m16: warp-cooperative (lane per token), full 64-bit compare, smaller token
+// on a full tie (hashing.py:124); every lane returns the winner
+__device__ __noinline__ uint32_t warp_resolve16(const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+                                                int f, uint32_t m16, const uint32_t *__restrict__ tokens,
+                                                int64_t beg, int len, int lane) {
+    uint64_t bg = ~0ull;
+    uint32_t bt = 0xFFFFFFFFu;
+    const size_t base = (size_t)f * 1024;
+    for (int i = lane; i < len; i += 32) {
+        const uint32_t tk = __ldg(tokens + beg + i);
+        const uint32_t b0 = tk & 255, b1 = (tk >> 8) & 255, b2 = (tk >> 16) & 255, b3 = tk >> 24;
+        const uint32_t h = __ldg(hi + base + b0) ^ __ldg(hi + base + 256 + b1) ^ __ldg(hi + base + 512 + b2) ^
+                           __ldg(hi + base + 768 + b3);
+        if ((h >> 16) == m16) {
+            const uint32_t l = __ldg(lo + base + b0) ^ __ldg(lo + base + 256 + b1) ^ __ldg(lo + base + 512 + b2) ^
+                               __ldg(lo + base + 768 + b3);
+            const uint64_t g = ((uint64_t)h << 32) | l;
+            if (g < bg || (g == bg && tk < bt)) {
+                bg = g;
+                bt = tk;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t og = __shfl_xor_sync(0xffffffffu, bg, o);
+        const uint32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+        if (og < bg || (og == bg && ot < bt)) {
+            bg = og;
+            bt = ot;
+        }
+    }
+    return bt;
+}
+
+template <int L>
+__global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
+    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
+    const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+    const uint32_t *__restrict__ bitmask, int F, uint32_t *__restrict__ values,
+    uint64_t *__restrict__ sketch) {
+    // [L][256][32] x uint2 {f0 << 16 | f32, f64 << 16 | f96} (16-bit hashes), then bit masks
+    extern __shared__ uint2 tab2[];
+    uint32_t *bm_s = reinterpret_cast<uint32_t *>(tab2 + L * 256 * 32);  // [128][33]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lane_base = (uint32_t)__cvta_generic_to_shared(tab2) + ((uint32_t)lane << 3);
+    const int nchunks = (F + 127) >> 7;
+    const int words32 = F >> 5;
+    const int64_t s_first = (int64_t)blockIdx.x * K1W_WARPS + warp, s_step = (int64_t)gridDim.x * K1W_WARPS;
+    for (int c = 0; c < nchunks; ++c) {
+        __syncthreads();
+        if (sketch != nullptr) {
+            for (int e = threadIdx.x; e < 128 * 32; e += K1W_THREADS) {
+                const int fl = e >> 5, w = e & 31, fn = (c << 7) + fl;
+                bm_s[fl * 33 + w] = fn < F ? bitmask[(size_t)fn * 32 + w] : 0u;
+            }
+        }
+        for (int e = threadIdx.x; e < L * 256 * 32; e += K1W_THREADS) {
+            const int k = e >> 13, b = (e >> 5) & 255, ln = e & 31;
+            uint32_t h16[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int fn = (c << 7) + ln + 32 * q;
+                uint32_t v = 0;
+                if (fn < F) {
+                    const size_t base = (size_t)fn * 1024;
+                    v = hi[base + k * 256 + b];
+                    if (k == L - 1)
+                        for (int kk = L; kk < 4; ++kk) v ^= hi[base + kk * 256];
+                }
+                h16[q] = v >> 16;
+            }
+            tab2[e] = make_uint2((h16[0] << 16) | h16[1], (h16[2] << 16) | h16[3]);
+        }
+        __syncthreads();
+        int fn[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fn[q] = (c << 7) + lane + 32 * q;
+        int64_t nbeg = 0, nend = 0;
+        if (s_first < n) {
+            nbeg = offsets[s_first];
+            nend = offsets[s_first + 1];
+        }
+        for (int64_t s = s_first; s < n; s += s_step) {
+            const int64_t beg = nbeg, end = nend;
+            if (s + s_step < n) {
+                nbeg = offsets[s + s_step];
+                nend = offsets[s + s_step + 1];
+            }
+            const int len = (int)(end - beg);
+            uint32_t tk[4] = {0, 0, 0, 0};
+            if (len > (int)K16_MASK + 1) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (fn[q] < F) tk[q] = resolve_tie(hi, lo, fn[q], tokens, beg, end);
+            } else if (len > 0) {
+                KeyMin km[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) km[q] = KeyMin{0xFFFFFFFFu, 0xFFFFFFFFu};
+                for (int base = 0; base < len; base += 32) {
+                    const int cnt = len - base < 32 ? len - base : 32;
+                    const uint32_t mine = lane < cnt ? __ldg(tokens + beg + base + lane) : 0u;
+#pragma unroll 4
+                    for (int j = 0; j < cnt; ++j) {
+                        const uint32_t tok = __shfl_sync(0xffffffffu, mine, j);
+                        const uint2 h = key_quad<L>(tok, lane_base);
+                        const uint32_t p = (uint32_t)(base + j);
+                        const uint32_t q = K16_MASK - p;
+                        key_update(km[0], h.x & 0xFFFF0000u, p, q);
+                        key_update(km[1], h.x << 16, p, q);
+                        key_update(km[2], h.y & 0xFFFF0000u, p, q);
+                        key_update(km[3], h.y << 16, p, q);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    tk[q] = __ldg(tokens + beg + (km[q].first & K16_MASK));
+                    // ties on the 16 compared bits: the whole warp rescans the
+                    // set for each tied function, lanes over tokens, and only
+                    // tokens sharing the minimal 16 bits evaluate the full
+                    // 64-bit hash; a warp argmin (hash, then token) settles it
+                    unsigned tied = __ballot_sync(0xffffffffu, key16_tie(km[q]) && fn[q] < F);
+                    while (tied) {
+                        const int src = __ffs(tied) - 1;
+                        tied &= tied - 1;
+                        const int f = __shfl_sync(0xffffffffu, fn[q], src);
+                        const uint32_t m16 = __shfl_sync(0xffffffffu, km[q].first >> 16, src);
+                        const uint32_t tbest = warp_resolve16(hi, lo, f, m16, tokens, beg, len, lane);
+                        if (lane == src) tk[q] = tbest;
+                    }
+                }
+            }
+            if (values != nullptr) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (fn[q] < F) values[s * F + fn[q]] = tk[q];
+            }
+            if (sketch != nullptr) {
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    w[q] = __ballot_sync(0xffffffffu, len > 0 && fn[q] < F && sketch_bit_s(bm_s, lane + 32 * q, tk[q]));
+                if (lane < 4) {
+                    // u32 words (c*4 + lane) of the row; F % 64 == 0 so they pair into u64 words
+                    const uint32_t mine_w = lane == 0 ? w[0] : lane == 1 ? w[1] : lane == 2 ? w[2] : w[3];
+                    if ((c << 2) + lane < words32)
+                        reinterpret_cast<uint32_t *>(sketch)[s * words32 + (c << 2) + lane] = mine_w;
+                }
+            }
+        }
+    }
+}
+
+template <int L>
+static void launch_minhash_k16(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
+                               int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
+    const int smem = L * 256 * 32 * 8 + (sketch != nullptr ? 128 * 33 * 4 : 0);
+    CPSJ_CUDA(cudaFuncSetAttribute(k_minhash_k16<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
+    ProfScope prof(ctx, PROF_K1, stream);
+    k_minhash_k16<L><<<grid, K1W_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask, fam->F,
+                                                          values, sketch);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
 template <int L>
 static void launch_minhash64(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
                              int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
@@ -540,10 +738,19 @@ int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_toke
         }
         return 0;
     }
+    const char *k32 = getenv("CPSJ_K1_KEY32");  // A/B switch for the 32-bit-key kernel
+    if (k32 != nullptr && k32[0] == '1' && L < 4) {
+        switch (L) {
+            case 1: launch_minhash_keyed<1>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+            case 2: launch_minhash_keyed<2>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+            default: launch_minhash_keyed<3>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+        }
+        return 0;
+    }
     switch (L) {
-        case 1: launch_minhash_keyed<1>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-        case 2: launch_minhash_keyed<2>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-        case 3: launch_minhash_keyed<3>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+        case 1: launch_minhash_k16<1>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+        case 2: launch_minhash_k16<2>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
+        case 3: launch_minhash_k16<3>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
         default: launch_minhash<4>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
     }
     return 0;
