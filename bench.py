@@ -38,7 +38,7 @@ METRIC = "self-join sets/s at lambda=0.5, >=90% recall (embed + sketch + join)"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
@@ -49,7 +49,7 @@ def parse():
     # nvidia-smi in its own process at 500 ms; an in-process NVML thread
     # contends for the GIL with the launch path and slows the step (measured)
     ap.add_argument("--clock-source", default="smi", choices=["nvml", "smi"])
-    ap.add_argument("--clock-ms", type=int, default=500)
+    ap.add_argument("--clock-ms", type=int, default=1000)
     return ap.parse_args()
 
 
@@ -435,7 +435,10 @@ def run_ours(args, rank: int, world: int):
     L = 1 if w.d <= 1 << 8 else 2 if w.d <= 1 << 16 else 3 if w.d <= 1 << 24 else 4
     f_clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     evals = nnz * 64 * cfg.ell
-    lookup_peak = 148 * f_clk * 32 / L   # one conflict-free 32-lane LDS wavefront per clk per SM
+    # K1 keeps 16-bit hash entries in shared memory: L lookups x 2 B per
+    # evaluation against the measured 126 B/clk/SM conflict-free LDS rate
+    # (profiles/int_peaks_r01.json: LDS.64 15.76 lanes x 8 B per clk per SM)
+    lookup_peak = 148 * f_clk * 126.0 / (2 * L)
     k4_ms = prof["k4_leaf"][0] + prof["point"][0]
     pre = res.counters.pre_candidates
     pairs_per_s = pre / (k4_ms / 1e3) if k4_ms > 0 else None
@@ -469,7 +472,7 @@ def run_ours(args, rank: int, world: int):
                      "kernel": "k_minhash<L> sketch launch (K1, 64*ell functions)",
                      "algorithmic_bytes": sk_bytes, "avg_launch_ms": k1_sk_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
-        "roofline_smem": {"bound": "shared-memory lookups (LDS.32, 32 lanes/clk/SM)",
+        "roofline_smem": {"bound": "shared-memory lookups (16-bit entries, 126 B/clk/SM measured LDS rate)",
                           "achieved_evals_per_s": evals / (k1_sk_ms / 1e3), "peak_evals_per_s": lookup_peak,
                           "frac": evals / (k1_sk_ms / 1e3) / lookup_peak, "key_bytes": L,
                           "values_launch_ms": k1_val_ms},

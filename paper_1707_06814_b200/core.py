@@ -47,6 +47,7 @@ class Dataset:
         self._records = records if _csr is None else None
         self._csr = None
         self._freq = None
+        self._nonempty = True if _csr is not None else None
 
     # -- construction ---------------------------------------------------
     @classmethod
@@ -83,6 +84,14 @@ class Dataset:
         """Trusted fast path: rows already sorted, unique, >= 2 tokens and
         pairwise distinct (what from_token_lists would produce with ``d``)."""
         return cls(d=d, _csr=(tokens, offsets))
+
+    @property
+    def rows_nonempty(self) -> bool:
+        """Every record is non-empty (guaranteed by from_token_lists and the
+        trusted from_csr; checked once for hand-built record lists)."""
+        if self._nonempty is None:
+            self._nonempty = bool(np.all(np.diff(self.offsets) > 0))
+        return self._nonempty
 
     # -- reference surface ----------------------------------------------
     def __len__(self) -> int:

@@ -333,7 +333,7 @@ def embed_dataset(params: EmbeddingParams, ds: Dataset, sketch: tuple[int, int] 
     """
     n = len(ds)
     if n > 0 and ((chunks is None and n >= _PIPELINE_MIN_SETS) or (chunks is not None and chunks > 1)):
-        return _embed_pipelined(params, ds, sketch, min(chunks or 8, n))
+        return _embed_pipelined(params, ds, sketch, min(chunks or 4, n))
     t = params.t
     tok, off = ds.flat_tokens()
     tok = np.ascontiguousarray(tok, dtype=np.uint32)
@@ -368,7 +368,8 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
     tok, off = ds.flat_tokens()
     tok = np.ascontiguousarray(tok, dtype=np.uint32)
     off = np.ascontiguousarray(off, dtype=np.int64)
-    if np.any(off[1:] == off[:-1]):
+    # Dataset rows hold >= 2 tokens by construction; other CSR sources are checked
+    if not getattr(ds, "rows_nonempty", False) and np.any(off[1:] == off[:-1]):
         raise ValueError("cannot embed an empty record")
     ctx = Context.get()
     efam = params.device(ctx)
