@@ -124,10 +124,15 @@ class ClockSampler:
         self.interval_ms = interval_ms
 
     def __enter__(self):
+        self.first = []
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # nvidia-smi's start-up (NVML init) stalls a busy device for up to
+            # ~1 s: wait for its first sample before any timed work starts
+            self.first.append(self.proc.stdout.readline())
+            time.sleep(0.3)
         except OSError:
             self.proc = None
         return self
@@ -141,6 +146,7 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
+            # the pre-roll sample is not inside the timed region
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self) -> dict:
@@ -385,11 +391,17 @@ def run_ours(args, rank: int, world: int):
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
         out = None
+        marks = []
         for _ in range(steps):
             out = fn()
+            marks.append(torch.cuda.Event(enable_timing=True))
+            marks[-1].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
         ms = start.elapsed_time(end)
+        per = [a.elapsed_time(b) for a, b in zip([start] + marks[:-1], marks)]
+        log(f"[rank {rank}] {getattr(fn, '__name__', 'step')}: per-step ms min {min(per):.2f} "
+            f"median {statistics.median(per):.2f} max {max(per):.2f}")
         if world > 1:
             t = torch.tensor([ms], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
