@@ -416,9 +416,12 @@ def run_ours(args, rank: int, world: int):
     sampler = ClockSampler(dev.index, args.clock_ms) if args.clock_source == "smi" else \
         NvmlClockSampler(dev.index, args.clock_ms / 1e3)
     with sampler as clk:
-        # let the sampler finish initialising before the timed region
-        time.sleep(1.0)
-        step_device()
+        # nvidia-smi keeps perturbing the device for a while after its first
+        # sample: run untimed steps for 3 s before the timed region
+        t_settle = time.perf_counter()
+        while time.perf_counter() - t_settle < 3.0:
+            step_device()
+            torch.cuda.synchronize()
         ms_dev, res = timed(step_device, args.steps)
         launches = ctx_launch_count(ctx) - launches0
         ms_e2e, res_e2e = timed(step_e2e, args.steps)

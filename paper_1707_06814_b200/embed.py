@@ -333,7 +333,7 @@ def embed_dataset(params: EmbeddingParams, ds: Dataset, sketch: tuple[int, int] 
     """
     n = len(ds)
     if n > 0 and ((chunks is None and n >= _PIPELINE_MIN_SETS) or (chunks is not None and chunks > 1)):
-        return _embed_pipelined(params, ds, sketch, min(chunks or 4, n))
+        return _embed_pipelined(params, ds, sketch, min(chunks or 5, n))
     t = params.t
     tok, off = ds.flat_tokens()
     tok = np.ascontiguousarray(tok, dtype=np.uint32)
@@ -385,7 +385,11 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
     d_vals = torch.empty((n, t), dtype=torch.int32, device=dev)
     d_sk = torch.empty((n, sketch[0]), dtype=torch.int64, device=dev) if sketch is not None else None
     # set-aligned chunk boundaries
-    bounds = np.linspace(0, n, chunks + 1).astype(np.int64)
+    # geometric chunks (1/2^(c-1), ..., 1/4, 1/2 of the sets): the first copy,
+    # which nothing can hide, is small; later copies hide behind compute
+    frac = np.array([0.0] + [2.0 ** -(chunks - 1)] + [2.0 ** -(chunks - k) for k in range(1, chunks)])
+    bounds = np.minimum(np.round(np.cumsum(frac) * n), n).astype(np.int64)
+    bounds[-1] = n
     events = []
     copier.wait_stream(compute)  # destination buffers were allocated on `compute`
     with torch.cuda.stream(copier):
