@@ -422,6 +422,8 @@ def run_ours(args, rank: int, world: int):
         while time.perf_counter() - t_settle < 3.0:
             step_device()
             torch.cuda.synchronize()
+        k1_events.clear()   # K1 launch times over the timed region only
+        launches0 = ctx_launch_count(ctx)
         ms_dev, res = timed(step_device, args.steps)
         launches = ctx_launch_count(ctx) - launches0
         ms_e2e, res_e2e = timed(step_e2e, args.steps)
