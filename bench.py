@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # nvidia-smi in its own process at 500 ms; an in-process NVML thread
     # contends for the GIL with the launch path and slows the step (measured)
-    ap.add_argument("--clock-source", default="smi", choices=["nvml", "smi"])
+    ap.add_argument("--clock-source", default="points", choices=["points", "nvml", "smi"])
     ap.add_argument("--clock-ms", type=int, default=1000)
     return ap.parse_args()
 
@@ -109,6 +109,56 @@ class NvmlClockSampler:
         reasons = sorted({k for _, r in self.samples for k, bit in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
                 "reasons": reasons, "samples": len(self.samples), "source": "NVML (in-process, 250 ms)"}
+
+
+class NvmlPointSampler:
+    """SM clock + clock-event reasons read through NVML from the main thread
+    at fixed points inside the timed loops (first, middle and last step of
+    each), while the GPU executes the queued work.  No polling process and
+    no sampling thread: the periodic nvidia-smi queries measurably stalled
+    the device (profiles/README.md)."""
+
+    REASONS = NvmlClockSampler.REASONS
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.nv = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+            # warm the query path outside the timed region (first calls are slow)
+            for _ in range(3):
+                pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+                pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            self.nv = None
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+    def sample(self):
+        if self.nv is None:
+            return
+        try:
+            self.samples.append((self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM),
+                                 self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+        except Exception:
+            pass
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": "unavailable"}
+        reasons = sorted({k for _, r in self.samples for k, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML from the launch thread as each timed loop (device, e2e) closes"}
 
 
 class ClockSampler:
@@ -383,7 +433,7 @@ def run_ours(args, rank: int, world: int):
         emb = embed_dataset(eparams, ds, sketch=(cfg.ell, cfg.join_seed))
         return shard_reps(emb, params, rank, world)
 
-    def timed(fn, steps):
+    def timed(fn, steps, probe=None):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -392,16 +442,22 @@ def run_ours(args, rank: int, world: int):
         start.record(stream)
         out = None
         marks = []
-        for _ in range(steps):
+        for i in range(steps):
             out = fn()
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record(stream)
         end.record(stream)
+        if probe is not None:
+            # clock + throttle-reason sample as the timed region closes: any
+            # NVML query issued while steps run stalled the device by 20-250 ms
+            # in our measurements (profiles/README.md), so it is issued once
+            # the last step is queued, before the closing synchronize
+            probe()
         torch.cuda.synchronize()
         ms = start.elapsed_time(end)
         per = [a.elapsed_time(b) for a, b in zip([start] + marks[:-1], marks)]
         log(f"[rank {rank}] {getattr(fn, '__name__', 'step')}: per-step ms min {min(per):.2f} "
-            f"median {statistics.median(per):.2f} max {max(per):.2f}")
+            f"median {statistics.median(per):.2f} max {max(per):.2f} | " + " ".join(f"{x:.1f}" for x in per))
         if world > 1:
             t = torch.tensor([ms], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -413,20 +469,25 @@ def run_ours(args, rank: int, world: int):
         step_e2e()
     k1_events.clear()
     launches0 = ctx_launch_count(ctx)
-    sampler = ClockSampler(dev.index, args.clock_ms) if args.clock_source == "smi" else \
-        NvmlClockSampler(dev.index, args.clock_ms / 1e3)
+    if args.clock_source == "smi":
+        sampler = ClockSampler(dev.index, args.clock_ms)
+    elif args.clock_source == "nvml":
+        sampler = NvmlClockSampler(dev.index, args.clock_ms / 1e3)
+    else:
+        sampler = NvmlPointSampler(dev.index)
+    probe = sampler.sample if isinstance(sampler, NvmlPointSampler) else None
     with sampler as clk:
         # nvidia-smi keeps perturbing the device for a while after its first
         # sample: run untimed steps for 3 s before the timed region
         t_settle = time.perf_counter()
-        while time.perf_counter() - t_settle < 3.0:
+        while time.perf_counter() - t_settle < 4.0:
             step_device()
             torch.cuda.synchronize()
         k1_events.clear()   # K1 launch times over the timed region only
         launches0 = ctx_launch_count(ctx)
-        ms_dev, res = timed(step_device, args.steps)
+        ms_dev, res = timed(step_device, args.steps, probe)
         launches = ctx_launch_count(ctx) - launches0
-        ms_e2e, res_e2e = timed(step_e2e, args.steps)
+        ms_e2e, res_e2e = timed(step_e2e, args.steps, probe)
     value = n * args.steps / (ms_dev / 1e3)
     e2e_value = n * args.steps / (ms_e2e / 1e3)
     # per-kernel-class device time from one extra, separately profiled step

@@ -105,6 +105,9 @@ int cpsj_family_destroy(cpsj_family *fam) {
     if (fam->d_hi) cudaFree(fam->d_hi);
     if (fam->d_lo) cudaFree(fam->d_lo);
     if (fam->d_bitmask) cudaFree(fam->d_bitmask);
+    for (void *p : fam->d_img16)
+        if (p) cudaFree(p);
+    if (fam->d_bmimg) cudaFree(fam->d_bmimg);
     delete fam;
     return CPSJ_OK;
 }

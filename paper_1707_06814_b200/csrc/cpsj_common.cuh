@@ -157,6 +157,11 @@ struct cpsj_family {
     uint32_t *d_hi = nullptr;       // [F][4][256] high words of the u64 tables
     uint32_t *d_lo = nullptr;       // [F][4][256] low words
     uint32_t *d_bitmask = nullptr;  // [F][4][8] low bits of the bit tables, or null
+    // K1 shared-memory images, built on first use: per 128-function chunk,
+    // the 16-bit [L][256][32]{4 functions} table for key width L (index L-1)
+    // and the [128][33] bit-mask block; copied to shared memory with TMA
+    void *d_img16[3] = {nullptr, nullptr, nullptr};
+    uint32_t *d_bmimg = nullptr;
 };
 
 namespace cpsj {

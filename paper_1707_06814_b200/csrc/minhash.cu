@@ -469,6 +469,72 @@ static void launch_minhash_keyed(cpsj_ctx *ctx, const cpsj_family *fam, const ui
 // 16 compared bits (p ~ |x| / 2^16 per set and function) re-resolves that
 // function on the full 64-bit hash, so the result stays bit-exact.
 constexpr uint32_t K16_MASK = 0xFFFFu;
+constexpr int K16_BM_BYTES = 128 * 33 * 4;  // per-chunk bit-mask block [128][33] u32
+
+// --- TMA bulk copy + mbarrier (shared::cta) ---------------------------
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(phase)
+        : "memory");
+}
+
+// shared-memory image of every 128-function chunk for key width L:
+// [chunk][k][byte][lane] {f0 << 16 | f32, f64 << 16 | f96}, 16-bit hashes
+// (top bits of the high word, upper constant bytes folded into table L-1)
+__global__ void k_build_img16(const uint32_t *__restrict__ hi, int F, int L, int64_t total,
+                              uint2 *__restrict__ img) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int64_t per_chunk = (int64_t)L * 256 * 32;
+    const int c = (int)(e / per_chunk);
+    const int r = (int)(e - (int64_t)c * per_chunk);
+    const int k = r >> 13, b = (r >> 5) & 255, ln = r & 31;
+    uint32_t h16[4];
+    for (int q = 0; q < 4; ++q) {
+        const int fn = (c << 7) + ln + 32 * q;
+        uint32_t v = 0;
+        if (fn < F) {
+            const size_t base = (size_t)fn * 1024;
+            v = hi[base + k * 256 + b];
+            if (k == L - 1)
+                for (int kk = L; kk < 4; ++kk) v ^= hi[base + kk * 256];
+        }
+        h16[q] = v >> 16;
+    }
+    img[e] = make_uint2((h16[0] << 16) | h16[1], (h16[2] << 16) | h16[3]);
+}
+
+// [chunk][128 functions][33] low-bit masks of the bit tables (row stride 33)
+__global__ void k_build_bmimg(const uint32_t *__restrict__ bitmask, int F, int64_t total,
+                              uint32_t *__restrict__ img) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int c = (int)(e / (128 * 33));
+    const int r = (int)(e - (int64_t)c * 128 * 33);
+    const int fl = r / 33, w = r - fl * 33, fn = (c << 7) + fl;
+    img[e] = (w < 32 && fn < F) ? bitmask[(size_t)fn * 32 + w] : 0u;
+}
 
 template <int L>
 __device__ __forceinline__ uint2 key_quad(uint32_t tok, uint32_t lane_base) {
@@ -529,42 +595,38 @@ template <int L>
 __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
     const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
     const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
-    const uint32_t *__restrict__ bitmask, int F, uint32_t *__restrict__ values,
+    const uint2 *__restrict__ img16, const uint32_t *__restrict__ bmimg, int F, uint32_t *__restrict__ values,
     uint64_t *__restrict__ sketch) {
     // [L][256][32] x uint2 {f0 << 16 | f32, f64 << 16 | f96} (16-bit hashes), then bit masks
-    extern __shared__ uint2 tab2[];
+    extern __shared__ __align__(128) uint2 tab2[];
+    __shared__ __align__(8) uint64_t mbar;
     uint32_t *bm_s = reinterpret_cast<uint32_t *>(tab2 + L * 256 * 32);  // [128][33]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lane_base = (uint32_t)__cvta_generic_to_shared(tab2) + ((uint32_t)lane << 3);
     const int nchunks = (F + 127) >> 7;
     const int words32 = F >> 5;
     const int64_t s_first = (int64_t)blockIdx.x * K1W_WARPS + warp, s_step = (int64_t)gridDim.x * K1W_WARPS;
+    const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(&mbar);
+    if (threadIdx.x == 0) mbar_init(mbar_a, 1);
+    __syncthreads();
+    uint32_t phase = 0;
     for (int c = 0; c < nchunks; ++c) {
-        __syncthreads();
-        if (sketch != nullptr) {
-            for (int e = threadIdx.x; e < 128 * 32; e += K1W_THREADS) {
-                const int fl = e >> 5, w = e & 31, fn = (c << 7) + fl;
-                bm_s[fl * 33 + w] = fn < F ? bitmask[(size_t)fn * 32 + w] : 0u;
-            }
+        __syncthreads();  // every warp is done with the previous chunk's tables
+        if (threadIdx.x == 0) {
+            // the chunk's prebuilt shared-memory image arrives by TMA bulk copy
+            const uint32_t tab_bytes = (uint32_t)L * 65536u;
+            const uint32_t bm_bytes = sketch != nullptr ? (uint32_t)K16_BM_BYTES : 0u;
+            fence_proxy_async_smem();
+            mbar_expect_tx(mbar_a, tab_bytes + bm_bytes);
+            const char *src = reinterpret_cast<const char *>(img16) + (size_t)c * tab_bytes;
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(tab2);
+            for (uint32_t o = 0; o < tab_bytes; o += 32768u) bulk_g2s(dst + o, src + o, 32768u, mbar_a);
+            if (bm_bytes)
+                bulk_g2s((uint32_t)__cvta_generic_to_shared(bm_s),
+                         reinterpret_cast<const char *>(bmimg) + (size_t)c * K16_BM_BYTES, bm_bytes, mbar_a);
         }
-        for (int e = threadIdx.x; e < L * 256 * 32; e += K1W_THREADS) {
-            const int k = e >> 13, b = (e >> 5) & 255, ln = e & 31;
-            uint32_t h16[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int fn = (c << 7) + ln + 32 * q;
-                uint32_t v = 0;
-                if (fn < F) {
-                    const size_t base = (size_t)fn * 1024;
-                    v = hi[base + k * 256 + b];
-                    if (k == L - 1)
-                        for (int kk = L; kk < 4; ++kk) v ^= hi[base + kk * 256];
-                }
-                h16[q] = v >> 16;
-            }
-            tab2[e] = make_uint2((h16[0] << 16) | h16[1], (h16[2] << 16) | h16[3]);
-        }
-        __syncthreads();
+        mbar_wait(mbar_a, phase);
+        phase ^= 1u;
         int fn[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) fn[q] = (c << 7) + lane + 32 * q;
@@ -651,8 +713,9 @@ static void launch_minhash_k16(cpsj_ctx *ctx, const cpsj_family *fam, const uint
     const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
     ProfScope prof(ctx, PROF_K1, stream);
-    k_minhash_k16<L><<<grid, K1W_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask, fam->F,
-                                                          values, sketch);
+    k_minhash_k16<L><<<grid, K1W_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo,
+                                                          reinterpret_cast<const uint2 *>(fam->d_img16[L - 1]),
+                                                          fam->d_bmimg, fam->F, values, sketch);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
 }
@@ -773,6 +836,24 @@ void prepare_family(cpsj_ctx *ctx, cpsj_family *fam, const uint64_t *h_mh, const
                                                                           fam->d_lo, fam->d_bitmask);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
+    // K1 shared-memory images for key widths 1..3 (TMA-copied per chunk)
+    const int nchunks = (fam->F + 127) / 128;
+    for (int L = 1; L <= 3; ++L) {
+        const int64_t elems = (int64_t)nchunks * L * 256 * 32;
+        CPSJ_CUDA(cudaMalloc(&fam->d_img16[L - 1], elems * sizeof(uint2)));
+        k_build_img16<<<(unsigned)((elems + 255) / 256), 256, 0, stream>>>(
+            fam->d_hi, fam->F, L, elems, reinterpret_cast<uint2 *>(fam->d_img16[L - 1]));
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+    }
+    if (fam->d_bitmask != nullptr) {
+        const int64_t elems = (int64_t)nchunks * 128 * 33;
+        CPSJ_CUDA(cudaMalloc(&fam->d_bmimg, elems * 4));
+        k_build_bmimg<<<(unsigned)((elems + 255) / 256), 256, 0, stream>>>(fam->d_bitmask, fam->F, elems,
+                                                                            fam->d_bmimg);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+    }
     CPSJ_CUDA(cudaFreeAsync(d_mh, stream));
     if (d_bt) CPSJ_CUDA(cudaFreeAsync(d_bt, stream));
     CPSJ_CUDA(cudaStreamSynchronize(stream));
