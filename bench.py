@@ -228,6 +228,18 @@ def measured_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
 
 
+def ncu_traffic(cfg: int, launch: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
+    dominant kernel from the committed ncu --set full capture, if it was
+    taken on this config (profiles/ncu_traffic_r01.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"][launch]) if int(d["config"]) == cfg else None
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def load_truth(cfg: int, scale: float, lam: float, tokens, offsets):
     from oracle.make_truth import csr_sha, truth_path
     path = truth_path(cfg, scale, lam)
@@ -546,7 +558,7 @@ def run_ours(args, rank: int, world: int):
         "config": workload_dict(w, cfg, R, rec, lam, {"parallelism": f"reps sharded over {world} GPU(s)",
                                                      "recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
-                     "frac": achieved / float(peaks["hbm_gbs"]), "traffic": None,
+                     "frac": achieved / float(peaks["hbm_gbs"]), "traffic": ncu_traffic(args.config, "sketch"),
                      "kernel": "k_minhash<L> sketch launch (K1, 64*ell functions)",
                      "algorithmic_bytes": sk_bytes, "avg_launch_ms": k1_sk_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
