@@ -1,4 +1,9 @@
-"""Repetition sharding across GPUs (one process per GPU, torch.distributed).
+"""Multi-GPU CPSJoin: set-sharded embedding + repetition sharding (one
+process per GPU, torch.distributed over NCCL).
+
+Embedding is per set: `embed_sharded` runs K1 on each rank's n/W slice of
+the sets and all-gathers the value and sketch rows (NVLink), so the
+dominant preprocessing cost divides by W.
 
 Repetition trees are independent (cpsjoin.py:346-349) and
 their seeds are host-derived and prefix-stable, so rank r runs trees
@@ -37,6 +42,89 @@ def _all_gather_var(x: np.ndarray, device, group=None) -> np.ndarray:
     outs = [torch.zeros_like(buf) for _ in range(world)]
     dist.all_gather(outs, buf, group=group)
     return np.concatenate([o[:s].cpu().numpy() for o, s in zip(outs, sizes)]) if world else x
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int, int]:
+    """Set shard of `rank`: [lo, hi) with a common padded size S."""
+    S = -(-n // world) if n else 0
+    lo = min(n, rank * S)
+    return lo, min(n, lo + S), S
+
+
+def _gpu_k1(eparams, sketch, d_tok, d_off, d, lo, hi, vals_out, sk_out):
+    """K1 over sets [lo, hi) of a device CSR into shard buffers (values
+    skipped when eparams is None, sketches when sketch is None)."""
+    import torch
+
+    from ._native import Context
+    from .hashing import sketch_family
+    ctx = Context.get()
+    n_loc = hi - lo
+    if n_loc <= 0:
+        return
+    max_token = min(int(d) - 1, 0xFFFFFFFF) if d else 0xFFFFFFFF
+    stream = torch.cuda.current_stream().cuda_stream
+    offp = d_off.data_ptr() + 8 * lo
+    if eparams is not None:
+        ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, eparams.device(ctx).handle, d_tok.data_ptr(), offp,
+                                              n_loc, max_token, vals_out.data_ptr(), None, stream))
+    if sketch is not None:
+        ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, sketch_family(*sketch).device(ctx).handle,
+                                              d_tok.data_ptr(), offp, n_loc, max_token, None, sk_out.data_ptr(),
+                                              stream))
+
+
+def _gather_rows(shard, world: int, group=None):
+    """All-gather equal-size row shards into one (world * S, ...) tensor."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world * shard.shape[0],) + tuple(shard.shape[1:]), dtype=shard.dtype, device=shard.device)
+        dist.all_gather_into_tensor(out, shard.contiguous(), group=group)
+        return out
+    parts = [torch.empty_like(shard) for _ in range(world)]
+    dist.all_gather(parts, shard.contiguous(), group=group)
+    return torch.cat(parts)
+
+
+def embed_sharded(eparams, d_tok, d_off, d: int, sketch, rank: int, world: int, group=None, local_k1=None):
+    """Set-sharded embedding: rank r runs K1 (values and, with ``sketch =
+    (ell, seed)``, the sketches) on its n/W slice of the sets, and one
+    all-gather per array replicates the (n, t) values and (n, ell) sketches
+    on every rank (the join's node sketches, splits and BruteForce read any
+    row).  Every rank holds the full CSR: verification reads any row too.
+    Returns (values, sketches) as device tensors of n rows."""
+    import torch
+    n = int(d_off.shape[0]) - 1
+    lo, hi, S = shard_range(n, rank, world)
+    vals = torch.zeros((max(S, 1), eparams.t if eparams else 1), dtype=torch.int32, device=d_tok.device)
+    sk = torch.zeros((max(S, 1), sketch[0] if sketch else 1), dtype=torch.int64, device=d_tok.device)
+    (local_k1 or _gpu_k1)(eparams, sketch, d_tok, d_off, d, lo, hi, vals, sk)
+    if world <= 1:
+        return (vals[:n] if eparams else None), (sk[:n] if sketch else None)
+    all_vals = _gather_rows(vals, world, group)[:n] if eparams else None
+    all_sk = _gather_rows(sk, world, group)[:n] if sketch else None
+    return all_vals, all_sk
+
+
+def embedded_from_parts(eparams, d_tok, d_off, d: int, values, sketches, sketch_key=None, host_csr=None):
+    """EmbeddedDataset over device tensors produced by embed_sharded."""
+    import torch
+
+    from .embed import EmbeddedDataset
+    n = int(d_off.shape[0]) - 1
+    emb = EmbeddedDataset(None, None, None, eparams.t, eparams.seed, None, None, np.arange(n, dtype=np.int64))
+    emb._dev.update(values=values, tokens=d_tok, offsets=d_off)
+    emb._dev["sizes"] = (d_off[1:] - d_off[:-1]).to(torch.int32)
+    emb._n = n
+    emb._width = int(d)
+    emb._ids_checked, emb._ids_ok = (id(emb.source_ids), n), True
+    emb._sizes_fn = lambda: emb._dev["sizes"].cpu().numpy().astype(np.int64)
+    if host_csr is not None:
+        emb._csr_arrays = (host_csr[0], host_csr[1], int(d))
+    if sketches is not None and sketch_key is not None:
+        emb._dev_sketch[tuple(sketch_key)] = sketches
+    return emb
 
 
 def merge_results(parts_keys: np.ndarray, parts_sims: np.ndarray):

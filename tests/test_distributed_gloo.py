@@ -117,6 +117,71 @@ def test_two_rank_rep_sharding_equals_single_process():
         assert c == [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members]
 
 
+def _oracle_k1(w):
+    """CPU stand-in for the K1 launch of one rank (test only)."""
+    import torch
+
+    def k1(eparams, sketch, d_tok, d_off, d, lo, hi, vals_out, sk_out):
+        off = w.offsets[lo:hi + 1]
+        tok = w.tokens[off[0]:off[-1]]
+        rel = off - off[0]
+        vals_out[:hi - lo] = torch.from_numpy(O.minhash(tok, rel, eparams.tables, 1).view(np.int32))
+        if sketch is not None:
+            mh, bt = O.sketch_tables(*sketch)
+            sk_out[:hi - lo] = torch.from_numpy(O.sketch(tok, rel, mh, bt, 1).view(np.int64))
+    return k1
+
+
+def _shard_main(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_06814_b200.distributed import embed_sharded
+    from paper_1707_06814_b200.embed import EmbeddingParams
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = _workload()
+        ep = EmbeddingParams(t=32, seed=7)
+        d_tok = torch.from_numpy(w.tokens.view(np.int32))
+        d_off = torch.from_numpy(w.offsets)
+        vals, sk = embed_sharded(ep, d_tok, d_off, w.d, (2, 7), rank, world, local_k1=_oracle_k1(w))
+        q.put((rank, vals.numpy().view(np.uint32).tolist(), sk.numpy().view(np.uint64).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_set_sharded_embedding_all_gathers_full_matrices(world):
+    w = _workload()
+    ref_vals = O.minhash(w.tokens, w.offsets, O.embedding_tables(32, 7), 1)
+    mh, bt = O.sketch_tables(2, 7)
+    ref_sk = O.sketch(w.tokens, w.offsets, mh, bt, 1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, vals, sk in outs:
+        assert np.array_equal(np.array(vals, dtype=np.uint32), ref_vals)
+        assert np.array_equal(np.array(sk, dtype=np.uint64), ref_sk)
+
+
+def test_shard_ranges_cover_every_set_once():
+    from paper_1707_06814_b200.distributed import shard_range
+    for n in (0, 1, 7, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            got = [shard_range(n, r, world)[:2] for r in range(world)]
+            covered = [i for lo, hi in got for i in range(lo, hi)]
+            assert covered == list(range(n))
+
+
 def test_merge_results_is_order_independent():
     from paper_1707_06814_b200.distributed import merge_results
     rng = np.random.default_rng(0)
