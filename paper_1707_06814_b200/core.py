@@ -75,6 +75,9 @@ class Dataset:
         if d is None:
             universe, flat = np.unique(flat, return_inverse=True)
             d = len(universe)
+        elif flat.min() < 0 or flat.max() >= d:
+            # the reference fails the same way when it builds the CSR (core.py:97-107)
+            raise ValueError("column index exceeds matrix dimensions")
         offsets = np.zeros(len(rows) + 1, dtype=np.int64)
         np.cumsum([len(r) for r in rows], out=offsets[1:])
         return cls(d=d, source_lines=lines, _csr=(flat.astype(np.uint32), offsets))

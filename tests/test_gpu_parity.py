@@ -160,6 +160,81 @@ def test_join_matches_oracle_on_workloads(cfg, scale, lam, ell, reps):
         [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members]
 
 
+def _csr_rows(rows):
+    tok = np.concatenate([np.asarray(r, dtype=np.uint32) for r in rows])
+    off = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    return tok, off
+
+
+@pytest.mark.parametrize("t,ell,lam,limit,eps", [(16, 1, 0.5, 30, 0.1), (64, 3, 0.6, 5, 0.2), (128, 2, 0.7, 1, 0.0),
+                                                 (33, 5, 0.55, 100, 0.5), (128, 16, 0.9, 60, 0.1)])
+def test_edge_parameters_match_oracle(t, ell, lam, limit, eps):
+    """Odd t (partial 128-function chunks), ell not a power of two (the
+    generic BruteForce path), limit = 1, epsilon 0 / 0.5."""
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    from paper_1707_06814_b200.workloads import generate
+    w = generate(1, scale=0.03)
+    emb = embed_dataset(EmbeddingParams(t=t, seed=3), Dataset.from_csr(w.tokens, w.offsets, w.d))
+    p = CPSJoinParams(lambda_=lam, ell=ell, seed=5, repetitions=3, limit=limit, epsilon=eps)
+    res = cpsjoin_self_arrays(emb, p)
+    assert np.array_equal(emb.values, O.minhash(w.tokens, w.offsets, O.embedding_tables(t, 3)))
+    ref = O.self_join(w.tokens, w.offsets, w.sizes, emb.values, emb.sketches(ell, 5), lam, epsilon=eps, limit=limit,
+                      repetitions=3, seed=5)
+    assert np.array_equal(emb.sketches(ell, 5), O.sketch(w.tokens, w.offsets, *O.sketch_tables(ell, 5)))
+    assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)
+    c = res.counters
+    assert [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members] == \
+        [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members]
+
+
+def test_long_sets_and_wide_tokens_match_oracle():
+    """Sets beyond the 16-bit position field (> 65536 tokens) and 4-byte
+    token ids (the 32-function K1 path), joined through the full pipeline."""
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    rng = np.random.default_rng(9)
+    base = np.unique(rng.integers(0, 2 ** 32 - 1, size=70000, dtype=np.uint64)).astype(np.int64)
+    rows = [base, np.sort(np.concatenate([base[:60000], np.unique(rng.integers(0, 2 ** 32 - 1, 12000))]))]
+    rows += [np.unique(rng.integers(0, 2 ** 32 - 1, size=int(rng.integers(2, 3000)))) for _ in range(60)]
+    rows = [np.unique(r) for r in rows]
+    tok, off = _csr_rows(rows)
+    ds = Dataset.from_csr(tok, off, 2 ** 32)
+    emb = embed_dataset(EmbeddingParams(t=64, seed=1), ds)
+    assert np.array_equal(emb.values, O.minhash(tok, off, O.embedding_tables(64, 1)))
+    p = CPSJoinParams(lambda_=0.5, seed=2, repetitions=2, limit=20)
+    res = cpsjoin_self_arrays(emb, p)
+    ref = O.self_join(tok, off, np.diff(off), emb.values, emb.sketches(8, 2), 0.5, limit=20, repetitions=2, seed=2)
+    assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)
+    assert res.counters.results == ref.results
+
+
+def test_long_set_three_byte_tokens_matches_oracle():
+    """A > 65536-token set with 3-byte tokens (16-bit K1's long-set path)."""
+    from oracle import oracle as O
+    from paper_1707_06814_b200.hashing import minhash_segments_many, sketch_family, build_sketch_matrix
+    rng = np.random.default_rng(4)
+    rows = [np.unique(rng.integers(0, 1 << 20, size=90000)), np.unique(rng.integers(0, 1 << 20, size=50))]
+    tok, off = _csr_rows(rows)
+    tables = O.derive_rng(3, 9).integers(0, 2 ** 64, size=(130, 4, 256), dtype=np.uint64)
+    assert np.array_equal(minhash_segments_many(tables, tok, off, d=1 << 20), O.minhash(tok, off, tables))
+    fam = sketch_family(1, 4)
+    assert np.array_equal(build_sketch_matrix(fam, tok, off), O.sketch(tok, off, *O.sketch_tables(1, 4)))
+
+
+def test_two_sets_and_identical_rows():
+    """n = 2 (root is a leaf), a pair of identical rows (J = 1) and the
+    empty result, through the C ABI."""
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    tok, off = _csr_rows([[1, 2, 3, 4], [1, 2, 3, 5]])
+    emb = embed_dataset(EmbeddingParams(seed=1), Dataset.from_csr(tok, off, 10))
+    res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=0.5, repetitions=3))
+    assert res.a.tolist() == [0] and res.b.tolist() == [1] and res.similarity.tolist() == [3 / 5]
+    assert res.counters.pre_candidates == 3 and res.counters.max_depth == 0
+    res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=0.9, repetitions=3))
+    assert len(res.a) == 0 and res.counters.pre_candidates == 3
+
+
 def test_small_limit_deep_tree_matches_oracle():
     # limit=8 forces many internal nodes and deep frontiers
     from oracle import oracle as O
