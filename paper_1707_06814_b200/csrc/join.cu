@@ -132,9 +132,25 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
         for (int k = 0; k < EL; ++k) cs.w[k] = jvalid ? __ldg(sketch + (size_t)col * ELL + k) : 0;
     }
     const int iend = min(m, (bi << 5) + 32);
+    // stage the tile's 32 row members (ids, sizes, sketches) in shared
+    // memory with one coalesced load per lane, so the row loop below reads
+    // broadcast shared words instead of a dependent global chain per row
+    constexpr int SK = ELL > 0 ? ELL : 1;
+    __shared__ uint64_t rsk_s[TPB / 32][32][SK];
+    __shared__ int32_t rid_s[TPB / 32][32], rsz_s[TPB / 32][32];
+    const int wib = threadIdx.x >> 5;
+    if (ELL > 0) {
+        const int ri = (bi << 5) + lane;
+        const int32_t r = ri < m ? mem[ri] : 0;
+        rid_s[wib][lane] = r;
+        rsz_s[wib][lane] = ri < m ? sizes[r] : 0;
+#pragma unroll
+        for (int k = 0; k < SK; ++k) rsk_s[wib][lane][k] = ri < m ? __ldg(sketch + (size_t)r * SK + k) : 0ull;
+        __syncwarp();
+    }
     for (int i = bi << 5; i < iend; ++i) {
-        const int32_t row = mem[i];
-        const uint64_t *rs = sketch + (size_t)row * ell;
+        const int32_t row = ELL > 0 ? rid_s[wib][i - (bi << 5)] : mem[i];
+        const uint64_t *rs = ELL > 0 ? rsk_s[wib][i - (bi << 5)] : sketch + (size_t)row * ell;
         const bool active = jvalid && j > i;
         int dist = 0;
         if (ELL >= 8) {
@@ -144,22 +160,24 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
             // (dist ~160 and ~192 of accept ~144 at l=8) end most rows early.
             constexpr int C1 = EL * 5 / 8, C2 = EL * 6 / 8;
 #pragma unroll
-            for (int k = 0; k < C1; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+            for (int k = 0; k < C1; ++k) dist += __popcll(rs[k] ^ cs.w[k]);
             if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
 #pragma unroll
-            for (int k = C1; k < C2; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+            for (int k = C1; k < C2; ++k) dist += __popcll(rs[k] ^ cs.w[k]);
             if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
 #pragma unroll
-            for (int k = C2; k < EL; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+            for (int k = C2; k < EL; ++k) dist += __popcll(rs[k] ^ cs.w[k]);
         } else if (ELL > 0) {
 #pragma unroll
-            for (int k = 0; k < EL; ++k) dist += __popcll(__ldg(rs + k) ^ cs.w[k]);
+            for (int k = 0; k < EL; ++k) dist += __popcll(rs[k] ^ cs.w[k]);
         } else {
             const uint64_t *csp = sketch + (size_t)col * ell;
             for (int k = 0; k < ell; ++k) dist += __popcll(__ldg(rs + k) ^ (jvalid ? __ldg(csp + k) : 0));
         }
         bool pass = active && dist <= accept;
-        if (pass) pass = size_filter(sizes[row], col_size, lam) && (side == nullptr || side[row] != side[col]);
+        if (pass)
+            pass = size_filter(ELL > 0 ? rsz_s[wib][i - (bi << 5)] : sizes[row], col_size, lam) &&
+                   (side == nullptr || side[row] != side[col]);
         const unsigned mask = __ballot_sync(0xffffffffu, pass);
         if (mask) {
             unsigned long long base = 0;
