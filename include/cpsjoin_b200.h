@@ -146,6 +146,30 @@ CPSJ_API int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys,
                             const double **d_sims, int64_t *n_pairs);
 
 /*
+ * Exact joins (SPEC.md module `allpairs`; specified by the
+ * reference but not shipped -- here the at-scale recall oracle).
+ *
+ * cpsj_frequency_order -- frequency_order: d_rank_out[v] =
+ *   position of token v when the universe [0, d) is sorted by (frequency
+ *   over d_tokens, token id) ascending; d_order_out (nullable) = the sorted
+ *   tokens.  Both u32, d entries.
+ * cpsj_exact_join -- naive == 0: allpairs_join, prefix
+ *   filtering under the frequency order with prefix |x| - ceil(lambda |x|)
+ *   + 1 and the reference's size filter; naive != 0:
+ *   naive_join, all C(n, 2) pairs.  Rows: d_tokens sorted
+ *   ascending per set, every token < d.  Results (unique, sorted keys
+ *   (min_row << 32) | max_row, f64 similarity >= lambda_) go to the ctx
+ *   arena like cpsj_self_join's; stats fills n_pairs, pre_candidates
+ *   (enumerated posting pairs), candidates (distinct pairs verified),
+ *   results, gpu_launches, lib_calls.
+ */
+CPSJ_API int cpsj_frequency_order(cpsj_ctx *ctx, const uint32_t *d_tokens, int64_t nnz, int64_t d,
+                         uint32_t *d_rank_out, uint32_t *d_order_out, void *stream);
+CPSJ_API int cpsj_exact_join(cpsj_ctx *ctx, const uint32_t *d_tokens, const int64_t *d_offsets,
+                    int64_t n_sets, int64_t d, double lambda_, int32_t naive,
+                    cpsj_join_stats *stats, void *stream);
+
+/*
  * Device-time profile by kernel class (CUDA events on the call's stream).
  * Classes: 0 K1 minhash/sketch, 1 K4 leaf BruteForce, 2 point compares,
  * 3 node sketch + flags, 4 split, 5 K5 verify, 6 K6 dedup, 7 level plan.

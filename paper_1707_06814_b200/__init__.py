@@ -10,6 +10,7 @@ kernels behind a C ABI (include/cpsjoin_b200.h).  There is no CPU
 fallback: without the built library and a CUDA device the entry points
 raise.
 """
+from .allpairs import allpairs_join, frequency_order, naive_join, prefix_length  # noqa: F401
 from .core import Counters, Dataset, Record, ResultPair, check_threshold, jaccard  # noqa: F401
 from .cpsjoin import CPSJoinParams, cpsjoin_self, cpsjoin_self_arrays, join_rs, join_rs_arrays  # noqa: F401
 from .embed import EmbeddedDataset, EmbeddingParams, embed_dataset, union_embedded  # noqa: F401

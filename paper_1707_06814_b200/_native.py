@@ -37,7 +37,7 @@ class JoinStats(ctypes.Structure):
 EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_error",
            "cpsj_family_create", "cpsj_family_destroy", "cpsj_minhash_sketch", "cpsj_self_join",
            "cpsj_join_copy_result", "cpsj_join_result_device", "cpsj_profile_enable", "cpsj_profile_read",
-           "cpsj_launch_counts"]
+           "cpsj_launch_counts", "cpsj_frequency_order", "cpsj_exact_join"]
 
 PROF_CLASSES = ["k1_minhash", "k4_leaf", "point", "node", "split", "k5_verify", "k6_dedup", "plan"]
 
@@ -74,6 +74,8 @@ def load(path: str | None = None):
         L.cpsj_profile_enable.argtypes = [P, ctypes.c_int]
         L.cpsj_profile_read.argtypes = [P, P, P, i32]
         L.cpsj_launch_counts.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.cpsj_frequency_order.argtypes = [P, P, i64, i64, P, P, P]
+        L.cpsj_exact_join.argtypes = [P, P, P, i64, i64, dbl, i32, ctypes.POINTER(JoinStats), P]
         _lib = L
         return L
 

@@ -162,6 +162,26 @@ int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys, const double
     return CPSJ_OK;
 }
 
+int cpsj_frequency_order(cpsj_ctx *ctx, const uint32_t *d_tokens, int64_t nnz, int64_t d, uint32_t *d_rank_out,
+                         uint32_t *d_order_out, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(nnz >= 0 && (nnz == 0 || d_tokens), "null token pointer");
+        cpsj::require(d_rank_out != nullptr, "null rank output");
+        cpsj::frequency_order(ctx, d_tokens, nnz, d, d_rank_out, d_order_out, (cudaStream_t)stream);
+    });
+}
+
+int cpsj_exact_join(cpsj_ctx *ctx, const uint32_t *d_tokens, const int64_t *d_offsets, int64_t n_sets, int64_t d,
+                    double lambda_, int32_t naive, cpsj_join_stats *stats, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(n_sets < 2 || (d_tokens && d_offsets), "null CSR pointers");
+        cpsj::require(d >= 1 && d < ((int64_t)1 << 31), "token universe must be in [1, 2^31)");
+        cpsj::exact_join(ctx, d_tokens, d_offsets, n_sets, d, lambda_, naive, stats, (cudaStream_t)stream);
+    });
+}
+
 int cpsj_launch_counts(const cpsj_ctx *ctx, int64_t *own_kernels, int64_t *lib_calls) {
     if (!ctx) return CPSJ_E_ARG;
     if (own_kernels) *own_kernels = ctx->launches;

@@ -133,3 +133,25 @@ def test_workload_generator_deterministic_and_planted_exact():
         row = a.tokens[a.offsets[i]:a.offsets[i + 1]]
         assert np.all(np.diff(row.astype(np.int64)) > 0)
         assert row.max() < a.d
+
+
+def test_allpairs_prefix_length_spec_examples():
+    """SPEC:459-466 examples; the prefix never loses a pair: for every pair of
+    sizes with J >= lambda achievable, the two prefixes must overlap."""
+    from paper_1707_06814_b200 import prefix_length
+    assert prefix_length(10, 0.5) == 6
+    assert prefix_length(2, 0.5) == 2
+    assert prefix_length(7, 0.999999) == 1
+    for lam in (0.3, 0.5, 0.6, 0.7, 0.9):
+        prev = 0
+        for s in range(1, 300):
+            p = prefix_length(s, lam)
+            assert 1 <= p <= s and p >= prev      # non-decreasing in |x|
+            prev = p
+            # overlap needed >= lam |x|: the prefix covers |x| - that + 1
+            assert p >= s - int(np.ceil(lam * s)) + 1 - 1e-12
+    for s in (5, 50, 500):
+        assert [prefix_length(s, lam) for lam in (0.2, 0.4, 0.6, 0.8)] == \
+            sorted([prefix_length(s, lam) for lam in (0.2, 0.4, 0.6, 0.8)], reverse=True)
+    with pytest.raises(ValueError):
+        prefix_length(0, 0.5)
