@@ -146,6 +146,35 @@ CPSJ_API int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys,
                             const double **d_sims, int64_t *n_pairs);
 
 /*
+ * MinHash LSH join (SPEC.md module `minhash_join`; Alg. 3 of
+ * the paper; the reference reserves KIND_MINHASH_REP, hashing.py:35, but
+ * ships no code).  Repetition r buckets record x by
+ *   key = mix64(...mix64(mix64(seed_r ^ v_0) ^ v_1)... ^ v_{k-1}),
+ *   v_j = values[x][h_positions[r][j]]
+ * (the bucket is key >> ceil(log2 n_reps), the repetition index taking
+ * those top bits of the device sort key) and runs the CPSJoin BruteForce (sketch filter dist <= accept_dist, size
+ * filter, exact verification) inside every bucket of >= 2 records.
+ * Results land in the ctx arena like cpsj_self_join's; pre_candidates =
+ * sum over repetitions and buckets of C(|b|, 2), candidates = pairs that
+ * passed the sketch and size filters, results = verified (with repeats).
+ * cost_only != 0 stops after bucketing: only pre_candidates is filled
+ * (choose_k's cost model).  in->d_tokens/offsets/sizes/values
+ * and d_sketch are required; d_side may be NULL.
+ */
+typedef struct {
+    double lambda_;
+    int32_t accept_dist;          /* as cpsj_plan.accept_dist               */
+    int32_t k;                    /* concatenation length                   */
+    int32_t n_reps;               /* L                                      */
+    const int16_t *h_positions;   /* (n_reps, k) positions in [0, t)        */
+    const uint64_t *h_rep_seeds;  /* (n_reps) bucket-key seeds              */
+    int32_t cost_only;
+} cpsj_lsh_plan;
+
+CPSJ_API int cpsj_lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_plan *plan,
+                  cpsj_join_stats *stats, void *stream);
+
+/*
  * Exact joins (SPEC.md module `allpairs`; specified by the
  * reference but not shipped -- here the at-scale recall oracle).
  *

@@ -209,3 +209,84 @@ def full_pipeline(tokens, offsets, sizes, *, lam, t=128, emb_seed=0, ell=8, seed
                     delta=delta, repetitions=repetitions, seed=seed, depth_cap=depth_cap,
                     threads=threads)
     return values, sk, out
+
+
+# ---------------------------------------------------------------- LSH join
+# SPEC.md minhash_join: the reference specifies it but ships
+# no code; this numpy restatement follows the definitions stated in
+# paper_1707_06814_b200/lsh.py and the shared
+# BruteForce semantics (cpsjoin.py:139-157).  Small n only.
+
+KIND_MINHASH_REP = 4
+_U = np.uint64
+
+
+def _mix64_vec(z):
+    z = np.asarray(z, dtype=_U)
+    with np.errstate(over="ignore"):
+        z = z + _U(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> _U(30))) * _U(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> _U(27))) * _U(0x94D049BB133111EB)
+        return z ^ (z >> _U(31))
+
+
+def lsh_rep_plan(seed: int, reps: int, k: int, t: int, path=()):
+    seeds = derive_rng(seed, KIND_MINHASH_REP, *path).integers(0, 2 ** 64, size=reps, dtype=np.uint64)
+    pos = np.zeros((reps, k), dtype=np.int64)
+    for r in range(reps):
+        w = _mix64_vec(_U(int(seeds[r])) ^ _mix64_vec(np.arange(k, dtype=_U)))
+        u = w / 2.0 ** 64
+        pos[r] = np.minimum((u * t).astype(np.int64), t - 1)
+    return pos, seeds
+
+
+def lsh_join(tokens, offsets, sizes, values, sketches, lam: float, accept: int, pos, seeds, cost_only=False):
+    """Returns (keys, sims, pre, cand, res) -- keys sorted unique."""
+    tokens = np.asarray(tokens)
+    offsets = np.asarray(offsets)
+    sizes = np.asarray(sizes, dtype=np.int64)
+    values = np.asarray(values, dtype=np.uint32)
+    n = len(sizes)
+    L = len(seeds)
+    rbits = 0
+    while ((L - 1) >> rbits) > 0:
+        rbits += 1
+    pre = cand = res = 0
+    found = {}
+    rows = [set(tokens[offsets[i]:offsets[i + 1]].tolist()) for i in range(n)]
+    for r in range(L):
+        h = np.full(n, int(seeds[r]), dtype=_U)
+        for j in range(pos.shape[1]):
+            h = _mix64_vec(h ^ values[:, pos[r, j]].astype(_U))
+        key = h >> _U(rbits) if rbits else h
+        order = np.argsort(key, kind="stable")
+        ks = key[order]
+        starts = np.flatnonzero(np.r_[True, ks[1:] != ks[:-1]])
+        ends = np.r_[starts[1:], n]
+        for s, e in zip(starts, ends):
+            m = e - s
+            if m < 2:
+                continue
+            pre += m * (m - 1) // 2
+            if cost_only:
+                continue
+            mem = order[s:e]
+            for a in range(m):
+                x = int(mem[a])
+                for b in range(a + 1, m):
+                    y = int(mem[b])
+                    dist = int(np.bitwise_count(sketches[x] ^ sketches[y]).sum())
+                    if dist > accept:
+                        continue
+                    mn, mx = min(sizes[x], sizes[y]), max(sizes[x], sizes[y])
+                    if not (float(mn) >= lam * float(mx) - 1e-9):
+                        continue
+                    cand += 1
+                    inter = len(rows[x] & rows[y])
+                    sim = inter / float(sizes[x] + sizes[y] - inter)
+                    if sim >= lam:
+                        res += 1
+                        found[(min(x, y) << 32) | max(x, y)] = sim
+    keys = np.array(sorted(found), dtype=np.uint64)
+    sims = np.array([found[int(k)] for k in keys], dtype=np.float64)
+    return keys, sims, pre, cand, res

@@ -15,5 +15,6 @@ from .core import Counters, Dataset, Record, ResultPair, check_threshold, jaccar
 from .cpsjoin import CPSJoinParams, cpsjoin_self, cpsjoin_self_arrays, join_rs, join_rs_arrays  # noqa: F401
 from .embed import EmbeddedDataset, EmbeddingParams, embed_dataset, union_embedded  # noqa: F401
 from .hashing import SketchFamily, match_threshold  # noqa: F401
+from .lsh import MinHashJoinParams, choose_k, minhash_join, repetitions_for_recall  # noqa: F401
 
 __version__ = "0.1.0"

@@ -28,6 +28,11 @@ class Plan(ctypes.Structure):
                 ("use_count_table", i32), ("count_threshold", dbl)]
 
 
+class LshPlan(ctypes.Structure):
+    _fields_ = [("lambda_", dbl), ("accept_dist", i32), ("k", i32), ("n_reps", i32), ("h_positions", P),
+                ("h_rep_seeds", P), ("cost_only", i32)]
+
+
 class JoinStats(ctypes.Structure):
     _fields_ = [("n_pairs", i64), ("pre_candidates", i64), ("candidates", i64), ("results", i64),
                 ("max_depth", i64), ("peak_live_members", i64), ("n_depth_cap_events", i64),
@@ -37,7 +42,8 @@ class JoinStats(ctypes.Structure):
 EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_error",
            "cpsj_family_create", "cpsj_family_destroy", "cpsj_minhash_sketch", "cpsj_self_join",
            "cpsj_join_copy_result", "cpsj_join_result_device", "cpsj_profile_enable", "cpsj_profile_read",
-           "cpsj_launch_counts", "cpsj_frequency_order", "cpsj_exact_join"]
+           "cpsj_launch_counts", "cpsj_frequency_order", "cpsj_exact_join",
+           "cpsj_lsh_join"]
 
 PROF_CLASSES = ["k1_minhash", "k4_leaf", "point", "node", "split", "k5_verify", "k6_dedup", "plan"]
 
@@ -75,6 +81,7 @@ def load(path: str | None = None):
         L.cpsj_profile_read.argtypes = [P, P, P, i32]
         L.cpsj_launch_counts.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.cpsj_frequency_order.argtypes = [P, P, i64, i64, P, P, P]
+        L.cpsj_lsh_join.argtypes = [P, ctypes.POINTER(Inputs), ctypes.POINTER(LshPlan), ctypes.POINTER(JoinStats), P]
         L.cpsj_exact_join.argtypes = [P, P, P, i64, i64, dbl, i32, ctypes.POINTER(JoinStats), P]
         _lib = L
         return L

@@ -162,6 +162,19 @@ int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys, const double
     return CPSJ_OK;
 }
 
+int cpsj_lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_plan *plan, cpsj_join_stats *stats,
+                  void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(in && plan && stats, "null argument");
+        cpsj::require(in->n < (int64_t)1 << 31, "at most 2^31 - 1 sets");
+        cpsj::require(in->n < 2 || (in->d_tokens && in->d_offsets && in->d_sizes && in->d_values &&
+                                    (in->d_sketch || plan->cost_only)),
+                      "null input pointers");
+        cpsj::lsh_join(ctx, in, plan, stats, (cudaStream_t)stream);
+    });
+}
+
 int cpsj_frequency_order(cpsj_ctx *ctx, const uint32_t *d_tokens, int64_t nnz, int64_t d, uint32_t *d_rank_out,
                          uint32_t *d_order_out, void *stream) {
     if (!ctx) return CPSJ_E_ARG;

@@ -193,6 +193,8 @@ int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_toke
                    uint64_t *d_sketch, cudaStream_t stream);
 void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
                cudaStream_t stream);
+void lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_plan *plan, cpsj_join_stats *stats,
+              cudaStream_t st);
 void frequency_order(cpsj_ctx *ctx, const uint32_t *d_tokens, int64_t nnz, int64_t d, uint32_t *d_rank,
                      uint32_t *d_order, cudaStream_t st);
 void exact_join(cpsj_ctx *ctx, const uint32_t *tok, const int64_t *off, int64_t n, int64_t d, double lam, int naive,

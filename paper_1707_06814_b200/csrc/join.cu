@@ -118,6 +118,16 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
     const int m = nd_cnt[node];
     const int T = (m + 31) >> 5;
     int bi = 0;
+    if (T > 16) {
+        // large (LSH) buckets: row bi of the tile triangle starts at
+        // bi T - bi (bi - 1) / 2; invert with a square root, then fix up
+        const double tt = (double)T + 0.5;
+        bi = (int)(tt - sqrt(tt * tt - 2.0 * (double)local));
+        bi = bi < 0 ? 0 : (bi >= T ? T - 1 : bi);
+        while (bi > 0 && (int64_t)bi * T - (int64_t)bi * (bi - 1) / 2 > local) --bi;
+        while ((int64_t)(bi + 1) * T - (int64_t)(bi + 1) * bi / 2 <= local) ++bi;
+        local -= (int64_t)bi * T - (int64_t)bi * (bi - 1) / 2;
+    }
     while (local >= T - bi) { local -= T - bi; ++bi; }
     const int bj = bi + (int)local;
     const int32_t *mem = members + nd_off[node];
@@ -581,15 +591,6 @@ __global__ void k_gather8(Gather8 g, int cnt, int64_t *__restrict__ out) {
     if (i < cnt) out[i] = *g.p[i];
 }
 
-__global__ void k_gather_scalars(const int64_t *__restrict__ a, int64_t ia, const int64_t *__restrict__ b,
-                                 int64_t ib, const int64_t *__restrict__ c, int64_t ic, int64_t *__restrict__ out) {
-    if (threadIdx.x == 0) {
-        out[0] = a ? a[ia] : 0;
-        out[1] = b ? b[ib] : 0;
-        out[2] = c ? c[ic] : 0;
-    }
-}
-
 // ------------------------------------------------------------ host side
 
 struct Level {
@@ -622,19 +623,6 @@ struct Driver {
         CPSJ_CUDA(cudaMemcpyAsync(ctx->h_scalars, dscal, cnt * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         CPSJ_CUDA(cudaStreamSynchronize(st));
         for (int i = 0; i < cnt; ++i) out[i] = ctx->h_scalars[i];
-    }
-
-    // read up to three device scalars with one synchronisation
-    void read3(const int64_t *a, int64_t ia, const int64_t *b, int64_t ib, const int64_t *c, int64_t ic,
-               int64_t *dscal, int64_t out[3]) {
-        k_gather_scalars<<<1, 32, 0, st>>>(a, ia, b, ib, c, ic, dscal);
-        CPSJ_LAUNCH_CHECK();
-        ctx->launches++;
-        CPSJ_CUDA(cudaMemcpyAsync(ctx->h_scalars, dscal, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        CPSJ_CUDA(cudaStreamSynchronize(st));
-        out[0] = ctx->h_scalars[0];
-        out[1] = ctx->h_scalars[1];
-        out[2] = ctx->h_scalars[2];
     }
 };
 
@@ -758,6 +746,97 @@ void leaf_dispatch(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Lev
     }
 }
 
+// Candidate and result buffers of one join call (grow on demand), K5 on
+// each batch of candidates and K6 at the end.
+struct Emitter {
+    cpsj_ctx *ctx;
+    cudaStream_t st;
+    const cpsj_inputs *in;
+    double lam;
+    DevCounters *ctr;
+    unsigned long long cand_cap = 1 << 20;
+    DevBuf<int2> cand;
+    unsigned long long res_cap = 1 << 16;
+    DevBuf<uint64_t> rkeys;
+    DevBuf<double> rsims;
+    unsigned long long res_bound = 0;  // host upper bound of result slots used
+    int64_t total_cand = 0;
+
+    Emitter(cpsj_ctx *c, cudaStream_t s, const cpsj_inputs *i, double l, DevCounters *k)
+        : ctx(c), st(s), in(i), lam(l), ctr(k) {
+        cand.alloc(cand_cap, st);
+        rkeys.alloc(res_cap, st);
+        rsims.alloc(res_cap, st);
+    }
+
+    // K5 on the `nc` candidates emitted since the last reset; `regen`
+    // re-emits them into a larger buffer when the first pass overflowed
+    template <typename Regen>
+    void verify(int64_t nc_in, Regen &&regen) {
+        unsigned long long nc = (unsigned long long)nc_in;
+        if (nc > cand_cap) {
+            cand_cap = nc + nc / 4 + 1024;
+            cand.alloc(cand_cap, st);
+            CPSJ_CUDA(cudaMemsetAsync(&ctr->cand_n, 0, sizeof(unsigned long long), st));
+            regen();
+        }
+        if (nc > 0) {
+            if (res_bound + nc > res_cap) {
+                const unsigned long long want = std::max(res_bound + nc, 2 * res_cap);
+                rkeys.grow(want, res_cap, st);
+                rsims.grow(want, res_cap, st);
+                res_cap = want;
+            }
+            ProfScope prof(ctx, PROF_VERIFY, st);
+            k_verify<<<blocks_for((int64_t)nc * 32), TPB, 0, st>>>((int64_t)nc, cand.p, in->d_tokens, in->d_offsets,
+                                                                   in->d_sizes, lam, rkeys.p, rsims.p, ctr);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            total_cand += (int64_t)nc;
+            res_bound += nc;
+        }
+        CPSJ_CUDA(cudaMemsetAsync(&ctr->cand_n, 0, sizeof(unsigned long long), st));
+    }
+
+    // K6: sort + unique of the verified pairs into the context arena;
+    // returns the device counters
+    DevCounters finish(Driver &drv) {
+        DevCounters hc{};
+        CPSJ_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        const int64_t nres = (int64_t)hc.res_n;
+        ProfScope prof_dedup(ctx, PROF_DEDUP, st);
+        ctx->res_keys.release();
+        ctx->res_sims.release();
+        ctx->n_pairs = 0;
+        if (nres > 0) {
+            DevBuf<uint64_t> k2(nres, st);
+            DevBuf<double> s2(nres, st);
+            size_t bytes = 0;
+            CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64, st));
+            if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+            CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64,
+                                                      st));
+            ctx->lib_calls++;
+            ctx->res_keys.alloc(nres, st);
+            ctx->res_sims.alloc(nres, st);
+            DevBuf<int64_t> nsel(1, st);
+            bytes = 0;
+            CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(nullptr, bytes, k2.p, s2.p, ctx->res_keys.p, ctx->res_sims.p,
+                                                     nsel.p, nres, st));
+            if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+            CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(drv.cub_tmp.p, bytes, k2.p, s2.p, ctx->res_keys.p,
+                                                     ctx->res_sims.p, nsel.p, nres, st));
+            ctx->lib_calls++;
+            int64_t u = 0;
+            CPSJ_CUDA(cudaMemcpyAsync(&u, nsel.p, 8, cudaMemcpyDeviceToHost, st));
+            CPSJ_CUDA(cudaStreamSynchronize(st));
+            ctx->n_pairs = u;
+        }
+        return hc;
+    }
+};
+
 }  // namespace
 
 void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
@@ -784,13 +863,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         CPSJ_CUDA(cudaMemcpyAsync(ctr.p, &init, sizeof(init), cudaMemcpyHostToDevice, st));
     }
     // candidate and result buffers grow on demand
-    unsigned long long cand_cap = 1 << 20;
-    DevBuf<int2> cand(cand_cap, st);
-    unsigned long long res_cap = 1 << 16;
-    DevBuf<uint64_t> rkeys(res_cap, st);
-    DevBuf<double> rsims(res_cap, st);
-    DevBuf<int64_t> cap_sizes;  // depth-cap survivor counts, per level
-    int64_t total_cand = 0, max_depth = 0, levels = 0;
+    Emitter em(ctx, st, in, lam, ctr.p);
+    int64_t max_depth = 0, levels = 0;
 
     Level lv;
     const int32_t R = plan->n_reps;
@@ -816,36 +890,6 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     }
     const uint64_t child_off = (uint64_t)t + 64ull * (uint64_t)ell;
     const int vbits = plan->value_bits > 0 && plan->value_bits < 32 ? plan->value_bits : 32;
-    unsigned long long res_bound = 0;  // host upper bound of result slots used
-
-    // K5 on `nc` candidates emitted since the last reset; `regen` re-emits
-    // them into a larger buffer when the first pass overflowed
-    auto verify_batch = [&](int64_t nc_in, auto &&regen) {
-        unsigned long long nc = (unsigned long long)nc_in;
-        if (nc > cand_cap) {
-            cand_cap = nc + nc / 4 + 1024;
-            cand.alloc(cand_cap, st);
-            CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cand_n, 0, sizeof(unsigned long long), st));
-            regen();
-        }
-        if (nc > 0) {
-            if (res_bound + nc > res_cap) {
-                const unsigned long long want = std::max(res_bound + nc, 2 * res_cap);
-                rkeys.grow(want, res_cap, st);
-                rsims.grow(want, res_cap, st);
-                res_cap = want;
-            }
-            ProfScope prof(ctx, PROF_VERIFY, st);
-            k_verify<<<blocks_for((int64_t)nc * 32), TPB, 0, st>>>((int64_t)nc, cand.p, in->d_tokens,
-                                                                   in->d_offsets, in->d_sizes, lam, rkeys.p,
-                                                                   rsims.p, ctr.p);
-            CPSJ_LAUNCH_CHECK();
-            ctx->launches++;
-            total_cand += (int64_t)nc;
-            res_bound += nc;
-        }
-        CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cand_n, 0, sizeof(unsigned long long), st));
-    };
 
     // Three host synchronisations per level: (A) leaf/internal totals,
     // (B) candidate count + flag/entry totals, (C) child totals.  Every
@@ -879,7 +923,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         // ---- leaves: K4 (candidates verified after sync B)
         auto gen_leaf = [&]() {
             if (work.tiles > 0 || work.pairs > 0)
-                leaf_dispatch(ctx, st, work, lv, in, plan->accept_dist, lam, cand.p, cand_cap, ctr.p);
+                leaf_dispatch(ctx, st, work, lv, in, plan->accept_dist, lam, em.cand.p, em.cand_cap, ctr.p);
         };
         gen_leaf();
 
@@ -959,7 +1003,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             CPSJ_CUDA(cudaStreamSynchronize(st));
             ctx->cap_events.insert(ctx->cap_events.end(), h.begin(), h.end());
         }
-        verify_batch(n_leaf_cand, gen_leaf);
+        em.verify(n_leaf_cand, gen_leaf);
 
         // ---- point comparisons of flagged members (K2)
         DevBuf<int64_t> flist;
@@ -968,7 +1012,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             ProfScope prof(ctx, PROF_POINT, st);
             k_point<<<blocks_for(n_flag * 32), TPB, 0, st>>>(
                 n_flag, flist.p, fscan.p, flags.p, im_off_c.p, n_int, ilist.p, lv.off.p, lv.cnt.p, lv.members.p,
-                in->d_sketch, ell, in->d_sizes, in->d_side, plan->accept_dist, lam, cand.p, cand_cap, count_pre,
+                in->d_sketch, ell, in->d_sizes, in->d_side, plan->accept_dist, lam, em.cand.p, em.cand_cap, count_pre,
                 ctr.p);
             CPSJ_LAUNCH_CHECK();
             ctx->launches++;
@@ -1030,7 +1074,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             else
                 drv.gather({{cand_n}}, 1, dscal.p, sc);
         }
-        if (n_flag > 0) verify_batch(sc[0], gen_point);
+        if (n_flag > 0) em.verify(sc[0], gen_point);
         nx.N = E > 0 ? sc[1] : 0;
         nx.M = E > 0 ? sc[2] : 0;
         if (nx.N > 0) {
@@ -1054,45 +1098,177 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     }
 
     // ---- K6: sort + unique of the verified pairs
-    DevCounters hc{};
-    CPSJ_CUDA(cudaMemcpyAsync(&hc, ctr.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    CPSJ_CUDA(cudaStreamSynchronize(st));
+    const DevCounters hc = em.finish(drv);
     const int64_t nres = (int64_t)hc.res_n;
-    ProfScope prof_dedup(ctx, PROF_DEDUP, st);
-    ctx->res_keys.release();
-    ctx->res_sims.release();
-    if (nres > 0) {
-        DevBuf<uint64_t> k2(nres, st);
-        DevBuf<double> s2(nres, st);
-        size_t bytes = 0;
-        CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64, st));
-        if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
-        CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64, st));
-        ctx->lib_calls++;
-        ctx->res_keys.alloc(nres, st);
-        ctx->res_sims.alloc(nres, st);
-        DevBuf<int64_t> nsel(1, st);
-        bytes = 0;
-        CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(nullptr, bytes, k2.p, s2.p, ctx->res_keys.p, ctx->res_sims.p, nsel.p,
-                                                 nres, st));
-        if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
-        CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(drv.cub_tmp.p, bytes, k2.p, s2.p, ctx->res_keys.p, ctx->res_sims.p,
-                                                 nsel.p, nres, st));
-        ctx->lib_calls++;
-        int64_t u = 0;
-        CPSJ_CUDA(cudaMemcpyAsync(&u, nsel.p, 8, cudaMemcpyDeviceToHost, st));
-        CPSJ_CUDA(cudaStreamSynchronize(st));
-        ctx->n_pairs = u;
-    }
     if (hc.err) throw Error{CPSJ_E_PICK, "node-sketch pick index out of range (uniform draw == 1.0)"};
     stats->n_pairs = ctx->n_pairs;
     stats->pre_candidates = (int64_t)hc.pre;
-    stats->candidates = total_cand;
+    stats->candidates = em.total_cand;
     stats->results = nres;
     stats->max_depth = max_depth;
     stats->peak_live_members = (n >= 2 && R > 0) ? hc.peak : 0;
     stats->n_depth_cap_events = (int64_t)ctx->cap_events.size();
     stats->n_levels = levels;
+    stats->gpu_launches = ctx->launches - launches0;
+    stats->lib_calls = ctx->lib_calls - lib0;
+}
+
+// ------------------------------------------------- MinHash LSH join (Alg. 3)
+//
+// SPEC.md module `minhash_join` (the reference reserves
+// KIND_MINHASH_REP = 4 for it, hashing.py:35, but ships no code).  Each
+// repetition buckets every record by its k embedded MinHash values at the
+// repetition's positions (sampled with replacement on the host, so a pair
+// with embedded Braun-Blanquet similarity s collides with probability s^k
+// exactly), the k-tuple chained through mix64 from the repetition seed into
+// one 64-bit key; every bucket of >= 2 records is a leaf of the CPSJoin
+// BruteForce (sketch filter, size filter, K5 verify) regardless of its size.
+// All repetitions of a batch are one radix sort over (repetition, key).
+
+namespace {
+
+__global__ void k_lsh_keys(int64_t n, int32_t nr, int t, int k, const uint32_t *__restrict__ values,
+                           const int16_t *__restrict__ pos, const uint64_t *__restrict__ seeds, int rbits,
+                           uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * nr) return;
+    const int64_t r = e / n, i = e - r * n;
+    uint64_t h = seeds[r];
+    const uint32_t *row = values + (size_t)i * t;
+    for (int j = 0; j < k; ++j) h = mix64(h ^ (uint64_t)row[pos[r * k + j]]);
+    // the bucket is the top 64 - rbits bits of h (rbits from the total
+    // repetition count, so batching never changes a bucket)
+    keys[e] = rbits ? (((uint64_t)r << (64 - rbits)) | (h >> rbits)) : h;
+    vals[e] = (int32_t)i;
+}
+
+// kept groups (>= 2 records) become leaf nodes
+__global__ void k_lsh_nodes(const int64_t *__restrict__ Gp, int64_t E, const int64_t *__restrict__ gstart,
+                            const int64_t *__restrict__ keep, const int64_t *__restrict__ kscan,
+                            const int64_t *__restrict__ mscan, int64_t *__restrict__ off, int32_t *__restrict__ cnt) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t G = *Gp;
+    if (g < G && keep[g]) {
+        const int64_t sz = (g + 1 < G ? gstart[g + 1] : E) - gstart[g];
+        off[kscan[g]] = mscan[g];
+        cnt[kscan[g]] = (int32_t)sz;
+    }
+}
+
+}  // namespace
+
+void lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_plan *plan, cpsj_join_stats *stats,
+              cudaStream_t st) {
+    require(in && plan && stats, "null argument");
+    require(in->n >= 0 && in->t >= 1 && in->t <= 32767 && in->ell >= 1, "bad input shape");
+    require(plan->k >= 1 && plan->n_reps >= 0, "bad plan");
+    require(plan->n_reps == 0 || (plan->h_positions && plan->h_rep_seeds), "null positions or seeds");
+    std::memset(stats, 0, sizeof(*stats));
+    const int64_t launches0 = ctx->launches, lib0 = ctx->lib_calls;
+    const int64_t n = in->n;
+    const int t = in->t, k = plan->k;
+    const int32_t L = plan->n_reps;
+    for (int64_t q = 0; q < (int64_t)L * k; ++q)
+        require(plan->h_positions[q] >= 0 && plan->h_positions[q] < t, "position out of range");
+    ctx->n_pairs = 0;
+    ctx->cap_events.clear();
+    Driver drv{ctx, st};
+    DevBuf<DevCounters> ctr(1, st);
+    DevBuf<int64_t> dscal(8, st);
+    CPSJ_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(DevCounters), st));
+    Emitter em(ctx, st, in, plan->lambda_, ctr.p);
+    if (n >= 2 && L > 0) {
+        DevBuf<int16_t> dpos((size_t)L * k, st);
+        DevBuf<uint64_t> dseed(L, st);
+        CPSJ_CUDA(cudaMemcpyAsync(dpos.p, plan->h_positions, (size_t)L * k * 2, cudaMemcpyHostToDevice, st));
+        CPSJ_CUDA(cudaMemcpyAsync(dseed.p, plan->h_rep_seeds, (size_t)L * 8, cudaMemcpyHostToDevice, st));
+        // batches of repetitions keep the sort at <= 2^26 entries
+        const int32_t per = (int32_t)std::max<int64_t>(1, std::min<int64_t>(L, ((int64_t)1 << 26) / n));
+        int rbits = 0;
+        while (((int64_t)(L - 1) >> rbits) > 0) ++rbits;
+        for (int32_t r0 = 0; r0 < L; r0 += per) {
+            const int32_t nr = std::min(per, L - r0);
+            const int64_t E = n * nr;
+            DevBuf<uint64_t> keys(E, st), keys2(E, st);
+            DevBuf<int32_t> vals(E, st), vals2(E, st);
+            {
+                ProfScope prof(ctx, PROF_SPLIT, st);
+                k_lsh_keys<<<blocks_for(E), TPB, 0, st>>>(n, nr, t, k, in->d_values, dpos.p + (size_t)r0 * k,
+                                                          dseed.p + r0, rbits, keys.p, vals.p);
+                CPSJ_LAUNCH_CHECK();
+                size_t bytes = 0;
+                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0, 64,
+                                                          st));
+                if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
+                                                          0, 64, st));
+                ctx->lib_calls++;
+            }
+            keys.release();
+            vals.release();
+            DevBuf<int64_t> head(E + 1, st), hscan(E + 1, st), gstart(E, st), keep(E + 1, st), ksize(E + 1, st),
+                kscan(E + 1, st), mscan(E + 1, st);
+            k_heads<<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
+            CPSJ_LAUNCH_CHECK();
+            drv.scan(head.p, hscan.p, E + 1);
+            k_group_start<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p);
+            CPSJ_LAUNCH_CHECK();
+            k_group_keep<<<blocks_for(E + 1), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, ksize.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 4;
+            drv.scan(keep.p, kscan.p, E + 1);
+            drv.scan(ksize.p, mscan.p, E + 1);
+            int64_t sc[8];
+            drv.gather({{kscan.p + E, mscan.p + E}}, 2, dscal.p, sc);
+            Level lv;
+            lv.N = sc[0];
+            lv.M = sc[1];
+            if (lv.N == 0) continue;
+            lv.off.alloc(lv.N, st);
+            lv.cnt.alloc(lv.N, st);
+            k_lsh_nodes<<<blocks_for(E + 1), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p,
+                                                           lv.off.p, lv.cnt.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            const int64_t N = lv.N;
+            DevBuf<int64_t> tiles(N + 1, st), spairs(N + 1, st), internal(N + 1, st), imem(N + 1, st);
+            DevBuf<int64_t> tile_off(N + 1, st), pair_off(N + 1, st);
+            // every bucket is a leaf (no size limit); k_plan adds C(m, 2)
+            // per bucket to pre_candidates (cps:144)
+            k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, INT32_MAX, tiles.p, spairs.p, internal.p, imem.p,
+                                                      ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            if (plan->cost_only) continue;
+            lv.members.alloc(lv.M, st);
+            k_scatter_children<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p, keep.p, mscan.p, vals2.p,
+                                                              lv.members.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            drv.scan(tiles.p, tile_off.p, N + 1);
+            drv.scan(spairs.p, pair_off.p, N + 1);
+            drv.gather({{tile_off.p + N, pair_off.p + N}}, 2, dscal.p, sc);
+            LeafWork work;
+            work.tiles = sc[0];
+            work.tile_off = tile_off.p;
+            work.pairs = sc[1];
+            work.pair_off = pair_off.p;
+            auto gen_leaf = [&]() {
+                if (work.tiles > 0 || work.pairs > 0)
+                    leaf_dispatch(ctx, st, work, lv, in, plan->accept_dist, plan->lambda_, em.cand.p, em.cand_cap,
+                                  ctr.p);
+            };
+            gen_leaf();
+            drv.gather({{reinterpret_cast<const int64_t *>(&ctr.p->cand_n)}}, 1, dscal.p, sc);
+            em.verify(sc[0], gen_leaf);
+        }
+    }
+    const DevCounters hc = em.finish(drv);
+    stats->n_pairs = ctx->n_pairs;
+    stats->pre_candidates = (int64_t)hc.pre;
+    stats->candidates = em.total_cand;
+    stats->results = (int64_t)hc.res_n;
+    stats->n_levels = L;
     stats->gpu_launches = ctx->launches - launches0;
     stats->lib_calls = ctx->lib_calls - lib0;
 }

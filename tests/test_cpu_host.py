@@ -155,3 +155,28 @@ def test_allpairs_prefix_length_spec_examples():
             sorted([prefix_length(s, lam) for lam in (0.2, 0.4, 0.6, 0.8)], reverse=True)
     with pytest.raises(ValueError):
         prefix_length(0, 0.5)
+
+
+def test_lsh_repetitions_for_recall_spec_examples():
+    from paper_1707_06814_b200.lsh import MinHashJoinParams, repetitions_for_recall, rep_plan
+    assert repetitions_for_recall(0.5, 4, 0.9) == 37
+    assert repetitions_for_recall(0.9, 1, 0.9) == 3
+    assert repetitions_for_recall(0.5, 3, 1e-12) == 1
+    with pytest.raises(ValueError):
+        MinHashJoinParams(lambda_=0.5, phi=1.0)
+    with pytest.raises(ValueError):
+        MinHashJoinParams(lambda_=0.5, k=0)
+    # positions are prefix-stable in L and in range
+    p5, s5 = rep_plan(3, 5, 4, 128)
+    p9, s9 = rep_plan(3, 9, 4, 128)
+    assert np.array_equal(p5, p9[:5]) and np.array_equal(s5, s9[:5])
+    assert p9.min() >= 0 and p9.max() < 128
+
+
+def test_lsh_oracle_plan_restatement_matches_host():
+    from oracle import oracle as O
+    from paper_1707_06814_b200.lsh import rep_plan
+    for seed, L, k in [(0, 3, 10), (7, 40, 3), (123, 2, 1)]:
+        p, s = rep_plan(seed, L, k, 128, path=(1,) if seed == 0 else ())
+        q, r = O.lsh_rep_plan(seed, L, k, 128, path=(1,) if seed == 0 else ())
+        assert np.array_equal(p, q) and np.array_equal(s, r)
