@@ -175,6 +175,46 @@ CPSJ_API int cpsj_lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_
                   cpsj_join_stats *stats, void *stream);
 
 /*
+ * Ingestion.
+ *
+ * cpsj_ingest_lists -- Dataset.from_token_lists (core.py:60-95) on the GPU:
+ *   d_values: int64 tokens of n_records raw records laid end to end,
+ *   d_offsets: int64 n_records + 1.  Per record sort + unique, drop records
+ *   with < 2 distinct tokens, drop duplicate records (first kept); d < 0:
+ *   remap to dense ids by ascending value over the kept records; d >= 0:
+ *   ids kept, every token must lie in [0, d) (else CPSJ_E_ARG "column index
+ *   exceeds matrix dimensions", as the reference's CSR build fails).
+ * cpsj_parse_text -- the SPEC harness loader (load_dataset):
+ *   d_bytes = an ASCII file (one record per line, blank-separated
+ *   non-negative decimal tokens, '\n' line ends with optional '\r'),
+ *   parsed on the GPU, then ingested as above (record = line).  Any other
+ *   byte, or a token >= 2^63, is CPSJ_E_ARG "line L: ..." with the 1-based
+ *   line in stats->error_line.
+ * The output CSR (u32 tokens, int64 offsets) and the input record index of
+ * every kept record stay in the ctx arena until the next ingestion call.
+ */
+typedef struct {
+    int64_t n_sets;           /* kept records                                 */
+    int64_t nnz;              /* tokens of the kept records                   */
+    int64_t d;                /* token universe of the output                 */
+    int64_t n_input_records;  /* records (lines) read                         */
+    int64_t error_line;       /* 1-based line of a parse error, else -1       */
+} cpsj_ingest_stats;
+
+CPSJ_API int cpsj_ingest_lists(cpsj_ctx *ctx, const int64_t *d_values, const int64_t *d_offsets,
+                      int64_t n_records, int64_t d, cpsj_ingest_stats *stats, void *stream);
+CPSJ_API int cpsj_parse_text(cpsj_ctx *ctx, const uint8_t *d_bytes, int64_t n_bytes, int64_t d,
+                    cpsj_ingest_stats *stats, void *stream);
+/* device pointers to the last ingestion's arena: tokens (nnz), offsets
+ * (n_sets + 1), source record index (n_sets) */
+CPSJ_API int cpsj_ingest_result_device(cpsj_ctx *ctx, const uint32_t **d_tokens, const int64_t **d_offsets,
+                              const int64_t **d_source);
+/* copy the last ingestion's arena to host arrays sized from the stats
+ * (any pointer may be NULL) */
+CPSJ_API int cpsj_ingest_copy(cpsj_ctx *ctx, uint32_t *h_tokens, int64_t *h_offsets, int64_t *h_source,
+                     void *stream);
+
+/*
  * Exact joins (SPEC.md module `allpairs`; specified by the
  * reference but not shipped -- here the at-scale recall oracle).
  *

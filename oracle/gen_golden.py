@@ -240,8 +240,59 @@ def ct_main():
     emb_fixture("ct_c1_sample", ds1, 128, 7, [dict(lam=0.5, seed=7, reps=3, ct=True)])
 
 
+def ingest_lists_case(seed, n, d_src, dup_rate, short_rate, neg=False, big=False):
+    """Raw token lists with in-record repeats, short and duplicate records."""
+    rng = np.random.default_rng(seed)
+    lists = []
+    for _ in range(n):
+        u = rng.random()
+        if u < short_rate:
+            k = int(rng.integers(0, 2))
+            row = rng.integers(0, d_src, size=k).tolist() * int(rng.integers(1, 3))
+        elif u < short_rate + dup_rate and lists:
+            row = list(lists[int(rng.integers(0, len(lists)))])
+            rng.shuffle(row)
+        else:
+            row = rng.integers(0, d_src, size=int(rng.integers(2, 40))).tolist()
+            row += row[: int(rng.integers(0, 4))]       # repeats inside the record
+            rng.shuffle(row)
+        lists.append(row)
+    if neg:
+        lists = [[v - d_src // 2 for v in row] for row in lists]
+    if big:
+        lists = [[v * 1_000_003_777 + 12_345 for v in row] for row in lists]
+    return lists
+
+
+def ingest_fixture(name, lists, d):
+    """Input lists and the reference's Dataset.from_token_lists output
+    (core.py:60-95), with source_lines = the input index."""
+    ds = Dataset.from_token_lists(lists, d=d, source_lines=list(range(len(lists))))
+    vals = np.array([v for row in lists for v in row], dtype=np.int64)
+    offs = np.zeros(len(lists) + 1, dtype=np.int64)
+    np.cumsum([len(r) for r in lists], out=offs[1:])
+    out = csr_of(ds) if len(ds) else dict(tokens=np.zeros(0, np.uint32), offsets=np.zeros(1, np.int64),
+                                          sizes=np.zeros(0, np.int64), d=np.int64(ds.d))
+    # the text form of the same records (one line per record)
+    text = "".join(" ".join(str(v) for v in row) + "\n" for row in lists) if not np.any(vals < 0) else ""
+    save(name, in_values=vals, in_offsets=offs, in_d=np.int64(-1 if d is None else d),
+         out_tokens=out["tokens"], out_offsets=out["offsets"], out_d=np.int64(ds.d),
+         out_source=np.asarray(ds.source_lines, dtype=np.int64), text=np.frombuffer(text.encode(), dtype=np.uint8))
+
+
+def ingest_main():
+    ingest_fixture("ingest_dense_remap", ingest_lists_case(1, 1500, 500, 0.1, 0.1), None)
+    ingest_fixture("ingest_given_d", ingest_lists_case(2, 1500, 800, 0.15, 0.05), 800)
+    ingest_fixture("ingest_negative", ingest_lists_case(3, 1000, 300, 0.1, 0.1, neg=True), None)
+    ingest_fixture("ingest_big_values", ingest_lists_case(4, 1000, 5000, 0.05, 0.05, big=True), None)
+    ingest_fixture("ingest_all_short", [[1], [], [2, 2, 2], [7]], None)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--ingest-only" in sys.argv:
+        ingest_main()
+        return
     if "--rs-only" in sys.argv:
         rs_main()
         return

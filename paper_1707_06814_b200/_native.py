@@ -33,6 +33,10 @@ class LshPlan(ctypes.Structure):
                 ("h_rep_seeds", P), ("cost_only", i32)]
 
 
+class IngestStats(ctypes.Structure):
+    _fields_ = [("n_sets", i64), ("nnz", i64), ("d", i64), ("n_input_records", i64), ("error_line", i64)]
+
+
 class JoinStats(ctypes.Structure):
     _fields_ = [("n_pairs", i64), ("pre_candidates", i64), ("candidates", i64), ("results", i64),
                 ("max_depth", i64), ("peak_live_members", i64), ("n_depth_cap_events", i64),
@@ -43,7 +47,7 @@ EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_err
            "cpsj_family_create", "cpsj_family_destroy", "cpsj_minhash_sketch", "cpsj_self_join",
            "cpsj_join_copy_result", "cpsj_join_result_device", "cpsj_profile_enable", "cpsj_profile_read",
            "cpsj_launch_counts", "cpsj_frequency_order", "cpsj_exact_join",
-           "cpsj_lsh_join"]
+           "cpsj_lsh_join", "cpsj_ingest_lists", "cpsj_parse_text", "cpsj_ingest_result_device", "cpsj_ingest_copy"]
 
 PROF_CLASSES = ["k1_minhash", "k4_leaf", "point", "node", "split", "k5_verify", "k6_dedup", "plan"]
 
@@ -82,6 +86,10 @@ def load(path: str | None = None):
         L.cpsj_launch_counts.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.cpsj_frequency_order.argtypes = [P, P, i64, i64, P, P, P]
         L.cpsj_lsh_join.argtypes = [P, ctypes.POINTER(Inputs), ctypes.POINTER(LshPlan), ctypes.POINTER(JoinStats), P]
+        L.cpsj_ingest_lists.argtypes = [P, P, P, i64, i64, ctypes.POINTER(IngestStats), P]
+        L.cpsj_parse_text.argtypes = [P, P, i64, i64, ctypes.POINTER(IngestStats), P]
+        L.cpsj_ingest_result_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
+        L.cpsj_ingest_copy.argtypes = [P, P, P, P, P]
         L.cpsj_exact_join.argtypes = [P, P, P, i64, i64, dbl, i32, ctypes.POINTER(JoinStats), P]
         _lib = L
         return L

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 SO = os.path.join(OUT_DIR, "libcpsjoin_b200.so")
-SOURCES = ["minhash.cu", "join.cu", "exact.cu", "capi.cu"]
+SOURCES = ["minhash.cu", "join.cu", "exact.cu", "ingest.cu", "capi.cu"]
 HEADERS = ["cpsj_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -69,6 +69,9 @@ int cpsj_ctx_destroy(cpsj_ctx *ctx) {
         CPSJ_CUDA(cudaDeviceSynchronize());
         ctx->res_keys.release();
         ctx->res_sims.release();
+        ctx->ing_tokens.release();
+        ctx->ing_offsets.release();
+        ctx->ing_src.release();
         if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
         ctx->h_scalars = nullptr;
     });
@@ -172,6 +175,52 @@ int cpsj_lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_plan *pla
                                     (in->d_sketch || plan->cost_only)),
                       "null input pointers");
         cpsj::lsh_join(ctx, in, plan, stats, (cudaStream_t)stream);
+    });
+}
+
+int cpsj_ingest_lists(cpsj_ctx *ctx, const int64_t *d_values, const int64_t *d_offsets, int64_t n_records,
+                      int64_t d, cpsj_ingest_stats *stats, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(stats != nullptr, "null stats");
+        cpsj::require(n_records == 0 || (d_values && d_offsets), "null input pointers");
+        cpsj::require(d < ((int64_t)1 << 32), "token universe must be below 2^32");
+        cpsj::ingest_lists(ctx, d_values, d_offsets, n_records, d, stats, (cudaStream_t)stream);
+    });
+}
+
+int cpsj_parse_text(cpsj_ctx *ctx, const uint8_t *d_bytes, int64_t n_bytes, int64_t d, cpsj_ingest_stats *stats,
+                    void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(stats != nullptr, "null stats");
+        cpsj::require(n_bytes == 0 || d_bytes, "null input pointer");
+        cpsj::require(d < ((int64_t)1 << 32), "token universe must be below 2^32");
+        cpsj::parse_text(ctx, d_bytes, n_bytes, d, stats, (cudaStream_t)stream);
+    });
+}
+
+int cpsj_ingest_result_device(cpsj_ctx *ctx, const uint32_t **d_tokens, const int64_t **d_offsets,
+                              const int64_t **d_source) {
+    if (!ctx) return CPSJ_E_ARG;
+    if (d_tokens) *d_tokens = ctx->ing_tokens.p;
+    if (d_offsets) *d_offsets = ctx->ing_offsets.p;
+    if (d_source) *d_source = ctx->ing_src.p;
+    return CPSJ_OK;
+}
+
+int cpsj_ingest_copy(cpsj_ctx *ctx, uint32_t *h_tokens, int64_t *h_offsets, int64_t *h_source, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cudaStream_t st = (cudaStream_t)stream;
+        if (h_tokens && ctx->ing_tokens.n)
+            CPSJ_CUDA(cudaMemcpyAsync(h_tokens, ctx->ing_tokens.p, ctx->ing_nnz * 4, cudaMemcpyDeviceToHost, st));
+        if (h_offsets && ctx->ing_offsets.n)
+            CPSJ_CUDA(cudaMemcpyAsync(h_offsets, ctx->ing_offsets.p, (ctx->ing_n + 1) * 8, cudaMemcpyDeviceToHost,
+                                      st));
+        if (h_source && ctx->ing_src.n)
+            CPSJ_CUDA(cudaMemcpyAsync(h_source, ctx->ing_src.p, ctx->ing_n * 8, cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -146,6 +146,11 @@ struct cpsj_ctx {
     cpsj::DevBuf<double> res_sims;
     int64_t n_pairs = 0;
     std::vector<int64_t> cap_events;
+    // CSR arena of the last ingestion
+    cpsj::DevBuf<uint32_t> ing_tokens;
+    cpsj::DevBuf<int64_t> ing_offsets;
+    cpsj::DevBuf<int64_t> ing_src;
+    int64_t ing_n = 0, ing_nnz = 0;
     // pinned scratch for small device->host reads
     int64_t *h_scalars = nullptr;
     int64_t launches = 0;
@@ -195,6 +200,10 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                cudaStream_t stream);
 void lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_plan *plan, cpsj_join_stats *stats,
               cudaStream_t st);
+void ingest_lists(cpsj_ctx *ctx, const int64_t *d_values, const int64_t *d_offsets, int64_t n, int64_t d,
+                  cpsj_ingest_stats *out, cudaStream_t st);
+void parse_text(cpsj_ctx *ctx, const uint8_t *d_bytes, int64_t B, int64_t d, cpsj_ingest_stats *out,
+                cudaStream_t st);
 void frequency_order(cpsj_ctx *ctx, const uint32_t *d_tokens, int64_t nnz, int64_t d, uint32_t *d_rank,
                      uint32_t *d_order, cudaStream_t st);
 void exact_join(cpsj_ctx *ctx, const uint32_t *tok, const int64_t *off, int64_t n, int64_t d, double lam, int naive,

@@ -180,3 +180,10 @@ def test_lsh_oracle_plan_restatement_matches_host():
         p, s = rep_plan(seed, L, k, 128, path=(1,) if seed == 0 else ())
         q, r = O.lsh_rep_plan(seed, L, k, 128, path=(1,) if seed == 0 else ())
         assert np.array_equal(p, q) and np.array_equal(s, r)
+
+
+def test_write_pairs_format(tmp_path):
+    from paper_1707_06814_b200.ingest import write_pairs
+    p = tmp_path / "out.txt"
+    write_pairs(str(p), [0, 3], [5, 9], [0.5, 2.0 / 3.0])
+    assert p.read_text() == "0 5 0.500000\n3 9 0.666667\n"
