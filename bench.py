@@ -50,6 +50,8 @@ def parse():
     # contends for the GIL with the launch path and slows the step (measured)
     ap.add_argument("--clock-source", default="points", choices=["points", "nvml", "smi"])
     ap.add_argument("--clock-ms", type=int, default=1000)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional multi-rank run through host-staged collectives (not a bench number)")
     return ap.parse_args()
 
 
@@ -618,9 +620,14 @@ def main():
         return
     import torch
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.distributed.init_process_group("gloo")
     try:
         run_ours(args, rank, world)
     finally:

@@ -82,9 +82,11 @@ def _gather_rows(shard, world: int, group=None):
         out = torch.empty((world * shard.shape[0],) + tuple(shard.shape[1:]), dtype=shard.dtype, device=shard.device)
         dist.all_gather_into_tensor(out, shard.contiguous(), group=group)
         return out
-    parts = [torch.empty_like(shard) for _ in range(world)]
-    dist.all_gather(parts, shard.contiguous(), group=group)
-    return torch.cat(parts)
+    # gloo (CPU tests, functional runs): stage through host memory
+    host = shard.detach().cpu().contiguous()
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host, group=group)
+    return torch.cat(parts).to(shard.device)
 
 
 def embed_sharded(eparams, d_tok, d_off, d: int, sketch, rank: int, world: int, group=None, local_k1=None):
