@@ -27,6 +27,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -894,10 +897,19 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     // Three host synchronisations per level: (A) leaf/internal totals,
     // (B) candidate count + flag/entry totals, (C) child totals.  Every
     // other size is an upper bound known on the host or read on the device.
+    // CPSJ_JOIN_TRACE=1: per-level sizes and host time on stderr (diagnostics;
+    // adds a synchronisation per level)
+    const char *trace_env = getenv("CPSJ_JOIN_TRACE");
+    const bool trace = trace_env != nullptr && trace_env[0] == '1';
+    auto t_level = std::chrono::steady_clock::now();
     for (int depth = 0; lv.N > 0; ++depth) {
         levels++;
         max_depth = depth;
         const int64_t N = lv.N;
+        if (trace) {
+            CPSJ_CUDA(cudaStreamSynchronize(st));
+            t_level = std::chrono::steady_clock::now();
+        }
         // ---- (A) plan: leaves vs internal nodes
         std::unique_ptr<ProfScope> prof_plan(new ProfScope(ctx, PROF_PLAN, st));
         DevBuf<int64_t> tiles(N + 1, st), spairs(N + 1, st), internal(N + 1, st), imem(N + 1, st);
@@ -1093,6 +1105,17 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                                                               nx.members.p);
             CPSJ_LAUNCH_CHECK();
             ctx->launches += 2;
+        }
+        if (trace) {
+            CPSJ_CUDA(cudaStreamSynchronize(st));
+            const double us =
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_level).count();
+            fprintf(stderr,
+                    "[join] depth %d nodes %lld members %lld internal %lld (members %lld) leaf_tiles %lld "
+                    "leaf_pairs %lld leaf_cand %lld flagged %lld entries %lld children %lld | %.1f us\n",
+                    depth, (long long)N, (long long)lv.M, (long long)n_int, (long long)Mi, (long long)work.tiles,
+                    (long long)work.pairs, (long long)n_leaf_cand, (long long)n_flag, (long long)E,
+                    (long long)nx.N, us);
         }
         lv = std::move(nx);
     }

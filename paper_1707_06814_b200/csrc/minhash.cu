@@ -12,15 +12,18 @@
 // Design.  The work is Sum|x| * F hash evaluations; every evaluation is
 // L table lookups (L = key bytes that vary, chosen from max_token; the
 // constant upper-byte entries are folded into table L-1).  A warp owns one
-// set and its 32 lanes own 32 functions of the current chunk, so one
-// token is hashed by 32 functions at once and lane f reads entry
-// [k][byte][f] of a [L][256][32] shared-memory table: the 32 lanes hit 32
-// consecutive words -> one conflict-free wavefront per lookup.  Only the
-// high 32 bits of g are compared in the hot loop; a tie on the high word
-// (p ~ |x| 2^-32 per set and function) sets a flag and that lane
-// re-resolves the set with the full 64-bit hash from global memory.
-// The bound is the shared-memory crossbar (128 B/clk/SM) and the integer
-// ALU issue; HBM traffic is the token stream once per chunk.
+// set and its lanes own the functions of the current chunk, so one token
+// (broadcast by SHFL) is hashed by every function of the chunk at once.
+//   k_minhash_k16<L> (L <= 3, the production kernel): 128 functions per
+//     chunk, the top 16 hash bits of 4 functions per lane in one LDS.64,
+//     keys (hash16 << 16 | position) with first/last tie detection and a
+//     warp-cooperative 64-bit resolution of 16-bit ties; tables arrive by
+//     TMA bulk copy from prebuilt images.  Integer-ALU bound (ncu ALU pipe
+//     ~81%); two further variants were measured and rejected (keys built
+//     on the FMA pipe: -16%; PRMT-only table addresses: -1%).
+//   k_minhash<L> (L = 4, tokens >= 2^24, and the CPSJ_K1_NARROW A/B
+//     switch): 32 functions per chunk on the high hash word.
+// HBM traffic is the token stream once per chunk.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -134,46 +137,9 @@ __global__ void __launch_bounds__(K1_THREADS) k_minhash(
 }
 
 // ---------------------------------------------------------------------
-// 64-function variant (key bytes L <= 3): every lane owns TWO functions of
-// a 64-function chunk (f = lane and f = lane + 32), the table row of one
-// (byte table k, byte value b) is 32 lanes x uint2 = 256 B, and one LDS.64
-// per lane fetches both functions' entries (2 conflict-free wavefronts).
-// Per token the warp-uniform address math (3 byte offsets) and the token
-// broadcast are amortised over 64 evaluations instead of 32.
+// Wide kernels: 32 warps per CTA, one CTA per SM.
 constexpr int K1W_WARPS = 32;
 constexpr int K1W_THREADS = K1W_WARPS * 32;
-
-struct MinState {
-    uint32_t best, tok;
-    bool tie;
-};
-
-__device__ __forceinline__ void min_update(MinState &m, uint32_t h, uint32_t tok) {
-    const bool lt = h < m.best;
-    m.tie = lt ? false : (m.tie | (h == m.best));
-    m.tok = lt ? tok : m.tok;
-    m.best = lt ? h : m.best;
-}
-
-template <int L>
-__device__ __forceinline__ uint2 hi_pair(const char *tab, uint32_t tok, uint32_t lane8) {
-    // byte offsets of entries (k, b, lane) = k * 64 KiB + b * 256 + lane * 8
-    const uint32_t o0 = ((tok << 8) & 0xFF00u) | lane8;
-    uint2 h = *reinterpret_cast<const uint2 *>(tab + o0);
-    if (L > 1) {
-        const uint32_t o1 = (tok & 0xFF00u) | lane8;
-        const uint2 v = *reinterpret_cast<const uint2 *>(tab + 65536 + o1);
-        h.x ^= v.x;
-        h.y ^= v.y;
-    }
-    if (L > 2) {
-        const uint32_t o2 = ((tok >> 8) & 0xFF00u) | lane8;
-        const uint2 v = *reinterpret_cast<const uint2 *>(tab + 131072 + o2);
-        h.x ^= v.x;
-        h.y ^= v.y;
-    }
-    return h;
-}
 
 __device__ __forceinline__ uint32_t resolve_tie(const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
                                                 int fn, const uint32_t *__restrict__ tokens, int64_t beg,
@@ -188,120 +154,12 @@ __device__ __forceinline__ uint32_t resolve_tie(const uint32_t *__restrict__ hi,
     return bt;
 }
 
-__device__ __forceinline__ uint32_t sketch_bit(const uint32_t *__restrict__ bitmask, int fn, uint32_t tok) {
-    const uint32_t *bm = bitmask + (size_t)fn * 32;
-    const uint32_t b0 = tok & 255, b1 = (tok >> 8) & 255, b2 = (tok >> 16) & 255, b3 = tok >> 24;
-    return ((bm[b0 >> 5] >> (b0 & 31)) ^ (bm[8 + (b1 >> 5)] >> (b1 & 31)) ^ (bm[16 + (b2 >> 5)] >> (b2 & 31)) ^
-            (bm[24 + (b3 >> 5)] >> (b3 & 31))) & 1u;
-}
-
-template <int L>
-__global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash64(
-    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
-    const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
-    const uint32_t *__restrict__ bitmask, int F, uint32_t *__restrict__ values,
-    uint64_t *__restrict__ sketch) {
-    extern __shared__ uint2 tab2[];  // [L][256][32] x {f = lane, f = lane + 32}
-    const char *tab = reinterpret_cast<const char *>(tab2);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t lane8 = (uint32_t)lane << 3;
-    const int nchunks = (F + 63) >> 6;
-    const int words = F >> 6;  // sketch words per set
-    for (int c = 0; c < nchunks; ++c) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < L * 256 * 32; e += K1W_THREADS) {
-            const int k = e >> 13, b = (e >> 5) & 255, ln = e & 31;
-            uint2 v = make_uint2(0u, 0u);
-            const int f0 = (c << 6) + ln, f1 = f0 + 32;
-            if (f0 < F) {
-                const size_t base = (size_t)f0 * 1024;
-                v.x = hi[base + k * 256 + b];
-                if (k == L - 1)
-                    for (int kk = L; kk < 4; ++kk) v.x ^= hi[base + kk * 256];
-            }
-            if (f1 < F) {
-                const size_t base = (size_t)f1 * 1024;
-                v.y = hi[base + k * 256 + b];
-                if (k == L - 1)
-                    for (int kk = L; kk < 4; ++kk) v.y ^= hi[base + kk * 256];
-            }
-            tab2[e] = v;
-        }
-        __syncthreads();
-        const int fn0 = (c << 6) + lane, fn1 = fn0 + 32;
-        for (int64_t s = (int64_t)blockIdx.x * K1W_WARPS + warp; s < n; s += (int64_t)gridDim.x * K1W_WARPS) {
-            const int64_t beg = offsets[s], end = offsets[s + 1];
-            MinState m0{0, 0, false}, m1{0, 0, false};
-            for (int64_t base = beg; base < end; base += 32) {
-                const int cnt = end - base < 32 ? (int)(end - base) : 32;
-                const uint32_t mine = lane < cnt ? __ldg(tokens + base + lane) : 0u;
-                int j = 0;
-                if (base == beg) {
-                    const uint32_t tok = __shfl_sync(0xffffffffu, mine, 0);
-                    const uint2 h = hi_pair<L>(tab, tok, lane8);
-                    m0 = MinState{h.x, tok, false};
-                    m1 = MinState{h.y, tok, false};
-                    j = 1;
-                }
-#pragma unroll 4
-                for (; j < cnt; ++j) {
-                    const uint32_t tok = __shfl_sync(0xffffffffu, mine, j);
-                    const uint2 h = hi_pair<L>(tab, tok, lane8);
-                    min_update(m0, h.x, tok);
-                    min_update(m1, h.y, tok);
-                }
-            }
-            // full 64-bit resolution of a high-word tie (hashing.py:124)
-            if (m0.tie && fn0 < F) m0.tok = resolve_tie(hi, lo, fn0, tokens, beg, end);
-            if (m1.tie && fn1 < F) m1.tok = resolve_tie(hi, lo, fn1, tokens, beg, end);
-            if (end == beg) m0.tok = m1.tok = 0;
-            if (values != nullptr) {
-                if (fn0 < F) values[s * F + fn0] = m0.tok;
-                if (fn1 < F) values[s * F + fn1] = m1.tok;
-            }
-            if (sketch != nullptr) {
-                const uint32_t w0 = __ballot_sync(0xffffffffu, end > beg && sketch_bit(bitmask, fn0, m0.tok));
-                const uint32_t w1 = __ballot_sync(0xffffffffu, end > beg && sketch_bit(bitmask, fn1, m1.tok));
-                if (lane == 0) sketch[s * words + c] = ((uint64_t)w1 << 32) | w0;
-            }
-        }
-    }
-}
-
 // ---------------------------------------------------------------------
-// Keyed variant (sets of <= 2048 tokens).  The smem tables hold the high
-// hash word with its low 11 bits cleared, so key = (T0 ^ T1 ^ T2) | p is
-// (21-bit hash part, 11-bit position p of the token in its set); a single
-// unsigned min over keys is the argmin over the hash part (ties broken by
-// position).  The second smallest key is tracked with min(max(.)); if its
-// hash part equals the minimum's, two tokens tie on the compared bits and
-// the lane re-resolves the set with the full 64-bit hash (hashing.py:124),
-// which also settles every case the 21-bit compare cannot.  Five integer
-// ops per evaluation instead of eight for the flag-based update.
-constexpr int KEY_BITS = 11;
-constexpr uint32_t KEY_MASK = (1u << KEY_BITS) - 1;
-
+// Shared-memory helpers of the 16-bit keyed kernel below.
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
     return v;
-}
-
-template <int L>
-__device__ __forceinline__ uint2 key_pair(uint32_t tok, uint32_t lane_base) {
-    // entry (k, b, lane) lives at k * 64 KiB + b * 256 + lane * 8
-    uint2 h = lds64(lane_base + __byte_perm(tok, 0u, 0x4404));
-    if (L > 1) {
-        const uint2 v = lds64(lane_base + 65536u + (tok & 0xFF00u));
-        h.x ^= v.x;
-        h.y ^= v.y;
-    }
-    if (L > 2) {
-        const uint2 v = lds64(lane_base + 131072u + __byte_perm(tok, 0u, 0x4424));
-        h.x ^= v.x;
-        h.y ^= v.y;
-    }
-    return h;
 }
 
 // Tie detection without a second-minimum: `first` is the min over
@@ -327,10 +185,6 @@ __device__ __forceinline__ void key_update(KeyMin &k, uint32_t h, uint32_t p, ui
     k.last = min(k.last, imad_add(h, q));
 }
 
-__device__ __forceinline__ bool key_tie(const KeyMin &k) {
-    return (k.first & KEY_MASK) != KEY_MASK - (k.last & KEY_MASK);
-}
-
 // sketch bit from the chunk's shared-memory copy of the bit-table low bits
 // (row stride 33 words spreads the 32 lanes over the banks)
 __device__ __forceinline__ uint32_t sketch_bit_s(const uint32_t *bm_s, int fl, uint32_t tok) {
@@ -340,132 +194,13 @@ __device__ __forceinline__ uint32_t sketch_bit_s(const uint32_t *bm_s, int fl, u
             (bm[24 + (b3 >> 5)] >> (b3 & 31))) & 1u;
 }
 
-template <int L>
-__global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_keyed(
-    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
-    const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
-    const uint32_t *__restrict__ bitmask, int F, uint32_t *__restrict__ values,
-    uint64_t *__restrict__ sketch) {
-    extern __shared__ uint2 tab2[];  // [L][256][32] x {f = lane, f = lane + 32}, then bit masks
-    // low bits of the chunk's bit tables: [64 functions][33 (4 x 8 + pad)] u32
-    uint32_t *bm_s = reinterpret_cast<uint32_t *>(tab2 + L * 256 * 32);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t lane_base = (uint32_t)__cvta_generic_to_shared(tab2) + ((uint32_t)lane << 3);
-    const int nchunks = (F + 63) >> 6;
-    const int words = F >> 6;
-    const int64_t s_first = (int64_t)blockIdx.x * K1W_WARPS + warp, s_step = (int64_t)gridDim.x * K1W_WARPS;
-    for (int c = 0; c < nchunks; ++c) {
-        __syncthreads();
-        if (sketch != nullptr) {
-            for (int e = threadIdx.x; e < 64 * 32; e += K1W_THREADS) {
-                const int fl = e >> 5, w = e & 31, fn = (c << 6) + fl;
-                bm_s[fl * 33 + w] = fn < F ? bitmask[(size_t)fn * 32 + w] : 0u;
-            }
-        }
-        for (int e = threadIdx.x; e < L * 256 * 32; e += K1W_THREADS) {
-            const int k = e >> 13, b = (e >> 5) & 255, ln = e & 31;
-            uint2 v = make_uint2(0u, 0u);
-            const int f0 = (c << 6) + ln, f1 = f0 + 32;
-            if (f0 < F) {
-                const size_t base = (size_t)f0 * 1024;
-                v.x = hi[base + k * 256 + b];
-                if (k == L - 1)
-                    for (int kk = L; kk < 4; ++kk) v.x ^= hi[base + kk * 256];
-            }
-            if (f1 < F) {
-                const size_t base = (size_t)f1 * 1024;
-                v.y = hi[base + k * 256 + b];
-                if (k == L - 1)
-                    for (int kk = L; kk < 4; ++kk) v.y ^= hi[base + kk * 256];
-            }
-            v.x &= ~KEY_MASK;
-            v.y &= ~KEY_MASK;
-            tab2[e] = v;
-        }
-        __syncthreads();
-        const int fn0 = (c << 6) + lane, fn1 = fn0 + 32;
-        // software-pipelined set loop: the next set's offsets are in flight
-        // while the current set is hashed
-        int64_t nbeg = 0, nend = 0;
-        if (s_first < n) {
-            nbeg = offsets[s_first];
-            nend = offsets[s_first + 1];
-        }
-        for (int64_t s = s_first; s < n; s += s_step) {
-            const int64_t beg = nbeg, end = nend;
-            if (s + s_step < n) {
-                nbeg = offsets[s + s_step];
-                nend = offsets[s + s_step + 1];
-            }
-            const int len = (int)(end - beg);
-            uint32_t t0 = 0, t1 = 0;
-            if (len > (int)KEY_MASK + 1) {
-                // long set: the 11-bit position field would wrap; resolve
-                // every function exactly (rare: sets > 2048 tokens)
-                if (fn0 < F) t0 = resolve_tie(hi, lo, fn0, tokens, beg, end);
-                if (fn1 < F) t1 = resolve_tie(hi, lo, fn1, tokens, beg, end);
-            } else if (len > 0) {
-                KeyMin k0{0xFFFFFFFFu, 0xFFFFFFFFu}, k1{0xFFFFFFFFu, 0xFFFFFFFFu};
-                for (int base = 0; base < len; base += 32) {
-                    const int cnt = len - base < 32 ? len - base : 32;
-                    const uint32_t mine = lane < cnt ? __ldg(tokens + beg + base + lane) : 0u;
-#pragma unroll 4
-                    for (int j = 0; j < cnt; ++j) {
-                        const uint32_t tok = __shfl_sync(0xffffffffu, mine, j);
-                        const uint2 h = key_pair<L>(tok, lane_base);
-                        // the hash words have their low KEY_BITS cleared, so
-                        // "| p" == "+ p"; IMADs keep the key formation off
-                        // the ALU pipe, this loop's bottleneck (ncu: alu 83%)
-                        const uint32_t p = (uint32_t)(base + j);
-                        const uint32_t q = KEY_MASK - p;
-                        key_update(k0, h.x, p, q);
-                        key_update(k1, h.y, p, q);
-                    }
-                }
-                if (key_tie(k0) && fn0 < F)
-                    t0 = resolve_tie(hi, lo, fn0, tokens, beg, end);
-                else
-                    t0 = __ldg(tokens + beg + (k0.first & KEY_MASK));
-                if (key_tie(k1) && fn1 < F)
-                    t1 = resolve_tie(hi, lo, fn1, tokens, beg, end);
-                else
-                    t1 = __ldg(tokens + beg + (k1.first & KEY_MASK));
-            }
-            if (values != nullptr) {
-                if (fn0 < F) values[s * F + fn0] = t0;
-                if (fn1 < F) values[s * F + fn1] = t1;
-            }
-            if (sketch != nullptr) {
-                const uint32_t w0 = __ballot_sync(0xffffffffu, len > 0 && fn0 < F && sketch_bit_s(bm_s, lane, t0));
-                const uint32_t w1 = __ballot_sync(0xffffffffu, len > 0 && fn1 < F &&
-                                                                   sketch_bit_s(bm_s, lane + 32, t1));
-                if (lane == 0) sketch[s * words + c] = ((uint64_t)w1 << 32) | w0;
-            }
-        }
-    }
-}
-
-template <int L>
-static void launch_minhash_keyed(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
-                                 int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
-    const int smem = L * 256 * 32 * 8 + (sketch != nullptr ? 64 * 33 * 4 : 0);
-    CPSJ_CUDA(cudaFuncSetAttribute(k_minhash_keyed<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
-    ProfScope prof(ctx, PROF_K1, stream);
-    k_minhash_keyed<L><<<grid, K1W_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask,
-                                                            fam->F, values, sketch);
-    CPSJ_LAUNCH_CHECK();
-    ctx->launches++;
-}
-
 // ---------------------------------------------------------------------
 // 16-bit keyed variant (key bytes L <= 3, sets <= 65536 tokens): the
 // shared tables keep only the top 16 bits of each hash, so one LDS.64 per
 // lane fetches FOUR functions' entries (f = lane, +32, +64, +96 of a
 // 128-function chunk) and both the shared-memory traffic and the per-token
 // address work per evaluation halve.  Keys are (hash16 << 16) | position;
-// first/last minimum tie detection as in k_minhash_keyed.  A tie on the
+// first/last minimum tie detection (key_update).  A tie on the
 // 16 compared bits (p ~ |x| / 2^16 per set and function) re-resolves that
 // function on the full 64-bit hash, so the result stays bit-exact.
 constexpr uint32_t K16_MASK = 0xFFFFu;
@@ -597,16 +332,17 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
     const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
     const uint2 *__restrict__ img16, const uint32_t *__restrict__ bmimg, int F, uint32_t *__restrict__ values,
     uint64_t *__restrict__ sketch) {
-    // [L][256][32] x uint2 {f0 << 16 | f32, f64 << 16 | f96} (16-bit hashes), then bit masks
+    // [L][256][32] x uint2 {f0 << 16 | f32, f64 << 16 | f96} (16-bit hashes),
+    // then the bit masks, then the mbarrier (no static shared memory)
     extern __shared__ __align__(128) uint2 tab2[];
-    __shared__ __align__(8) uint64_t mbar;
     uint32_t *bm_s = reinterpret_cast<uint32_t *>(tab2 + L * 256 * 32);  // [128][33]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(bm_s + (sketch != nullptr ? 128 * 33 : 0));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lane_base = (uint32_t)__cvta_generic_to_shared(tab2) + ((uint32_t)lane << 3);
     const int nchunks = (F + 127) >> 7;
     const int words32 = F >> 5;
     const int64_t s_first = (int64_t)blockIdx.x * K1W_WARPS + warp, s_step = (int64_t)gridDim.x * K1W_WARPS;
-    const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(&mbar);
+    const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(mbar);
     if (threadIdx.x == 0) mbar_init(mbar_a, 1);
     __syncthreads();
     uint32_t phase = 0;
@@ -708,28 +444,14 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
 template <int L>
 static void launch_minhash_k16(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
                                int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
-    const int smem = L * 256 * 32 * 8 + (sketch != nullptr ? 128 * 33 * 4 : 0);
+    const int smem = L * 256 * 32 * 8 + (sketch != nullptr ? 128 * 33 * 4 : 0) + 16;  // + mbarrier
     CPSJ_CUDA(cudaFuncSetAttribute(k_minhash_k16<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
     ProfScope prof(ctx, PROF_K1, stream);
-    k_minhash_k16<L><<<grid, K1W_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo,
-                                                          reinterpret_cast<const uint2 *>(fam->d_img16[L - 1]),
-                                                          fam->d_bmimg, fam->F, values, sketch);
-    CPSJ_LAUNCH_CHECK();
-    ctx->launches++;
-}
-
-template <int L>
-static void launch_minhash64(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
-                             int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
-    const int smem = L * 256 * 32 * 8;
-    CPSJ_CUDA(cudaFuncSetAttribute(k_minhash64<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
-    ProfScope prof(ctx, PROF_K1, stream);
-    k_minhash64<L><<<grid, K1W_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask,
-                                                        fam->F, values, sketch);
+    k_minhash_k16<L><<<grid, K1W_THREADS, smem, stream>>>(
+        tok, off, n, fam->d_hi, fam->d_lo, reinterpret_cast<const uint2 *>(fam->d_img16[L - 1]), fam->d_bmimg,
+        fam->F, values, sketch);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
 }
@@ -789,24 +511,6 @@ int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_toke
             case 1: launch_minhash<1>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
             case 2: launch_minhash<2>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
             default: launch_minhash<3>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
-        }
-        return 0;
-    }
-    const char *flagged = getenv("CPSJ_K1_FLAGGED");  // A/B switch for the flag-based 64-function kernel
-    if (flagged != nullptr && flagged[0] == '1' && L < 4) {
-        switch (L) {
-            case 1: launch_minhash64<1>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-            case 2: launch_minhash64<2>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-            default: launch_minhash64<3>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-        }
-        return 0;
-    }
-    const char *k32 = getenv("CPSJ_K1_KEY32");  // A/B switch for the 32-bit-key kernel
-    if (k32 != nullptr && k32[0] == '1' && L < 4) {
-        switch (L) {
-            case 1: launch_minhash_keyed<1>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-            case 2: launch_minhash_keyed<2>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-            default: launch_minhash_keyed<3>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
         }
         return 0;
     }
