@@ -50,6 +50,8 @@ def parse():
     # contends for the GIL with the launch path and slows the step (measured)
     ap.add_argument("--clock-source", default="points", choices=["points", "nvml", "smi"])
     ap.add_argument("--clock-ms", type=int, default=1000)
+    ap.add_argument("--k1-transport", default="p2p", choices=["p2p", "collective"],
+                    help="N>1: K1 rows stored on every GPU by the kernel (p2p) or an NCCL all-gather after it")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional multi-rank run through host-staged collectives (not a bench number)")
     return ap.parse_args()
@@ -391,7 +393,8 @@ def run_ours(args, rank: int, world: int):
 
     from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
     from paper_1707_06814_b200._native import Context
-    from paper_1707_06814_b200.distributed import embed_sharded, embedded_from_parts, shard_reps
+    from paper_1707_06814_b200.distributed import (PeerArrays, embed_sharded, embed_sharded_p2p,
+                                                   embedded_from_parts, shard_reps)
     from paper_1707_06814_b200.embed import embed_device_csr
     from paper_1707_06814_b200.workloads import CONFIGS, generate
 
@@ -435,6 +438,26 @@ def run_ours(args, rank: int, world: int):
 
     skey = (cfg.ell, cfg.join_seed)
 
+    peers = None
+    if world > 1 and args.k1_transport == "p2p":
+        # node-wide exchange buffers: K1 stores every row on every GPU
+        peers = PeerArrays(ctx, n, 128, cfg.ell, rank, world)
+
+    def k1_sharded(t_tok, t_off, ev=None):
+        if peers is not None:
+            # set-sharded K1 with the all-gather fused into its epilogue
+            vals, _ = embed_sharded_p2p(eparams, t_tok, t_off, w.d, None, rank, world, peers)
+            if ev is not None:
+                ev[1].record(stream)
+            _, sk = embed_sharded_p2p(None, t_tok, t_off, w.d, skey, rank, world, peers)
+        else:
+            # set-sharded K1 + NCCL all-gather of the value / sketch rows
+            vals, _ = embed_sharded(eparams, t_tok, t_off, w.d, None, rank, world)
+            if ev is not None:
+                ev[1].record(stream)
+            _, sk = embed_sharded(None, t_tok, t_off, w.d, skey, rank, world)
+        return embedded_from_parts(eparams, t_tok, t_off, w.d, vals, sk, skey)
+
     def step_device():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
@@ -443,11 +466,7 @@ def run_ours(args, rank: int, world: int):
             ev[1].record(stream)
             emb.sketches_device(*skey)
         else:
-            # set-sharded K1 + NVLink all-gather of the value / sketch rows
-            vals, _ = embed_sharded(eparams, d_tok, d_off, w.d, None, rank, world)
-            ev[1].record(stream)
-            _, sk = embed_sharded(None, d_tok, d_off, w.d, skey, rank, world)
-            emb = embedded_from_parts(eparams, d_tok, d_off, w.d, vals, sk, skey)
+            emb = k1_sharded(d_tok, d_off, ev)
         ev[2].record(stream)
         k1_events.append(ev)
         return shard_reps(emb, params, rank, world)
@@ -458,8 +477,7 @@ def run_ours(args, rank: int, world: int):
         else:
             t_tok = tok_pin.to(dev, non_blocking=True)
             t_off = off_pin.to(dev, non_blocking=True)
-            vals, sk = embed_sharded(eparams, t_tok, t_off, w.d, skey, rank, world)
-            emb = embedded_from_parts(eparams, t_tok, t_off, w.d, vals, sk, skey)
+            emb = k1_sharded(t_tok, t_off)
         return shard_reps(emb, params, rank, world)
 
     def timed(fn, steps, probe=None):
@@ -574,7 +592,8 @@ def run_ours(args, rank: int, world: int):
         "data": "synthetic (seeded generator for BASELINE.json config; Mann et al. datasets unavailable)",
         "config": workload_dict(w, cfg, R, rec, lam, {"parallelism": (
                                     "single GPU" if world == 1 else
-                                    f"K1 set-sharded over {world} GPUs + NCCL all-gather; "
+                                    f"K1 set-sharded over {world} GPUs, rows stored to every GPU "
+                                    f"{'by the kernel over NVLink (fused all-gather)' if args.k1_transport == 'p2p' else 'by an NCCL all-gather'}; "
                                     f"repetitions sharded round-robin + pair gather"),
                                                      "recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",

@@ -75,6 +75,41 @@ CPSJ_API int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam,
                         uint32_t *d_values_out, uint64_t *d_sketch_out,
                         void *stream);
 
+/*
+ * K1 with several output destinations: the n_sets rows computed here (the
+ * CSR rows d_offsets[0 .. n_sets]) are written to rows row0 .. row0+n_sets-1
+ * of every destination.  With the destinations = the same (n, F) values and
+ * (n, F/64) sketch arrays on every GPU of the node (peer pointers from
+ * cpsj_xbuf_open), a set-sharded K1 leaves the full arrays on every GPU: the
+ * all-gather of embed_sharded is fused into the kernel's epilogue and its
+ * NVLink stores overlap the hashing.  Every destination must name the same
+ * outputs (values and/or sketches).
+ */
+#define CPSJ_MAX_DSTS 8
+typedef struct {
+    uint32_t *d_values[CPSJ_MAX_DSTS];
+    uint64_t *d_sketch[CPSJ_MAX_DSTS];
+    int32_t n_dsts;
+    int64_t row0;
+} cpsj_k1_dsts;
+
+CPSJ_API int cpsj_minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam,
+                              const uint32_t *d_tokens, const int64_t *d_offsets,
+                              int64_t n_sets, uint32_t max_token,
+                              const cpsj_k1_dsts *dsts, void *stream);
+
+/*
+ * Node-local exchange buffers (CUDA IPC).  cpsj_xbuf_create allocates
+ * `bytes` of device memory and returns its 64-byte IPC handle; another
+ * process on the node maps it with cpsj_xbuf_open (peer access over
+ * NVLink/NVSwitch enabled lazily).  cpsj_xbuf_close frees (opened == 0) or
+ * unmaps (opened != 0).
+ */
+#define CPSJ_IPC_HANDLE_BYTES 64
+CPSJ_API int cpsj_xbuf_create(cpsj_ctx *ctx, int64_t bytes, void **d_ptr, uint8_t *h_ipc_handle);
+CPSJ_API int cpsj_xbuf_open(cpsj_ctx *ctx, const uint8_t *h_ipc_handle, void **d_ptr);
+CPSJ_API int cpsj_xbuf_close(cpsj_ctx *ctx, void *d_ptr, int32_t opened);
+
 /* device inputs of a self-join: the EmbeddedDataset fields the engine reads
  * (cpsjoin.py:95-108) */
 typedef struct {

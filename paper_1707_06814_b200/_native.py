@@ -47,7 +47,15 @@ EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_err
            "cpsj_family_create", "cpsj_family_destroy", "cpsj_minhash_sketch", "cpsj_self_join",
            "cpsj_join_copy_result", "cpsj_join_result_device", "cpsj_profile_enable", "cpsj_profile_read",
            "cpsj_launch_counts", "cpsj_frequency_order", "cpsj_exact_join",
-           "cpsj_lsh_join", "cpsj_ingest_lists", "cpsj_parse_text", "cpsj_ingest_result_device", "cpsj_ingest_copy"]
+           "cpsj_lsh_join", "cpsj_ingest_lists", "cpsj_parse_text", "cpsj_ingest_result_device", "cpsj_ingest_copy",
+           "cpsj_minhash_sketch_multi", "cpsj_xbuf_create", "cpsj_xbuf_open", "cpsj_xbuf_close"]
+
+MAX_DSTS = 8
+IPC_HANDLE_BYTES = 64
+
+
+class K1Dsts(ctypes.Structure):
+    _fields_ = [("d_values", P * MAX_DSTS), ("d_sketch", P * MAX_DSTS), ("n_dsts", i32), ("row0", i64)]
 
 PROF_CLASSES = ["k1_minhash", "k4_leaf", "point", "node", "split", "k5_verify", "k6_dedup", "plan"]
 
@@ -90,6 +98,10 @@ def load(path: str | None = None):
         L.cpsj_parse_text.argtypes = [P, P, i64, i64, ctypes.POINTER(IngestStats), P]
         L.cpsj_ingest_result_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
         L.cpsj_ingest_copy.argtypes = [P, P, P, P, P]
+        L.cpsj_minhash_sketch_multi.argtypes = [P, P, P, P, i64, u32, ctypes.POINTER(K1Dsts), P]
+        L.cpsj_xbuf_create.argtypes = [P, i64, ctypes.POINTER(P), P]
+        L.cpsj_xbuf_open.argtypes = [P, P, ctypes.POINTER(P)]
+        L.cpsj_xbuf_close.argtypes = [P, P, i32]
         L.cpsj_exact_join.argtypes = [P, P, P, i64, i64, dbl, i32, ctypes.POINTER(JoinStats), P]
         _lib = L
         return L

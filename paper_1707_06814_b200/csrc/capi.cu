@@ -126,6 +126,65 @@ int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d
     });
 }
 
+int cpsj_minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,
+                              const int64_t *d_offsets, int64_t n_sets, uint32_t max_token, const cpsj_k1_dsts *dsts,
+                              void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(dsts != nullptr, "null destinations");
+        cpsj::require(n_sets == 0 || (d_tokens && d_offsets), "null CSR pointers");
+        cpsj::require(dsts->n_dsts >= 1 && dsts->n_dsts <= CPSJ_MAX_DSTS, "1 to 8 destinations");
+        cpsj::K1Out out{};
+        for (int d = 0; d < dsts->n_dsts; ++d) {
+            out.values[d] = dsts->d_values[d];
+            out.sketch[d] = dsts->d_sketch[d];
+        }
+        out.n = dsts->n_dsts;
+        out.row0 = dsts->row0;
+        cpsj::minhash_sketch_multi(ctx, fam, d_tokens, d_offsets, n_sets, max_token, out, (cudaStream_t)stream);
+    });
+}
+
+int cpsj_xbuf_create(cpsj_ctx *ctx, int64_t bytes, void **d_ptr, uint8_t *h_ipc_handle) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(d_ptr && h_ipc_handle && bytes > 0, "bad xbuf arguments");
+        static_assert(sizeof(cudaIpcMemHandle_t) == CPSJ_IPC_HANDLE_BYTES, "IPC handle size");
+        CPSJ_CUDA(cudaSetDevice(ctx->device));
+        void *p = nullptr;
+        CPSJ_CUDA(cudaMalloc(&p, (size_t)bytes));
+        cudaIpcMemHandle_t h;
+        const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            CPSJ_CUDA(e);
+        }
+        std::memcpy(h_ipc_handle, &h, sizeof(h));
+        *d_ptr = p;
+    });
+}
+
+int cpsj_xbuf_open(cpsj_ctx *ctx, const uint8_t *h_ipc_handle, void **d_ptr) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(d_ptr && h_ipc_handle, "bad xbuf arguments");
+        CPSJ_CUDA(cudaSetDevice(ctx->device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, h_ipc_handle, sizeof(h));
+        CPSJ_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int cpsj_xbuf_close(cpsj_ctx *ctx, void *d_ptr, int32_t opened) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        if (!d_ptr) return;
+        CPSJ_CUDA(cudaSetDevice(ctx->device));
+        if (opened) CPSJ_CUDA(cudaIpcCloseMemHandle(d_ptr));
+        else CPSJ_CUDA(cudaFree(d_ptr));
+    });
+}
+
 int cpsj_self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
                    void *stream) {
     if (!ctx) return CPSJ_E_ARG;

@@ -193,6 +193,20 @@ struct ProfScope {
     }
 };
 
+// K1 output rows: every computed row r of the launch goes to row row0 + r of
+// each destination (1 = the local arrays; up to 8 = the same arrays on every
+// GPU of the node through peer pointers, which fuses the all-gather of a
+// set-sharded K1 into its epilogue)
+constexpr int K1_MAX_DSTS = 8;
+struct K1Out {
+    uint32_t *values[K1_MAX_DSTS];
+    uint64_t *sketch[K1_MAX_DSTS];
+    int n;
+    int64_t row0;
+};
+
+void minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens, const int64_t *d_offsets,
+                          int64_t n, uint32_t max_token, const K1Out &out, cudaStream_t stream);
 int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,
                    const int64_t *d_offsets, int64_t n, uint32_t max_token, uint32_t *d_values,
                    uint64_t *d_sketch, cudaStream_t stream);

@@ -59,8 +59,8 @@ template <int L>
 __global__ void __launch_bounds__(K1_THREADS) k_minhash(
     const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
     const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
-    const uint32_t *__restrict__ bitmask, int F, uint32_t *__restrict__ values,
-    uint32_t *__restrict__ sketch32) {
+    const uint32_t *__restrict__ bitmask, int F, const K1Out out) {
+    const bool want_values = out.values[0] != nullptr, want_sketch = out.sketch[0] != nullptr;
     extern __shared__ uint32_t smem[];  // [L][256][32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nchunks = (F + 31) >> 5;
@@ -117,8 +117,10 @@ __global__ void __launch_bounds__(K1_THREADS) k_minhash(
                 best_tok = bt;
             }
             if (end == beg) best_tok = 0;
-            if (values != nullptr && fn < F) values[s * F + fn] = best_tok;
-            if (sketch32 != nullptr) {
+            const int64_t row = out.row0 + s;
+            if (want_values && fn < F)
+                for (int d = 0; d < out.n; ++d) out.values[d][row * F + fn] = best_tok;
+            if (want_sketch) {
                 uint32_t bit = 0;
                 if (fn < F) {
                     const uint32_t *bm = bitmask + (size_t)fn * 32;
@@ -130,10 +132,13 @@ __global__ void __launch_bounds__(K1_THREADS) k_minhash(
                     if (end == beg) bit = 0;
                 }
                 const uint32_t word = __ballot_sync(0xffffffffu, bit);
-                if (lane == 0) sketch32[s * words32 + c] = word;
+                if (lane == 0)
+                    for (int d = 0; d < out.n; ++d)
+                        reinterpret_cast<uint32_t *>(out.sketch[d])[row * words32 + c] = word;
             }
         }
     }
+    if (out.n > 1) __threadfence_system();  // peer stores visible node-wide
 }
 
 // ---------------------------------------------------------------------
@@ -330,13 +335,13 @@ template <int L>
 __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
     const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
     const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
-    const uint2 *__restrict__ img16, const uint32_t *__restrict__ bmimg, int F, uint32_t *__restrict__ values,
-    uint64_t *__restrict__ sketch) {
+    const uint2 *__restrict__ img16, const uint32_t *__restrict__ bmimg, int F, const K1Out out) {
+    const bool want_values = out.values[0] != nullptr, want_sketch = out.sketch[0] != nullptr;
     // [L][256][32] x uint2 {f0 << 16 | f32, f64 << 16 | f96} (16-bit hashes),
     // then the bit masks, then the mbarrier (no static shared memory)
     extern __shared__ __align__(128) uint2 tab2[];
     uint32_t *bm_s = reinterpret_cast<uint32_t *>(tab2 + L * 256 * 32);  // [128][33]
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(bm_s + (sketch != nullptr ? 128 * 33 : 0));
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(bm_s + (want_sketch ? 128 * 33 : 0));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lane_base = (uint32_t)__cvta_generic_to_shared(tab2) + ((uint32_t)lane << 3);
     const int nchunks = (F + 127) >> 7;
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
         if (threadIdx.x == 0) {
             // the chunk's prebuilt shared-memory image arrives by TMA bulk copy
             const uint32_t tab_bytes = (uint32_t)L * 65536u;
-            const uint32_t bm_bytes = sketch != nullptr ? (uint32_t)K16_BM_BYTES : 0u;
+            const uint32_t bm_bytes = want_sketch ? (uint32_t)K16_BM_BYTES : 0u;
             fence_proxy_async_smem();
             mbar_expect_tx(mbar_a, tab_bytes + bm_bytes);
             const char *src = reinterpret_cast<const char *>(img16) + (size_t)c * tab_bytes;
@@ -420,12 +425,17 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
                     }
                 }
             }
-            if (values != nullptr) {
+            // the row goes to every destination (peer GPUs through NVLink when
+            // K1 is set-sharded: the all-gather rides on the epilogue)
+            const int64_t row = out.row0 + s;
+            if (want_values) {
+                for (int d = 0; d < out.n; ++d) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (fn[q] < F) values[s * F + fn[q]] = tk[q];
+                    for (int q = 0; q < 4; ++q)
+                        if (fn[q] < F) out.values[d][row * F + fn[q]] = tk[q];
+                }
             }
-            if (sketch != nullptr) {
+            if (want_sketch) {
                 uint32_t w[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
@@ -434,24 +444,28 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
                     // u32 words (c*4 + lane) of the row; F % 64 == 0 so they pair into u64 words
                     const uint32_t mine_w = lane == 0 ? w[0] : lane == 1 ? w[1] : lane == 2 ? w[2] : w[3];
                     if ((c << 2) + lane < words32)
-                        reinterpret_cast<uint32_t *>(sketch)[s * words32 + (c << 2) + lane] = mine_w;
+                        for (int d = 0; d < out.n; ++d)
+                            reinterpret_cast<uint32_t *>(out.sketch[d])[row * words32 + (c << 2) + lane] = mine_w;
                 }
             }
         }
     }
+    // peer stores must be visible node-wide before the host-side ordering
+    // (the exchange's barrier) releases the readers
+    if (out.n > 1) __threadfence_system();
 }
 
 template <int L>
 static void launch_minhash_k16(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
-                               int64_t n, uint32_t *values, uint64_t *sketch, cudaStream_t stream) {
-    const int smem = L * 256 * 32 * 8 + (sketch != nullptr ? 128 * 33 * 4 : 0) + 16;  // + mbarrier
+                               int64_t n, const K1Out &out, cudaStream_t stream) {
+    const int smem = L * 256 * 32 * 8 + (out.sketch[0] != nullptr ? 128 * 33 * 4 : 0) + 16;  // + mbarrier
     CPSJ_CUDA(cudaFuncSetAttribute(k_minhash_k16<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t want = (n + K1W_WARPS - 1) / K1W_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
     ProfScope prof(ctx, PROF_K1, stream);
     k_minhash_k16<L><<<grid, K1W_THREADS, smem, stream>>>(
         tok, off, n, fam->d_hi, fam->d_lo, reinterpret_cast<const uint2 *>(fam->d_img16[L - 1]), fam->d_bmimg,
-        fam->F, values, sketch);
+        fam->F, out);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
 }
@@ -476,9 +490,8 @@ __global__ void k_prepare_family(const uint64_t *__restrict__ mh, const uint64_t
 }
 
 template <int L>
-static void launch_minhash(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok,
-                           const int64_t *off, int64_t n, uint32_t *values, uint32_t *sketch32,
-                           cudaStream_t stream) {
+static void launch_minhash(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
+                           int64_t n, const K1Out &out, cudaStream_t stream) {
     const int smem = L * 256 * 32 * 4;
     CPSJ_CUDA(cudaFuncSetAttribute(k_minhash<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
@@ -487,39 +500,54 @@ static void launch_minhash(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t
     const int64_t want = (n + K1_WARPS - 1) / K1_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count * per_sm));
     ProfScope prof(ctx, PROF_K1, stream);
-    k_minhash<L><<<grid, K1_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask,
-                                                     fam->F, values, sketch32);
+    k_minhash<L><<<grid, K1_THREADS, smem, stream>>>(tok, off, n, fam->d_hi, fam->d_lo, fam->d_bitmask, fam->F,
+                                                     out);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
+}
+
+void minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens, const int64_t *d_offsets,
+                          int64_t n, uint32_t max_token, const K1Out &out, cudaStream_t stream) {
+    require(fam != nullptr, "family is null");
+    require(n >= 0, "n_sets must be non-negative");
+    require(out.n >= 1 && out.n <= K1_MAX_DSTS, "1 to 8 output destinations");
+    require(out.row0 >= 0, "negative output row offset");
+    const bool want_values = out.values[0] != nullptr, want_sketch = out.sketch[0] != nullptr;
+    for (int d = 1; d < out.n; ++d)
+        require((out.values[d] != nullptr) == want_values && (out.sketch[d] != nullptr) == want_sketch,
+                "every destination needs the same outputs");
+    if (want_sketch) {
+        require(fam->d_bitmask != nullptr, "sketches need a family with bit tables");
+        require(fam->F % 64 == 0, "sketch family size must be a multiple of 64");
+    }
+    if (n == 0 || (!want_values && !want_sketch)) return;
+    const int L = max_token < (1u << 8) ? 1 : max_token < (1u << 16) ? 2 : max_token < (1u << 24) ? 3 : 4;
+    const char *force32 = getenv("CPSJ_K1_NARROW");  // A/B switch for the 32-function kernel
+    if (force32 != nullptr && force32[0] == '1' && L < 4) {
+        switch (L) {
+            case 1: launch_minhash<1>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+            case 2: launch_minhash<2>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+            default: launch_minhash<3>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+        }
+        return;
+    }
+    switch (L) {
+        case 1: launch_minhash_k16<1>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+        case 2: launch_minhash_k16<2>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+        case 3: launch_minhash_k16<3>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+        default: launch_minhash<4>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+    }
 }
 
 int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,
                    const int64_t *d_offsets, int64_t n, uint32_t max_token, uint32_t *d_values,
                    uint64_t *d_sketch, cudaStream_t stream) {
-    require(fam != nullptr, "family is null");
-    require(n >= 0, "n_sets must be non-negative");
-    if (d_sketch != nullptr) {
-        require(fam->d_bitmask != nullptr, "sketches need a family with bit tables");
-        require(fam->F % 64 == 0, "sketch family size must be a multiple of 64");
-    }
-    if (n == 0 || (d_values == nullptr && d_sketch == nullptr)) return 0;
-    const int L = max_token < (1u << 8) ? 1 : max_token < (1u << 16) ? 2 : max_token < (1u << 24) ? 3 : 4;
-    uint32_t *sk32 = reinterpret_cast<uint32_t *>(d_sketch);
-    const char *force32 = getenv("CPSJ_K1_NARROW");  // A/B switch for the 32-function kernel
-    if (force32 != nullptr && force32[0] == '1' && L < 4) {
-        switch (L) {
-            case 1: launch_minhash<1>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
-            case 2: launch_minhash<2>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
-            default: launch_minhash<3>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
-        }
-        return 0;
-    }
-    switch (L) {
-        case 1: launch_minhash_k16<1>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-        case 2: launch_minhash_k16<2>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-        case 3: launch_minhash_k16<3>(ctx, fam, d_tokens, d_offsets, n, d_values, d_sketch, stream); break;
-        default: launch_minhash<4>(ctx, fam, d_tokens, d_offsets, n, d_values, sk32, stream); break;
-    }
+    K1Out out{};
+    out.values[0] = d_values;
+    out.sketch[0] = d_sketch;
+    out.n = 1;
+    out.row0 = 0;
+    minhash_sketch_multi(ctx, fam, d_tokens, d_offsets, n, max_token, out, stream);
     return 0;
 }
 

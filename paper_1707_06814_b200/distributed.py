@@ -109,6 +109,132 @@ def embed_sharded(eparams, d_tok, d_off, d: int, sketch, rank: int, world: int, 
     return all_vals, all_sk
 
 
+class _DeviceArray:
+    """CUDA Array Interface view of library-owned device memory (lets
+    torch.as_tensor wrap it without a copy)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str, owner):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+        self._owner = owner
+
+
+class PeerArrays:
+    """The (n, t) values and (n, ell) sketch arrays of a node-wide K1 as
+    CUDA IPC exchange buffers: every rank allocates its own pair
+    (cpsj_xbuf_create), the 64-byte handles are all-gathered once, and every
+    rank maps every peer's pair (cpsj_xbuf_open, NVLink peer access).  K1 then
+    writes each row it computes to all ranks' buffers
+    (cpsj_minhash_sketch_multi), so the all-gather of the set-sharded
+    embedding happens inside the kernel's epilogue."""
+
+    def __init__(self, ctx, n: int, t: int, ell: int, rank: int, world: int, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from ._native import IPC_HANDLE_BYTES, P
+        if world > 8:
+            raise ValueError("peer exchange supports up to 8 ranks per node")
+        self.ctx, self.n, self.t, self.ell, self.rank, self.world = ctx, n, t, ell, rank, world
+        self._own, self._opened = [], []
+        handles = []
+        for nbytes in (max(1, n * t * 4), max(1, n * ell * 8)):
+            p = P()
+            h = (ctypes.c_uint8 * IPC_HANDLE_BYTES)()
+            ctx.check(ctx.lib.cpsj_xbuf_create(ctx.handle, nbytes, ctypes.byref(p), h))
+            self._own.append(int(p.value))
+            handles.append(bytes(h))
+        gathered = [None] * world
+        dist.all_gather_object(gathered, handles, group=group)
+        self.values_ptrs, self.sketch_ptrs = [], []
+        for r in range(world):
+            if r == rank:
+                self.values_ptrs.append(self._own[0])
+                self.sketch_ptrs.append(self._own[1])
+                continue
+            ptrs = []
+            for hb in gathered[r]:
+                p = P()
+                buf = (ctypes.c_uint8 * IPC_HANDLE_BYTES).from_buffer_copy(hb)
+                ctx.check(ctx.lib.cpsj_xbuf_open(ctx.handle, buf, ctypes.byref(p)))
+                self._opened.append(int(p.value))
+                ptrs.append(int(p.value))
+            self.values_ptrs.append(ptrs[0])
+            self.sketch_ptrs.append(ptrs[1])
+        dev = torch.device("cuda", ctx.device)
+        self.values = torch.as_tensor(_DeviceArray(self._own[0], (n, t), "<i4", self), device=dev)
+        self.sketch = torch.as_tensor(_DeviceArray(self._own[1], (n, ell), "<i8", self), device=dev)
+
+    def close(self):
+        for p in self._opened:
+            self.ctx.lib.cpsj_xbuf_close(self.ctx.handle, p, 1)
+        for p in self._own:
+            self.ctx.lib.cpsj_xbuf_close(self.ctx.handle, p, 0)
+        self._opened, self._own = [], []
+
+
+def _k1_to_peers(ctx, fam, d_tok, d_off, d: int, lo: int, hi: int, ptrs: list, is_sketch: bool):
+    import ctypes
+
+    import torch
+
+    from ._native import K1Dsts
+    n_loc = hi - lo
+    if n_loc <= 0:
+        return
+    dst = K1Dsts()
+    for i, p in enumerate(ptrs):
+        if is_sketch:
+            dst.d_sketch[i] = p
+        else:
+            dst.d_values[i] = p
+    dst.n_dsts = len(ptrs)
+    dst.row0 = lo
+    max_token = min(int(d) - 1, 0xFFFFFFFF) if d else 0xFFFFFFFF
+    stream = torch.cuda.current_stream().cuda_stream
+    ctx.check(ctx.lib.cpsj_minhash_sketch_multi(ctx.handle, fam.handle, d_tok.data_ptr(), d_off.data_ptr() + 8 * lo,
+                                                n_loc, max_token, ctypes.byref(dst), stream))
+
+
+def embed_sharded_p2p(eparams, d_tok, d_off, d: int, sketch, rank: int, world: int, peers: PeerArrays,
+                      group=None):
+    """Set-sharded embedding with the all-gather fused into K1: rank r
+    hashes sets [r n/W, (r+1) n/W) and stores each row into every rank's
+    PeerArrays over NVLink; one barrier (a 1-element all-reduce, stream
+    ordered under NCCL) publishes the rows.  Returns (values, sketches) =
+    this rank's full (n, t) / (n, ell) arrays."""
+    import torch
+    import torch.distributed as dist
+
+    from ._native import Context
+    from .hashing import sketch_family
+    ctx = Context.get()
+    n = int(d_off.shape[0]) - 1
+    lo, hi, _ = shard_range(n, rank, world)
+    nccl = world > 1 and dist.get_backend(group) == "nccl"
+    if nccl:
+        # write-after-read guard: no peer may still be reading the previous
+        # contents (stream ordered, no host synchronisation)
+        flag = torch.zeros(1, dtype=torch.int32, device=d_tok.device)
+        dist.all_reduce(flag, group=group)
+    elif world > 1:
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+    if eparams is not None:
+        _k1_to_peers(ctx, eparams.device(ctx), d_tok, d_off, d, lo, hi, peers.values_ptrs, False)
+    if sketch is not None:
+        _k1_to_peers(ctx, sketch_family(*sketch).device(ctx), d_tok, d_off, d, lo, hi, peers.sketch_ptrs, True)
+    if nccl:
+        flag = torch.zeros(1, dtype=torch.int32, device=d_tok.device)
+        dist.all_reduce(flag, group=group)        # every rank's K1 stores precede the readers
+    elif world > 1:
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+    return (peers.values if eparams is not None else None), (peers.sketch if sketch is not None else None)
+
+
 def embedded_from_parts(eparams, d_tok, d_off, d: int, values, sketches, sketch_key=None, host_csr=None):
     """EmbeddedDataset over device tensors produced by embed_sharded."""
     import torch
