@@ -110,6 +110,8 @@ int cpsj_family_destroy(cpsj_family *fam) {
     if (fam->d_bitmask) cudaFree(fam->d_bitmask);
     for (void *p : fam->d_img16)
         if (p) cudaFree(p);
+    for (void *p : fam->d_simg)
+        if (p) cudaFree(p);
     if (fam->d_bmimg) cudaFree(fam->d_bmimg);
     delete fam;
     return CPSJ_OK;

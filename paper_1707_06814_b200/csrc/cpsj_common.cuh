@@ -166,6 +166,8 @@ struct cpsj_family {
     // the 16-bit [L][256][32]{4 functions} table for key width L (index L-1)
     // and the [128][33] bit-mask block; copied to shared memory with TMA
     void *d_img16[3] = {nullptr, nullptr, nullptr};
+    // and the sketch kernel's [L][256][16]{8 functions} (h15 << 1 | bit) images
+    void *d_simg[3] = {nullptr, nullptr, nullptr};
     uint32_t *d_bmimg = nullptr;
 };
 

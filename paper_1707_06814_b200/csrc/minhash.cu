@@ -455,6 +455,359 @@ __global__ void __launch_bounds__(K1W_THREADS, 1) k_minhash_k16(
     if (out.n > 1) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------
+// Half-warp helpers: 16 lanes own one set and each lane owns EIGHT
+// functions of a 128-function chunk (f = l, l+16, ..., l+112), so one
+// LDS.128 per key byte fetches eight 16-bit entries.  The two halves of a
+// warp run two sets of (nearly) equal length: sets are visited in a
+// length-bucketed order (length_order).
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
+// XOR of the L entries of token `tok`: [k][byte][l16] rows of 256 bytes
+template <int L>
+__device__ __forceinline__ uint4 key_oct(uint32_t tok, uint32_t lane_base) {
+    uint4 h = lds128(lane_base + __byte_perm(tok, 0u, 0x4404));
+    if (L > 1) {
+        const uint4 v = lds128(lane_base + 65536u + (tok & 0xFF00u));
+        h.x ^= v.x; h.y ^= v.y; h.z ^= v.z; h.w ^= v.w;
+    }
+    if (L > 2) {
+        const uint4 v = lds128(lane_base + 131072u + __byte_perm(tok, 0u, 0x4424));
+        h.x ^= v.x; h.y ^= v.y; h.z ^= v.z; h.w ^= v.w;
+    }
+    return h;
+}
+
+constexpr int K1H_WARPS = 24;
+constexpr int K1H_THREADS = K1H_WARPS * 32;
+
+// ---------------------------------------------------------------------
+// Sketch-only kernel (the production sketch path for L <= 3).  A sketch
+// bit needs only the low bit of the bit-hash of the argmin token, not the
+// token, and both the MinHash and the bit hash are XOR tabulation over the
+// same key bytes, so each 16-bit shared-memory entry carries
+// (top 15 bits of T_k[b] << 1) | (low bit of B_k[b]): the XOR over the key
+// bytes is (h15 << 1) | bit of the token, and the minimum over a set of
+// these 16-bit keys carries the sketch bit of the h15-argmin.  Keys hold no
+// position, so two functions are tracked per 32-bit register with the
+// three-input SIMD integer min (VIMNMX3.U16x2, two tokens per instruction):
+// m1 = min key and m1x = min of the keys with the sketch bit inverted.  A
+// tie on the 15 compared hash bits only matters when the tied tokens carry
+// different bits, which is exactly m1 == m1x; those functions are
+// re-resolved on the full 64-bit hash (smaller token on a full tie,
+// hashing.py:124) and the winner's bit read from the bit-table masks, so
+// the sketch stays bit-exact (hashing.py:197-211).  Integer ALU per
+// evaluation: 0.5 (mins) + 1 (XORs) vs about 3 for the position-keyed
+// kernels; the bound becomes the shared-memory lookups.
+__global__ void k_build_simg(const uint32_t *__restrict__ hi, const uint32_t *__restrict__ bitmask, int F, int L,
+                             int64_t total, uint4 *__restrict__ img) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int64_t per_chunk = (int64_t)L * 256 * 16;
+    const int c = (int)(e / per_chunk);
+    const int r = (int)(e - (int64_t)c * per_chunk);
+    const int k = r >> 12, b = (r >> 4) & 255, ln = r & 15;
+    uint32_t v16[8];
+    for (int q = 0; q < 8; ++q) {
+        const int fn = (c << 7) + ln + 16 * q;
+        uint32_t v = 0, bit = 0;
+        if (fn < F) {
+            const size_t base = (size_t)fn * 1024;
+            v = hi[base + k * 256 + b];
+            bit = bitmask[(size_t)fn * 32 + k * 8 + (b >> 5)] >> (b & 31);
+            if (k == L - 1)
+                for (int kk = L; kk < 4; ++kk) {
+                    v ^= hi[base + kk * 256];
+                    bit ^= bitmask[(size_t)fn * 32 + kk * 8];
+                }
+        }
+        v16[q] = ((v >> 17) << 1) | (bit & 1u);
+    }
+    img[e] = make_uint4((v16[0] << 16) | v16[1], (v16[2] << 16) | v16[3], (v16[4] << 16) | v16[5],
+                        (v16[6] << 16) | v16[7]);
+}
+
+__device__ __forceinline__ uint32_t vmin16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t vmax16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+// low bit of function f's bit-hash of `tok` from the global bit masks
+__device__ __forceinline__ uint32_t sketch_bit_g(const uint32_t *__restrict__ bitmask, int f, uint32_t tok) {
+    const uint32_t *bm = bitmask + (size_t)f * 32;
+    const uint32_t b0 = tok & 255, b1 = (tok >> 8) & 255, b2 = (tok >> 16) & 255, b3 = tok >> 24;
+    return ((__ldg(bm + (b0 >> 5)) >> (b0 & 31)) ^ (__ldg(bm + 8 + (b1 >> 5)) >> (b1 & 31)) ^
+            (__ldg(bm + 16 + (b2 >> 5)) >> (b2 & 31)) ^ (__ldg(bm + 24 + (b3 >> 5)) >> (b3 & 31))) & 1u;
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// exact argmin token of function f over a set whose minimal top-15 hash bits
+// are m15, 16 lanes of the half cooperating (lanes over tokens).  Candidates
+// are found on the shared-memory 16-bit entries of f (column `col` = its
+// word in the [k][byte][l16] rows, `sh` = 16 for the high half); only they
+// evaluate the full 64-bit hash from the global tables (the smaller token
+// wins a full tie, hashing.py:124).  Every lane of the half returns the winner.
+template <int L>
+__device__ __noinline__ uint32_t half_resolve15(const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+                                                int f, uint32_t m15, uint32_t col, int sh,
+                                                const uint32_t *__restrict__ tokens, int64_t beg, int len, int l,
+                                                unsigned hmask) {
+    uint64_t bg = ~0ull;
+    uint32_t bt = 0xFFFFFFFFu;
+    const size_t base = (size_t)f * 1024;
+    for (int i = l; i < len; i += 16) {
+        const uint32_t tk = __ldg(tokens + beg + i);
+        uint32_t e = lds32(col + __byte_perm(tk, 0u, 0x4404));
+        if (L > 1) e ^= lds32(col + 65536u + (tk & 0xFF00u));
+        if (L > 2) e ^= lds32(col + 131072u + __byte_perm(tk, 0u, 0x4424));
+        if (((e >> (sh + 1)) & 0x7FFFu) == m15) {
+            const uint32_t b0 = tk & 255, b1 = (tk >> 8) & 255, b2 = (tk >> 16) & 255, b3 = tk >> 24;
+            const uint32_t h = __ldg(hi + base + b0) ^ __ldg(hi + base + 256 + b1) ^ __ldg(hi + base + 512 + b2) ^
+                               __ldg(hi + base + 768 + b3);
+            const uint32_t lw = __ldg(lo + base + b0) ^ __ldg(lo + base + 256 + b1) ^ __ldg(lo + base + 512 + b2) ^
+                                __ldg(lo + base + 768 + b3);
+            const uint64_t g = ((uint64_t)h << 32) | lw;
+            if (g < bg || (g == bg && tk < bt)) {
+                bg = g;
+                bt = tk;
+            }
+        }
+    }
+    for (int o = 8; o > 0; o >>= 1) {
+        const uint64_t og = __shfl_xor_sync(hmask, bg, o);
+        const uint32_t ot = __shfl_xor_sync(hmask, bt, o);
+        if (og < bg || (og == bg && ot < bt)) {
+            bg = og;
+            bt = ot;
+        }
+    }
+    return bt;
+}
+
+template <int L>
+__global__ void __launch_bounds__(K1H_THREADS, 1) k_sketch_s16(
+    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
+    const int32_t *__restrict__ order, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+    const uint32_t *__restrict__ bitmask, const uint4 *__restrict__ simg, int F, const K1Out out) {
+    extern __shared__ __align__(128) uint4 tab4[];  // [L][256][16] x uint4, then the mbarrier
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + L * 256 * 16);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int h = lane >> 4, l = lane & 15;
+    const unsigned hmask = 0xFFFFu << (16 * h);
+    const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tab4);
+    const uint32_t lane_base = smem0 + ((uint32_t)l << 4);
+    const int nchunks = (F + 127) >> 7;
+    const int words32 = F >> 5;
+    const int64_t npairs = (n + 1) >> 1;
+    const int64_t p_first = (int64_t)blockIdx.x * K1H_WARPS + warp, p_step = (int64_t)gridDim.x * K1H_WARPS;
+    const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(mbar);
+    if (threadIdx.x == 0) mbar_init(mbar_a, 1);
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        __syncthreads();  // every warp is done with the previous chunk's tables
+        if (threadIdx.x == 0) {
+            const uint32_t tab_bytes = (uint32_t)L * 65536u;
+            fence_proxy_async_smem();
+            mbar_expect_tx(mbar_a, tab_bytes);
+            const char *src = reinterpret_cast<const char *>(simg) + (size_t)c * tab_bytes;
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(tab4);
+            for (uint32_t o = 0; o < tab_bytes; o += 32768u) bulk_g2s(dst + o, src + o, 32768u, mbar_a);
+        }
+        mbar_wait(mbar_a, phase);
+        phase ^= 1u;
+        for (int64_t pr = p_first; pr < npairs; pr += p_step) {
+            const int64_t idx = 2 * pr + h;
+            const bool has = idx < n;
+            int64_t s = 0, beg = 0, end = 0;
+            if (has) {
+                s = order != nullptr ? (int64_t)order[idx] : idx;
+                beg = offsets[s];
+                end = offsets[s + 1];
+            }
+            const int64_t len64 = end - beg;
+            const int len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
+            // m1[r]: min of the (h15 << 1 | bit) keys of functions
+            // (l + 32r, l + 32r + 16) in the high / low halves; m1x[r]: min of
+            // the keys with the bit inverted.  Among the tokens of minimal
+            // h15, both bits occur iff m1 == m1x (both are (h15min, 0));
+            // otherwise they all carry m1's bit and any tie on h15 is harmless.
+            uint32_t m1[4], m1x[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) m1[r] = m1x[r] = 0xFFFFFFFFu;
+            for (int base = 0; base < len; base += 16) {
+                const int cnt = len - base < 16 ? len - base : 16;
+                const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
+                int j = 0;
+#pragma unroll 2
+                for (; j + 1 < cnt; j += 2) {
+                    const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                    const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
+                    const uint4 ha = key_oct<L>(ta, lane_base);
+                    const uint4 hb = key_oct<L>(tb, lane_base);
+                    const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w}, xb[4] = {hb.x, hb.y, hb.z, hb.w};
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        m1[r] = __vimin3_u16x2(m1[r], xa[r], xb[r]);
+                        m1x[r] = __vimin3_u16x2(m1x[r], xa[r] ^ 0x00010001u, xb[r] ^ 0x00010001u);
+                    }
+                }
+                if (j < cnt) {
+                    const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                    const uint4 ha = key_oct<L>(ta, lane_base);
+                    const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w};
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        m1[r] = vmin16x2(m1[r], xa[r]);
+                        m1x[r] = vmin16x2(m1x[r], xa[r] ^ 0x00010001u);
+                    }
+                }
+            }
+            // bits: q = 2j (high half) and 2j+1 (low half) of register j
+            uint32_t bits = 0;  // bit q = sketch bit of function l + 16q
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t a1 = m1[j] >> 16, ax = m1x[j] >> 16, b1 = m1[j] & 0xFFFFu, bx = m1x[j] & 0xFFFFu;
+                bits |= (a1 & 1u) << (2 * j);
+                bits |= (b1 & 1u) << (2 * j + 1);
+                const int fa = (c << 7) + l + 32 * j, fb = fa + 16;
+                const bool tie_a = len > 1 && fa < F && a1 == ax;
+                const bool tie_b = len > 1 && fb < F && b1 == bx;
+                unsigned tied = __ballot_sync(hmask, tie_a);
+                while (tied) {
+                    const int src = __ffs(tied) - 1;
+                    tied &= tied - 1;
+                    const int f = __shfl_sync(hmask, fa, src);
+                    const uint32_t m15 = __shfl_sync(hmask, a1 >> 1, src);
+                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
+                    const uint32_t tw = half_resolve15<L>(hi, lo, f, m15, col, 16, tokens, beg, len, l, hmask);
+                    if (lane == src) bits = (bits & ~(1u << (2 * j))) | (sketch_bit_g(bitmask, f, tw) << (2 * j));
+                }
+                tied = __ballot_sync(hmask, tie_b);
+                while (tied) {
+                    const int src = __ffs(tied) - 1;
+                    tied &= tied - 1;
+                    const int f = __shfl_sync(hmask, fb, src);
+                    const uint32_t m15 = __shfl_sync(hmask, b1 >> 1, src);
+                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
+                    const uint32_t tw = half_resolve15<L>(hi, lo, f, m15, col, 0, tokens, beg, len, l, hmask);
+                    if (lane == src)
+                        bits = (bits & ~(1u << (2 * j + 1))) | (sketch_bit_g(bitmask, f, tw) << (2 * j + 1));
+                }
+            }
+            if (len <= 0) bits = 0;
+            __syncwarp();
+            uint32_t bq[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) bq[q] = __ballot_sync(0xffffffffu, (bits >> q) & 1u);
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                w[k] = h == 0 ? (bq[2 * k] & 0xFFFFu) | (bq[2 * k + 1] << 16)
+                              : (bq[2 * k] >> 16) | (bq[2 * k + 1] & 0xFFFF0000u);
+            const int64_t row = out.row0 + s;
+            if (has && l < 4 && (c << 2) + l < words32) {
+                const uint32_t mine_w = l == 0 ? w[0] : l == 1 ? w[1] : l == 2 ? w[2] : w[3];
+                for (int d = 0; d < out.n; ++d)
+                    reinterpret_cast<uint32_t *>(out.sketch[d])[row * words32 + (c << 2) + l] = mine_w;
+            }
+        }
+    }
+    if (out.n > 1) __threadfence_system();
+}
+
+// length-bucketed visiting order of the half-warp kernels: a counting sort
+// of the sets by min(|x|, 1023), longest first (the last, partial round of
+// the grid-stride loop gets the shortest sets); the order within a bucket
+// does not matter because every set's row is independent
+constexpr int K1_LEN_BINS = 1024;
+__device__ __forceinline__ int len_bin(int64_t len) {
+    return (K1_LEN_BINS - 1) - (int)(len < K1_LEN_BINS - 1 ? len : K1_LEN_BINS - 1);
+}
+
+__global__ void k_len_hist(const int64_t *__restrict__ offsets, int64_t n, int32_t *__restrict__ hist) {
+    __shared__ int32_t sh[K1_LEN_BINS];
+    for (int i = threadIdx.x; i < K1_LEN_BINS; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&sh[len_bin(offsets[s + 1] - offsets[s])], 1);
+    __syncthreads();
+    for (int i = threadIdx.x; i < K1_LEN_BINS; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void k_len_scan(int32_t *__restrict__ hist) {  // one block of K1_LEN_BINS threads
+    __shared__ int32_t sh[K1_LEN_BINS];
+    const int i = threadIdx.x;
+    sh[i] = hist[i];
+    __syncthreads();
+    for (int o = 1; o < K1_LEN_BINS; o <<= 1) {
+        const int32_t v = i >= o ? sh[i - o] : 0;
+        __syncthreads();
+        sh[i] += v;
+        __syncthreads();
+    }
+    hist[i] = sh[i] - hist[i];  // exclusive
+}
+
+__global__ void k_len_scatter(const int64_t *__restrict__ offsets, int64_t n, int32_t *__restrict__ cursor,
+                              int32_t *__restrict__ order) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    order[atomicAdd(&cursor[len_bin(offsets[s + 1] - offsets[s])], 1)] = (int32_t)s;
+}
+
+static DevBuf<int32_t> length_order(cpsj_ctx *ctx, const int64_t *off, int64_t n, cudaStream_t stream) {
+    DevBuf<int32_t> order;
+    const char *noord = getenv("CPSJ_K1_NO_ORDER");  // A/B switch: CSR order pairing
+    if (n >= 2 * K1H_WARPS && n < (int64_t)INT32_MAX && !(noord && noord[0] == '1')) {
+        DevBuf<int32_t> hist(K1_LEN_BINS, stream);
+        order.alloc(n, stream);
+        CPSJ_CUDA(cudaMemsetAsync(hist.p, 0, K1_LEN_BINS * sizeof(int32_t), stream));
+        const int hb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sm_count * 4);
+        k_len_hist<<<hb, 256, 0, stream>>>(off, n, hist.p);
+        CPSJ_LAUNCH_CHECK();
+        k_len_scan<<<1, K1_LEN_BINS, 0, stream>>>(hist.p);
+        CPSJ_LAUNCH_CHECK();
+        k_len_scatter<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(off, n, hist.p, order.p);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches += 3;
+    }
+    return order;
+}
+
+template <int L>
+static void launch_sketch_s16(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
+                              int64_t n, const K1Out &out, cudaStream_t stream) {
+    const int smem = L * 256 * 16 * 16 + 16;
+    CPSJ_CUDA(cudaFuncSetAttribute(k_sketch_s16<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ProfScope prof(ctx, PROF_K1, stream);
+    DevBuf<int32_t> order = length_order(ctx, off, n, stream);
+    const int64_t want = ((n + 1) / 2 + K1H_WARPS - 1) / K1H_WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
+    k_sketch_s16<L><<<grid, K1H_THREADS, smem, stream>>>(tok, off, n, order.p, fam->d_hi, fam->d_lo,
+                                                         fam->d_bitmask,
+                                                         reinterpret_cast<const uint4 *>(fam->d_simg[L - 1]), fam->F,
+                                                         out);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
 template <int L>
 static void launch_minhash_k16(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
                                int64_t n, const K1Out &out, cudaStream_t stream) {
@@ -531,6 +884,15 @@ void minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t 
         }
         return;
     }
+    const char *s16 = getenv("CPSJ_K1_NO_S16");  // A/B switch: sketches by the position-keyed kernels
+    if (want_sketch && !want_values && L < 4 && fam->d_simg[L - 1] != nullptr && !(s16 && s16[0] == '1')) {
+        switch (L) {
+            case 1: launch_sketch_s16<1>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+            case 2: launch_sketch_s16<2>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+            default: launch_sketch_s16<3>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+        }
+        return;
+    }
     switch (L) {
         case 1: launch_minhash_k16<1>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
         case 2: launch_minhash_k16<2>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
@@ -577,6 +939,16 @@ void prepare_family(cpsj_ctx *ctx, cpsj_family *fam, const uint64_t *h_mh, const
             fam->d_hi, fam->F, L, elems, reinterpret_cast<uint2 *>(fam->d_img16[L - 1]));
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
+    }
+    if (fam->d_bitmask != nullptr) {
+        for (int L = 1; L <= 3; ++L) {
+            const int64_t elems8 = (int64_t)nchunks * L * 256 * 16;
+            CPSJ_CUDA(cudaMalloc(&fam->d_simg[L - 1], elems8 * sizeof(uint4)));
+            k_build_simg<<<(unsigned)((elems8 + 255) / 256), 256, 0, stream>>>(
+                fam->d_hi, fam->d_bitmask, fam->F, L, elems8, reinterpret_cast<uint4 *>(fam->d_simg[L - 1]));
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+        }
     }
     if (fam->d_bitmask != nullptr) {
         const int64_t elems = (int64_t)nchunks * 128 * 33;

@@ -93,6 +93,49 @@ def test_minhash_high_word_ties_resolved_on_full_hash():
     assert np.array_equal(got, O.minhash(tok, off, tables))
 
 
+def _sketch_gpu(mh, bt, tok, off, max_token):
+    import torch
+
+    from paper_1707_06814_b200._native import Context, Family
+    ctx = Context.get()
+    fam = Family(ctx, mh, bt)
+    n = len(off) - 1
+    dev = torch.device("cuda", ctx.device)
+    t = torch.from_numpy(np.ascontiguousarray(tok, dtype=np.uint32).view(np.int32)).to(dev)
+    o = torch.from_numpy(np.ascontiguousarray(off, dtype=np.int64)).to(dev)
+    out = torch.full((n, mh.shape[0] // 64), -1, dtype=torch.int64, device=dev)
+    ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, fam.handle, t.data_ptr(), o.data_ptr(), n, max_token, None,
+                                          out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    return out.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 4])
+@pytest.mark.parametrize("n_sets", [5, 3000])
+def test_sketch_15bit_ties_and_bit_disagreement(L, n_sets):
+    # the sketch kernel compares (top 15 hash bits, sketch bit) keys; tables
+    # with few distinct top-15 values force ties on the compared bits whose
+    # tied tokens carry different sketch bits, plus full high-word ties and
+    # full 64-bit ties (smallest token), empty and single-token sets
+    from oracle import oracle as O
+    rng = np.random.default_rng(100 + L)
+    hi = (1 << (8 * L)) - 1
+    lens = rng.integers(0, 400, size=n_sets)
+    lens[:3] = [0, 1, 2]
+    rows = [np.unique(rng.integers(0, hi + 1, size=int(k), dtype=np.uint64)) for k in lens]
+    tok = np.concatenate(rows).astype(np.uint32)
+    off = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    g = O.derive_rng(11, L)
+    mh = g.integers(0, 2 ** 64, size=(128, 4, 256), dtype=np.uint64)
+    bt = g.integers(0, 2 ** 64, size=(128, 4, 256), dtype=np.uint64)
+    mask17 = np.uint64((1 << 49) - 1)  # keep the low 49 bits: top 15 bits come from `few`
+    few = g.integers(0, 3, size=(40, 4, 256), dtype=np.uint64) << np.uint64(49)
+    mh[:40] = (mh[:40] & mask17) | few
+    mh[40:60] &= np.uint64(0xFFFFFFFF)  # high word 0: every token ties on the high word
+    mh[60:70] = 0  # full ties: the smallest token wins
+    got = _sketch_gpu(mh, bt, tok, off, hi)
+    assert np.array_equal(got, O.sketch(tok, off, mh, bt))
+
+
 EMB_FIXTURES = ["planted_small", "planted_880", "dense_cluster", "c1_sample", "c3_sample", "c4_sample",
                 "ct_planted", "ct_dense", "ct_c1_sample"]
 
