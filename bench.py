@@ -232,6 +232,19 @@ def measured_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
 
 
+def int_peak(op_prefix: str, default: float):
+    """Integer-pipe rate (per clk per SM) measured on the B200 by
+    tools/int_peaks.cu (profiles/int_peaks_r01.json), else the default."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "int_peaks_r01.json")) as f:
+            for r in json.load(f)["results"]:
+                if r["op"].startswith(op_prefix):
+                    return float(r["ops_per_clk_per_sm"]), "measured, profiles/int_peaks_r01.json"
+    except (OSError, KeyError, ValueError):
+        pass
+    return default, "assumed, SURVEY.md 8(d)"
+
+
 def ncu_traffic(cfg: int, launch: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
     dominant kernel from the committed ncu --set full capture, if it was
@@ -567,7 +580,8 @@ def run_ours(args, rank: int, world: int):
     k4_ms = prof["k4_leaf"][0] + prof["point"][0]
     pre = res.counters.pre_candidates
     pairs_per_s = pre / (k4_ms / 1e3) if k4_ms > 0 else None
-    popc_peak = 148 * 16 * f_clk / (2 * cfg.ell)  # POPC 16/clk/SM assumed, 2 per u64 word
+    popc_rate, popc_basis = int_peak("POPC", 16.0)
+    popc_peak = 148 * popc_rate * f_clk / (2 * cfg.ell)  # 2 POPC per u64 word
     h2d = int(w.tokens.nbytes + w.offsets.nbytes)
     d2h = int(len(res_e2e.a) * 16)
     cpu = None
@@ -598,7 +612,7 @@ def run_ours(args, rank: int, world: int):
                                                      "recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
                      "frac": achieved / float(peaks["hbm_gbs"]), "traffic": ncu_traffic(args.config, "sketch"),
-                     "kernel": "k_minhash<L> sketch launch (K1, 64*ell functions)",
+                     "kernel": "k_sketch_s16<L> sketch launch (K1, 64*ell functions)",
                      "algorithmic_bytes": sk_bytes, "avg_launch_ms": k1_sk_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
         "roofline_smem": {"bound": "shared-memory lookups (16-bit entries, 126 B/clk/SM measured LDS rate)",
@@ -608,7 +622,7 @@ def run_ours(args, rank: int, world: int):
         "roofline_int": {"kernel": "k_leaf_tiles + k_point (K4 BruteForce)", "pairs_per_s": pairs_per_s,
                          "peak_pairs_per_s": popc_peak,
                          "frac": (pairs_per_s / popc_peak) if pairs_per_s else None,
-                         "peak_basis": "POPC 16/clk/SM x 148 x sm_max_mhz / (2 ell) (assumed, SURVEY.md 8(d))"},
+                         "peak_basis": f"POPC {popc_rate:.2f}/clk/SM ({popc_basis}) x 148 x sm_max_mhz / (2 ell)"},
         "kernels_ms_per_step": {k: v[0] for k, v in prof.items()},
         "kernels_note": "device time per class from one extra profiled step (events around each class)",
         "join_counters": {"pre_candidates": pre, "candidates": res.counters.candidates,

@@ -765,11 +765,30 @@ __global__ void k_len_scan(int32_t *__restrict__ hist) {  // one block of K1_LEN
     hist[i] = sh[i] - hist[i];  // exclusive
 }
 
-__global__ void k_len_scatter(const int64_t *__restrict__ offsets, int64_t n, int32_t *__restrict__ cursor,
-                              int32_t *__restrict__ order) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    order[atomicAdd(&cursor[len_bin(offsets[s + 1] - offsets[s])], 1)] = (int32_t)s;
+// block-aggregated scatter: shared-memory ranks within the block, one
+// global atomic per (block, bin) -- sets of equal length all hit one bin,
+// so per-set global atomics would serialise
+constexpr int K1_LEN_PER_BLOCK = 4096;
+__global__ void __launch_bounds__(1024) k_len_scatter(const int64_t *__restrict__ offsets, int64_t n,
+                                                      int32_t *__restrict__ cursor, int32_t *__restrict__ order) {
+    __shared__ int32_t cnt[K1_LEN_BINS], base[K1_LEN_BINS];
+    for (int i = threadIdx.x; i < K1_LEN_BINS; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int64_t s0 = (int64_t)blockIdx.x * K1_LEN_PER_BLOCK;
+    int bin[K1_LEN_PER_BLOCK / 1024], rank[K1_LEN_PER_BLOCK / 1024];
+#pragma unroll
+    for (int k = 0; k < K1_LEN_PER_BLOCK / 1024; ++k) {
+        const int64_t s = s0 + k * 1024 + threadIdx.x;
+        bin[k] = s < n ? len_bin(offsets[s + 1] - offsets[s]) : -1;
+        rank[k] = bin[k] >= 0 ? atomicAdd(&cnt[bin[k]], 1) : 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < K1_LEN_BINS; i += blockDim.x)
+        if (cnt[i]) base[i] = atomicAdd(&cursor[i], cnt[i]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K1_LEN_PER_BLOCK / 1024; ++k)
+        if (bin[k] >= 0) order[base[bin[k]] + rank[k]] = (int32_t)(s0 + k * 1024 + threadIdx.x);
 }
 
 static DevBuf<int32_t> length_order(cpsj_ctx *ctx, const int64_t *off, int64_t n, cudaStream_t stream) {
@@ -784,7 +803,8 @@ static DevBuf<int32_t> length_order(cpsj_ctx *ctx, const int64_t *off, int64_t n
         CPSJ_LAUNCH_CHECK();
         k_len_scan<<<1, K1_LEN_BINS, 0, stream>>>(hist.p);
         CPSJ_LAUNCH_CHECK();
-        k_len_scatter<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(off, n, hist.p, order.p);
+        k_len_scatter<<<(unsigned)((n + K1_LEN_PER_BLOCK - 1) / K1_LEN_PER_BLOCK), 1024, 0, stream>>>(off, n, hist.p,
+                                                                                                      order.p);
         CPSJ_LAUNCH_CHECK();
         ctx->launches += 3;
     }
