@@ -333,7 +333,7 @@ def embed_dataset(params: EmbeddingParams, ds: Dataset, sketch: tuple[int, int] 
     """
     n = len(ds)
     if n > 0 and ((chunks is None and n >= _PIPELINE_MIN_SETS) or (chunks is not None and chunks > 1)):
-        return _embed_pipelined(params, ds, sketch, min(chunks or 5, n))
+        return _embed_pipelined(params, ds, sketch, None if chunks is None else min(chunks, n))
     t = params.t
     tok, off = ds.flat_tokens()
     tok = np.ascontiguousarray(tok, dtype=np.uint32)
@@ -384,27 +384,34 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
     d_tok = torch.empty(len(tok), dtype=torch.int32, device=dev)
     d_vals = torch.empty((n, t), dtype=torch.int32, device=dev)
     d_sk = torch.empty((n, sketch[0]), dtype=torch.int64, device=dev) if sketch is not None else None
-    # set-aligned chunk boundaries
-    # geometric chunks (1/2^(c-1), ..., 1/4, 1/2 of the sets): the first copy,
-    # which nothing can hide, is small; later copies hide behind compute
-    frac = np.array([0.0] + [2.0 ** -(chunks - 1)] + [2.0 ** -(chunks - k) for k in range(1, chunks)])
-    bounds = np.minimum(np.round(np.cumsum(frac) * n), n).astype(np.int64)
-    bounds[-1] = n
+    bounds = _chunk_bounds(n, chunks)
+    chunks = len(bounds) - 1
+    d_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
     events = []
     copier.wait_stream(compute)  # destination buffers were allocated on `compute`
     with torch.cuda.stream(copier):
-        d_off = src_off.to(dev, non_blocking=True)
         for c in range(chunks):
-            t0, t1 = int(off[bounds[c]]), int(off[bounds[c + 1]])
+            s0, s1 = int(bounds[c]), int(bounds[c + 1])
+            t0, t1 = int(off[s0]), int(off[s1])
+            d_off[s0 + (c > 0):s1 + 1].copy_(src_off[s0 + (c > 0):s1 + 1], non_blocking=True)
             if t1 > t0:
                 d_tok[t0:t1].copy_(src_tok[t0:t1], non_blocking=True)
-            ev = torch.cuda.Event()
+            ev = torch.cuda.Event(enable_timing=_PIPE_TRACE is not None)
             ev.record(copier)
             events.append(ev)
     h = compute.cuda_stream
+    trace = _PIPE_TRACE if _PIPE_TRACE is not None and len(_PIPE_TRACE) == 0 else None
+    if trace is not None:
+        trace.append(("copies", events))
+        kev = []
+        trace.append(("k1", kev))
     for c in range(chunks):
         s0, s1 = int(bounds[c]), int(bounds[c + 1])
         compute.wait_event(events[c])
+        if trace is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(compute)
+            kev.append(e)
         if s1 <= s0:
             continue
         offp = d_off.data_ptr() + 8 * s0
@@ -415,7 +422,7 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
                                                   max_token, None, d_sk.data_ptr() + 8 * sketch[0] * s0, h))
     # the copier's work is consumed on `compute`; keep the buffers alive there
     d_tok.record_stream(copier)
-    d_off.record_stream(compute)
+    d_off.record_stream(copier)
     emb = EmbeddedDataset._device_backed(d_vals, t, params.seed, tok, off, width, ds, (d_tok, d_off))
     emb._dev["sizes"] = (d_off[1:] - d_off[:-1]).to(torch.int32)
     if sketch is not None:
@@ -423,7 +430,37 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
     return emb
 
 
+# Chunk schedule of the pipelined embed: the first copy is exposed, so it is
+# small; every later chunk must arrive while K1 hashes the previous one.  The
+# H2D rate (pinned, ~44 GB/s of CSR on the B200 box) against K1 (values +
+# sketch, ~30 GB/s of CSR on config 2) allows a growth factor of about 1.5,
+# and every chunk costs ~0.15 ms of K1 launch overhead (table loads, tails),
+# so the schedule trades the exposed first copy against the chunk count
+# (simulated optimum on config 2: 1/32 growing by 1.6, 7 chunks).
+_FIRST_CHUNK = 1.0 / 32
+_CHUNK_GROWTH = 1.6
+
+
+def _chunk_bounds(n: int, chunks: int | None) -> np.ndarray:
+    """Set-aligned chunk boundaries: an explicit count uses doubling chunks
+    (1/2^(c-1), ..., 1/4, 1/2); None uses the growth schedule above."""
+    if chunks is not None:
+        frac = np.array([0.0] + [2.0 ** -(chunks - 1)] + [2.0 ** -(chunks - k) for k in range(1, chunks)])
+    else:
+        f, acc, fr = _FIRST_CHUNK, 0.0, [0.0]
+        while acc + f < 1.0 - 1e-9:
+            fr.append(f)
+            acc += f
+            f *= _CHUNK_GROWTH
+        fr.append(1.0 - acc)
+        frac = np.array(fr)
+    bounds = np.minimum(np.round(np.cumsum(frac) * n), n).astype(np.int64)
+    bounds[-1] = n
+    return bounds
+
+
 _COPY_STREAMS: dict = {}
+_PIPE_TRACE = None  # diagnostics (tools/embed_probe.py): an empty list collects one call's events
 
 
 def _copy_stream(dev):
