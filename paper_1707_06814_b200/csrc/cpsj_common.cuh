@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -54,6 +55,12 @@ struct DevBuf {
         s = stream;
         n = count;
         if (count) CPSJ_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), stream));
+    }
+    // capacity for at least `count` elements; the allocation is reused when
+    // it is large enough (per-level scratch that lives across levels)
+    void ensure(size_t count, cudaStream_t stream) {
+        if (p != nullptr && count <= n) return;
+        alloc(std::max<size_t>(count + count / 4, 1), stream);
     }
     // grow to at least `count` elements, keeping the first `keep` elements
     void grow(size_t count, size_t keep, cudaStream_t stream) {

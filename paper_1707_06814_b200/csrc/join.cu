@@ -31,6 +31,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
+#include <type_traits>
 #include <memory>
 
 #include "cpsj_common.cuh"
@@ -88,9 +90,17 @@ __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit
 }
 
 __global__ void k_compact_internal(int64_t N, const int64_t *__restrict__ internal,
-                                   const int64_t *__restrict__ iscan, int64_t *__restrict__ ilist) {
+                                   const int64_t *__restrict__ iscan, int64_t *__restrict__ ilist,
+                                   const int64_t *__restrict__ im_off = nullptr, int64_t *__restrict__ im_off_c = nullptr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < N && internal[i]) ilist[iscan[i]] = i;
+    if (i < N && internal[i]) {
+        ilist[iscan[i]] = i;
+        // internal members are contiguous in node order: node k's member
+        // offset among internal nodes is the scan of imem at its index
+        if (im_off_c != nullptr) im_off_c[iscan[i]] = im_off[i];
+    } else if (i == N && im_off_c != nullptr) {
+        im_off_c[iscan[N]] = im_off[N];
+    }
 }
 
 // ------------------------------------------------------ K4 leaf BruteForce
@@ -573,13 +583,6 @@ __global__ void k_verify(int64_t nc, const int2 *__restrict__ cand, const uint32
     }
 }
 
-__global__ void k_gather_counts(int64_t ni, const int64_t *__restrict__ il, const int32_t *__restrict__ cnt,
-                                int64_t *__restrict__ out) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < ni) out[k] = cnt[il[k]];
-    else if (k == ni) out[k] = 0;
-}
-
 __global__ void k_fill_roots(int64_t n, int32_t R, int32_t *__restrict__ members) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < n * R) members[e] = (int32_t)(e % n);
@@ -605,10 +608,147 @@ struct Level {
     DevBuf<int32_t> members;
 };
 
+// Exclusive scans of up to four int64 arrays of the same length n with one
+// set of launches: tiles of 4096 elements (1024 threads x 4 consecutive
+// elements, coalesced); <= 1 tile: one launch; more: tile sums, one CTA
+// scans them, then every tile scans itself from its prefix (3 launches for
+// all K arrays, where CUB takes 2 per array).
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_TILE = SCAN_THREADS * 4;
+struct ScanSet {
+    const int64_t *in[4];
+    int64_t *out[4];
+    int64_t *part;  // [K][tiles] tile sums, then their exclusive scan
+};
+
+template <int K>
+__device__ __forceinline__ void scan_load(const ScanSet &a, int64_t n, int64_t base, int64_t (&v)[K][4]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = base + j;
+            v[k][j] = i < n ? a.in[k][i] : 0;
+        }
+}
+
+// block-wide exclusive scan of one value per thread; returns the prefix and
+// the block total
+__device__ __forceinline__ int64_t scan_block(int64_t x, int64_t *wsum, int64_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t v = wsum[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        wsum[lane] = v;
+    }
+    __syncthreads();
+    const int64_t r = (wid > 0 ? wsum[wid - 1] : 0) + incl - x;
+    total = wsum[31];
+    __syncthreads();
+    return r;
+}
+
+template <int K>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(ScanSet a, int64_t n, int64_t tiles) {
+    __shared__ int64_t wsum[32];
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * 4;
+    int64_t v[K][4];
+    scan_load<K>(a, n, base, v);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        int64_t total;
+        scan_block(v[k][0] + v[k][1] + v[k][2] + v[k][3], wsum, total);
+        if (threadIdx.x == 0) a.part[k * tiles + blockIdx.x] = total;
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(ScanSet a, int64_t tiles) {
+    __shared__ int64_t wsum[32];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        int64_t carry = 0;
+        for (int64_t b0 = 0; b0 < tiles; b0 += SCAN_THREADS) {
+            const int64_t i = b0 + threadIdx.x;
+            const int64_t x = i < tiles ? a.part[k * tiles + i] : 0;
+            int64_t total;
+            const int64_t r = scan_block(x, wsum, total);
+            if (i < tiles) a.part[k * tiles + i] = carry + r;
+            carry += total;
+        }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(ScanSet a, int64_t n, int64_t tiles) {
+    __shared__ int64_t wsum[32];
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * 4;
+    int64_t v[K][4];
+    scan_load<K>(a, n, base, v);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        int64_t total;
+        int64_t run = scan_block(v[k][0] + v[k][1] + v[k][2] + v[k][3], wsum, total);
+        if (tiles > 1) run += a.part[k * tiles + blockIdx.x];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (base + j < n) a.out[k][base + j] = run;
+            run += v[k][j];
+        }
+    }
+}
+
 struct Driver {
     cpsj_ctx *ctx;
     cudaStream_t st;
     DevBuf<uint8_t> cub_tmp;
+
+    DevBuf<int64_t> scan_part;
+
+    // exclusive scans of k <= 4 arrays of length n (see k_scan_apply)
+    void scan_multi(std::initializer_list<const int64_t *> ins, std::initializer_list<int64_t *> outs, int64_t n) {
+        ScanSet a{};
+        int k = 0;
+        for (const int64_t *p : ins) a.in[k++] = p;
+        k = 0;
+        for (int64_t *p : outs) a.out[k++] = p;
+        const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+        if (k == 1 && tiles > 1) {  // CUB's two launches beat three
+            scan(a.in[0], a.out[0], n);
+            return;
+        }
+        if (tiles > 1) {
+            scan_part.ensure((size_t)4 * tiles, st);
+            a.part = scan_part.p;
+        }
+        auto run = [&](auto kk) {
+            constexpr int KK = decltype(kk)::value;
+            if (tiles > 1) {
+                k_scan_reduce<KK><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(a, n, tiles);
+                k_scan_partials<KK><<<1, SCAN_THREADS, 0, st>>>(a, tiles);
+                ctx->launches += 2;
+            }
+            k_scan_apply<KK><<<(unsigned)std::max<int64_t>(1, tiles), SCAN_THREADS, 0, st>>>(a, n, tiles);
+            ctx->launches++;
+        };
+        switch (k) {
+            case 1: run(std::integral_constant<int, 1>{}); break;
+            case 2: run(std::integral_constant<int, 2>{}); break;
+            case 3: run(std::integral_constant<int, 3>{}); break;
+            default: run(std::integral_constant<int, 4>{}); break;
+        }
+        CPSJ_LAUNCH_CHECK();
+    }
 
     void scan(const int64_t *in, int64_t *out, int64_t n) {
         size_t bytes = 0;
@@ -619,12 +759,15 @@ struct Driver {
     }
 
     // read up to eight device scalars with one synchronisation
+    double sync_us = 0;  // host time blocked in gather (diagnostics)
     void gather(Gather8 g, int cnt, int64_t *dscal, int64_t *out) {
         k_gather8<<<1, 32, 0, st>>>(g, cnt, dscal);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
         CPSJ_CUDA(cudaMemcpyAsync(ctx->h_scalars, dscal, cnt * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        const auto t0 = std::chrono::steady_clock::now();
         CPSJ_CUDA(cudaStreamSynchronize(st));
+        sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
         for (int i = 0; i < cnt; ++i) out[i] = ctx->h_scalars[i];
     }
 };
@@ -869,7 +1012,10 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     Emitter em(ctx, st, in, lam, ctr.p);
     int64_t max_depth = 0, levels = 0;
 
-    Level lv;
+    // level arrays: lv (current) and nx (next) swap each level; they and
+    // every per-level scratch array below keep their allocation across
+    // levels (DevBuf::ensure), so a level allocates nothing once warm
+    Level lv, nx;
     const int32_t R = plan->n_reps;
     if (n >= 2 && R > 0) {
         lv.N = R;
@@ -893,6 +1039,15 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     }
     const uint64_t child_off = (uint64_t)t + 64ull * (uint64_t)ell;
     const int vbits = plan->value_bits > 0 && plan->value_bits < 32 ? plan->value_bits : 32;
+    // per-level scratch (see above)
+    DevBuf<int64_t> tiles, spairs, internal, imem, tile_off, pair_off, iscan, im_off;
+    DevBuf<int64_t> ilist, im_off_c, flags, fscan, nsel, nent, seg_off, e_off, capsz, flist;
+    DevBuf<uint64_t> nsk;
+    DevBuf<int32_t> surv;
+    DevBuf<int16_t> sel_pos;
+    DevBuf<uint64_t> keys, keys2;
+    DevBuf<int32_t> vals, vals2;
+    DevBuf<int64_t> head, hscan, gstart, keep, ksize, kscan, mscan;
 
     // Three host synchronisations per level: (A) leaf/internal totals,
     // (B) candidate count + flag/entry totals, (C) child totals.  Every
@@ -909,19 +1064,17 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         if (trace) {
             CPSJ_CUDA(cudaStreamSynchronize(st));
             t_level = std::chrono::steady_clock::now();
+            drv.sync_us = 0;
         }
         // ---- (A) plan: leaves vs internal nodes
         std::unique_ptr<ProfScope> prof_plan(new ProfScope(ctx, PROF_PLAN, st));
-        DevBuf<int64_t> tiles(N + 1, st), spairs(N + 1, st), internal(N + 1, st), imem(N + 1, st);
-        DevBuf<int64_t> tile_off(N + 1, st), pair_off(N + 1, st), iscan(N + 1, st), im_off(N + 1, st);
+        for (DevBuf<int64_t> *b : {&tiles, &spairs, &internal, &imem, &tile_off, &pair_off, &iscan, &im_off})
+            b->ensure(N + 1, st);
         k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, spairs.p, internal.p, imem.p,
                                                   ctr.p);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
-        drv.scan(tiles.p, tile_off.p, N + 1);
-        drv.scan(spairs.p, pair_off.p, N + 1);
-        drv.scan(internal.p, iscan.p, N + 1);
-        drv.scan(imem.p, im_off.p, N + 1);
+        drv.scan_multi({tiles.p, spairs.p, internal.p, imem.p}, {tile_off.p, pair_off.p, iscan.p, im_off.p}, N + 1);
         int64_t sc[8];
         drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, pair_off.p + N}}, 4, dscal.p, sc);
         LeafWork work;
@@ -939,33 +1092,22 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         };
         gen_leaf();
 
-        Level nx;
-        // internal-node state that lives until the end of the level
-        DevBuf<int64_t> ilist, im_off_c, flags, fscan, nsel, nent, seg_off, e_off, capsz;
-        DevBuf<uint64_t> nsk;
-        DevBuf<int32_t> surv;
-        DevBuf<int16_t> sel_pos;
         if (n_int > 0) {
             std::unique_ptr<ProfScope> prof_node(new ProfScope(ctx, PROF_NODE, st));
-            ilist.alloc(n_int, st);
-            im_off_c.alloc(n_int + 1, st);
-            k_compact_internal<<<blocks_for(N), TPB, 0, st>>>(N, internal.p, iscan.p, ilist.p);
+            ilist.ensure(n_int, st);
+            im_off_c.ensure(n_int + 1, st);
+            k_compact_internal<<<blocks_for(N + 1), TPB, 0, st>>>(N, internal.p, iscan.p, ilist.p, im_off.p,
+                                                                  im_off_c.p);
             CPSJ_LAUNCH_CHECK();
-            {
-                DevBuf<int64_t> icnt(n_int + 1, st);
-                k_gather_counts<<<blocks_for(n_int + 1), TPB, 0, st>>>(n_int, ilist.p, lv.cnt.p, icnt.p);
-                CPSJ_LAUNCH_CHECK();
-                drv.scan(icnt.p, im_off_c.p, n_int + 1);
-            }
-            nsk.alloc(n_int * ell, st);
+            nsk.ensure(n_int * ell, st);
             if (!plan->use_count_table) {
                 k_node_sketch<<<(unsigned)n_int, TPB, 0, st>>>(ilist.p, lv.off.p, lv.cnt.p, lv.seed.p,
                                                                lv.members.p, in->d_sketch, ell, t,
                                                                reinterpret_cast<uint32_t *>(nsk.p), ctr.p);
                 CPSJ_LAUNCH_CHECK();
             }
-            flags.alloc(Mi + 1, st);
-            fscan.alloc(Mi + 1, st);
+            flags.ensure(Mi + 1, st);
+            fscan.ensure(Mi + 1, st);
             if (plan->use_count_table)
                 count_table_flags(ctx, drv, in, plan, vbits, n_int, Mi, ilist.p, im_off_c.p, lv, flags.p, st);
             else
@@ -973,29 +1115,25 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                                                             lv.members.p, in->d_sketch, ell, nsk.p, plan->flag_dist,
                                                             flags.p);
             CPSJ_LAUNCH_CHECK();
-            drv.scan(flags.p, fscan.p, Mi + 1);
-            surv.alloc(std::max<int64_t>(1, Mi), st);
+            drv.scan_multi({flags.p}, {fscan.p}, Mi + 1);
+            surv.ensure(std::max<int64_t>(1, Mi), st);
             k_survivors<<<blocks_for(Mi), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p, lv.members.p,
                                                         flags.p, fscan.p, surv.p);
             CPSJ_LAUNCH_CHECK();
-            ctx->launches += 5;
+            ctx->launches += 4;
             prof_node.reset();
             // ---- split, part 1: selected positions and entry counts
             ProfScope prof_split(ctx, PROF_SPLIT, st);
-            sel_pos.alloc(n_int * t, st);
-            nsel.alloc(n_int + 1, st);
-            nent.alloc(n_int + 1, st);
-            seg_off.alloc(n_int + 1, st);
-            e_off.alloc(n_int + 1, st);
-            capsz.alloc(n_int, st);
+            sel_pos.ensure(n_int * t, st);
+            for (DevBuf<int64_t> *b : {&nsel, &nent, &seg_off, &e_off}) b->ensure(n_int + 1, st);
+            capsz.ensure(n_int, st);
             CPSJ_CUDA(cudaMemsetAsync(&ctr.p->cap_n, 0, sizeof(unsigned long long), st));
             k_select<<<blocks_for((n_int + 1) * 32), TPB, 0, st>>>(
                 n_int, ilist.p, lv.cnt.p, lv.seed.p, depth, plan->depth_cap, im_off_c.p, fscan.p, t, plan->split_p,
                 sel_pos.p, nsel.p, nent.p, capsz.p, ctr.p);
             CPSJ_LAUNCH_CHECK();
             ctx->launches++;
-            drv.scan(nsel.p, seg_off.p, n_int + 1);
-            drv.scan(nent.p, e_off.p, n_int + 1);
+            drv.scan_multi({nsel.p, nent.p}, {seg_off.p, e_off.p}, n_int + 1);
         }
         // ---- (B) one read: leaf candidates, flags, split entries, depth caps
         {
@@ -1018,7 +1156,6 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         em.verify(n_leaf_cand, gen_leaf);
 
         // ---- point comparisons of flagged members (K2)
-        DevBuf<int64_t> flist;
         int count_pre = 1;
         auto gen_point = [&]() {
             ProfScope prof(ctx, PROF_POINT, st);
@@ -1031,7 +1168,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             count_pre = 0;  // a regeneration must not count twice
         };
         if (n_flag > 0) {
-            flist.alloc(n_flag, st);
+            flist.ensure(n_flag, st);
             k_flag_list<<<blocks_for(Mi), TPB, 0, st>>>(Mi, flags.p, fscan.p, flist.p);
             CPSJ_LAUNCH_CHECK();
             ctx->launches++;
@@ -1039,15 +1176,12 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         }
 
         // ---- split, part 2: stable group-by (K3)
-        DevBuf<uint64_t> keys, keys2;
-        DevBuf<int32_t> vals, vals2;
-        DevBuf<int64_t> head, hscan, gstart, keep, ksize, kscan, mscan;
         if (E > 0) {
             ProfScope prof_split(ctx, PROF_SPLIT, st);
-            keys.alloc(E, st);
-            keys2.alloc(E, st);
-            vals.alloc(E, st);
-            vals2.alloc(E, st);
+            keys.ensure(E, st);
+            keys2.ensure(E, st);
+            vals.ensure(E, st);
+            vals2.ensure(E, st);
             k_build_keys<<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p, im_off_c.p, fscan.p,
                                                         sel_pos.p, t, surv.p, in->d_values, vbits, keys.p, vals.p);
             CPSJ_LAUNCH_CHECK();
@@ -1060,23 +1194,16 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0,
                                                       end_bit, st));
             ctx->lib_calls++;
-            head.alloc(E + 1, st);
-            hscan.alloc(E + 1, st);
+            for (DevBuf<int64_t> *b : {&head, &hscan, &gstart, &keep, &ksize, &kscan, &mscan}) b->ensure(E + 1, st);
             k_heads<<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
             CPSJ_LAUNCH_CHECK();
-            drv.scan(head.p, hscan.p, E + 1);
-            gstart.alloc(E, st);
-            keep.alloc(E + 1, st);
-            ksize.alloc(E + 1, st);
-            kscan.alloc(E + 1, st);
-            mscan.alloc(E + 1, st);
+            drv.scan_multi({head.p}, {hscan.p}, E + 1);
             k_group_start<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p);
             CPSJ_LAUNCH_CHECK();
             k_group_keep<<<blocks_for(E + 1), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, ksize.p);
             CPSJ_LAUNCH_CHECK();
             ctx->launches += 4;
-            drv.scan(keep.p, kscan.p, E + 1);
-            drv.scan(ksize.p, mscan.p, E + 1);
+            drv.scan_multi({keep.p, ksize.p}, {kscan.p, mscan.p}, E + 1);
         }
         // ---- (C) one read: point candidates, children totals
         {
@@ -1091,11 +1218,11 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         nx.M = E > 0 ? sc[2] : 0;
         if (nx.N > 0) {
             ProfScope prof_split(ctx, PROF_SPLIT, st);
-            nx.off.alloc(nx.N, st);
-            nx.cnt.alloc(nx.N, st);
-            nx.seed.alloc(nx.N, st);
-            nx.S.alloc(nx.N, st);
-            nx.members.alloc(nx.M, st);
+            nx.off.ensure(nx.N, st);
+            nx.cnt.ensure(nx.N, st);
+            nx.seed.ensure(nx.N, st);
+            nx.S.ensure(nx.N, st);
+            nx.members.ensure(nx.M, st);
             k_children<<<blocks_for(E), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p,
                                                       keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p, lv.S.p,
                                                       child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, vbits,
@@ -1112,12 +1239,14 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_level).count();
             fprintf(stderr,
                     "[join] depth %d nodes %lld members %lld internal %lld (members %lld) leaf_tiles %lld "
-                    "leaf_pairs %lld leaf_cand %lld flagged %lld entries %lld children %lld | %.1f us\n",
+                    "leaf_pairs %lld leaf_cand %lld flagged %lld entries %lld children %lld | %.1f us "
+                    "(%.1f us blocked in syncs)\n",
                     depth, (long long)N, (long long)lv.M, (long long)n_int, (long long)Mi, (long long)work.tiles,
                     (long long)work.pairs, (long long)n_leaf_cand, (long long)n_flag, (long long)E,
-                    (long long)nx.N, us);
+                    (long long)nx.N, us, drv.sync_us);
         }
-        lv = std::move(nx);
+        std::swap(lv, nx);  // the old level's arrays become the next level's storage
+        nx.N = nx.M = 0;
     }
 
     // ---- K6: sort + unique of the verified pairs
