@@ -112,6 +112,8 @@ int cpsj_family_destroy(cpsj_family *fam) {
         if (p) cudaFree(p);
     for (void *p : fam->d_simg)
         if (p) cudaFree(p);
+    for (void *p : fam->d_vimg)
+        if (p) cudaFree(p);
     if (fam->d_bmimg) cudaFree(fam->d_bmimg);
     delete fam;
     return CPSJ_OK;

@@ -175,6 +175,7 @@ struct cpsj_family {
     void *d_img16[3] = {nullptr, nullptr, nullptr};
     // and the sketch kernel's [L][256][16]{8 functions} (h15 << 1 | bit) images
     void *d_simg[3] = {nullptr, nullptr, nullptr};
+    void *d_vimg[3] = {nullptr, nullptr, nullptr};  // same layout, top-16-bit entries (values kernel)
     uint32_t *d_bmimg = nullptr;
 };
 

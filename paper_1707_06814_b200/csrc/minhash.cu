@@ -518,14 +518,16 @@ __global__ void k_build_simg(const uint32_t *__restrict__ hi, const uint32_t *__
         if (fn < F) {
             const size_t base = (size_t)fn * 1024;
             v = hi[base + k * 256 + b];
-            bit = bitmask[(size_t)fn * 32 + k * 8 + (b >> 5)] >> (b & 31);
+            if (bitmask != nullptr) bit = bitmask[(size_t)fn * 32 + k * 8 + (b >> 5)] >> (b & 31);
             if (k == L - 1)
                 for (int kk = L; kk < 4; ++kk) {
                     v ^= hi[base + kk * 256];
-                    bit ^= bitmask[(size_t)fn * 32 + kk * 8];
+                    if (bitmask != nullptr) bit ^= bitmask[(size_t)fn * 32 + kk * 8];
                 }
         }
-        v16[q] = ((v >> 17) << 1) | (bit & 1u);
+        // sketch image: (top 15 hash bits << 1) | bit; values image (no bit
+        // tables): the top 16 hash bits
+        v16[q] = bitmask != nullptr ? ((v >> 17) << 1) | (bit & 1u) : v >> 16;
     }
     img[e] = make_uint4((v16[0] << 16) | v16[1], (v16[2] << 16) | v16[3], (v16[4] << 16) | v16[5],
                         (v16[6] << 16) | v16[7]);
@@ -731,6 +733,188 @@ __global__ void __launch_bounds__(K1H_THREADS, 1) k_sketch_s16(
     if (out.n > 1) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------
+// Values kernel (the production values path for L <= 3): the layout of
+// k_sketch_s16 (16 lanes per set, 8 functions per lane, one LDS.128 per key
+// byte) with the position keys of k_minhash_k16 -- values[r, i] is the
+// argmin TOKEN, so keys are (hash16 << 16) | position, `first` = min key,
+// `last` = min over (hash16 << 16) | (65535 - position); a tie on the 16
+// compared bits is first != last and is re-resolved exactly on the full
+// 64-bit hash.  Tokens are taken two at a time so every min is a
+// three-input VIMNMX3: per two tokens and two functions of a register,
+// 2 LOP3 + 2 XOR (high function's keys), 4 IMAD (low function's keys, FMA
+// pipe) and 4 VIMNMX3.
+__device__ __noinline__ uint32_t half_resolve16(const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+                                                int f, uint32_t m16, uint32_t col, int sh,
+                                                const uint32_t *__restrict__ tokens, int64_t beg, int len, int l,
+                                                unsigned hmask, int L) {
+    uint64_t bg = ~0ull;
+    uint32_t bt = 0xFFFFFFFFu;
+    const size_t base = (size_t)f * 1024;
+    for (int i = l; i < len; i += 16) {
+        const uint32_t tk = __ldg(tokens + beg + i);
+        uint32_t e = lds32(col + __byte_perm(tk, 0u, 0x4404));
+        if (L > 1) e ^= lds32(col + 65536u + (tk & 0xFF00u));
+        if (L > 2) e ^= lds32(col + 131072u + __byte_perm(tk, 0u, 0x4424));
+        if (((e >> sh) & 0xFFFFu) == m16) {
+            const uint32_t b0 = tk & 255, b1 = (tk >> 8) & 255, b2 = (tk >> 16) & 255, b3 = tk >> 24;
+            const uint32_t h = __ldg(hi + base + b0) ^ __ldg(hi + base + 256 + b1) ^ __ldg(hi + base + 512 + b2) ^
+                               __ldg(hi + base + 768 + b3);
+            const uint32_t lw = __ldg(lo + base + b0) ^ __ldg(lo + base + 256 + b1) ^ __ldg(lo + base + 512 + b2) ^
+                                __ldg(lo + base + 768 + b3);
+            const uint64_t g = ((uint64_t)h << 32) | lw;
+            if (g < bg || (g == bg && tk < bt)) {
+                bg = g;
+                bt = tk;
+            }
+        }
+    }
+    for (int o = 8; o > 0; o >>= 1) {
+        const uint64_t og = __shfl_xor_sync(hmask, bg, o);
+        const uint32_t ot = __shfl_xor_sync(hmask, bt, o);
+        if (og < bg || (og == bg && ot < bt)) {
+            bg = og;
+            bt = ot;
+        }
+    }
+    return bt;
+}
+
+__device__ __forceinline__ uint32_t imad16(uint32_t x, uint32_t add) {
+    uint32_t r;  // x * 2^16 + add on the FMA pipe
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(65536u), "r"(add));
+    return r;
+}
+
+template <int L>
+__global__ void __launch_bounds__(K1H_THREADS, 1) k_values_h8(
+    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
+    const int32_t *__restrict__ order, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+    const uint4 *__restrict__ vimg, int F, const K1Out out) {
+    extern __shared__ __align__(128) uint4 tab4[];  // [L][256][16] x uint4, then the mbarrier
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + L * 256 * 16);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int h = lane >> 4, l = lane & 15;
+    const unsigned hmask = 0xFFFFu << (16 * h);
+    const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tab4);
+    const uint32_t lane_base = smem0 + ((uint32_t)l << 4);
+    const int nchunks = (F + 127) >> 7;
+    const int64_t npairs = (n + 1) >> 1;
+    const int64_t p_first = (int64_t)blockIdx.x * K1H_WARPS + warp, p_step = (int64_t)gridDim.x * K1H_WARPS;
+    const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(mbar);
+    if (threadIdx.x == 0) mbar_init(mbar_a, 1);
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t tab_bytes = (uint32_t)L * 65536u;
+            fence_proxy_async_smem();
+            mbar_expect_tx(mbar_a, tab_bytes);
+            const char *src = reinterpret_cast<const char *>(vimg) + (size_t)c * tab_bytes;
+            const uint32_t dst = smem0;
+            for (uint32_t o = 0; o < tab_bytes; o += 32768u) bulk_g2s(dst + o, src + o, 32768u, mbar_a);
+        }
+        mbar_wait(mbar_a, phase);
+        phase ^= 1u;
+        for (int64_t pr = p_first; pr < npairs; pr += p_step) {
+            const int64_t idx = 2 * pr + h;
+            const bool has = idx < n;
+            int64_t s = 0, beg = 0, end = 0;
+            if (has) {
+                s = order != nullptr ? (int64_t)order[idx] : idx;
+                beg = offsets[s];
+                end = offsets[s + 1];
+            }
+            const int64_t len64 = end - beg;
+            const int len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
+            uint32_t tk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tk[q] = 0;
+            if (len > (int)K16_MASK + 1) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int f = (c << 7) + l + 16 * q;
+                    if (f < F) tk[q] = resolve_tie(hi, lo, f, tokens, beg, end);
+                }
+            } else if (len > 0) {
+                // f[2r] / f[2r+1]: first keys of the high / low function of
+                // register r; g[..]: last keys
+                uint32_t fk[8], gk[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) fk[q] = gk[q] = 0xFFFFFFFFu;
+                for (int base = 0; base < len; base += 16) {
+                    const int cnt = len - base < 16 ? len - base : 16;
+                    const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
+                    int j = 0;
+#pragma unroll 2
+                    for (; j + 1 < cnt; j += 2) {
+                        const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                        const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
+                        const uint4 ha = key_oct<L>(ta, lane_base);
+                        const uint4 hb = key_oct<L>(tb, lane_base);
+                        const uint32_t pa = (uint32_t)(base + j), pb = pa + 1;
+                        const uint32_t qa = K16_MASK - pa, qb = qa - 1;
+                        const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w}, xb[4] = {hb.x, hb.y, hb.z, hb.w};
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const uint32_t ma = xa[r] & 0xFFFF0000u, mb = xb[r] & 0xFFFF0000u;
+                            fk[2 * r] = __vimin3_u32(fk[2 * r], ma | pa, mb | pb);
+                            gk[2 * r] = __vimin3_u32(gk[2 * r], ma | qa, mb | qb);
+                            fk[2 * r + 1] = __vimin3_u32(fk[2 * r + 1], imad16(xa[r], pa), imad16(xb[r], pb));
+                            gk[2 * r + 1] = __vimin3_u32(gk[2 * r + 1], imad16(xa[r], qa), imad16(xb[r], qb));
+                        }
+                    }
+                    if (j < cnt) {
+                        const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                        const uint4 ha = key_oct<L>(ta, lane_base);
+                        const uint32_t pa = (uint32_t)(base + j), qa = K16_MASK - pa;
+                        const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w};
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const uint32_t ma = xa[r] & 0xFFFF0000u;
+                            fk[2 * r] = min(fk[2 * r], ma | pa);
+                            gk[2 * r] = min(gk[2 * r], ma | qa);
+                            fk[2 * r + 1] = min(fk[2 * r + 1], imad16(xa[r], pa));
+                            gk[2 * r + 1] = min(gk[2 * r + 1], imad16(xa[r], qa));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    // slot q = 2r (+1): function l + 32r (+16) of this chunk
+                    const int r = q >> 1;
+                    const int f = (c << 7) + l + 32 * r + 16 * (q & 1);
+                    tk[q] = __ldg(tokens + beg + (fk[q] & K16_MASK));
+                    const bool tie = (fk[q] & K16_MASK) != K16_MASK - (gk[q] & K16_MASK);
+                    unsigned tied = __ballot_sync(hmask, tie && f < F);
+                    while (tied) {
+                        const int src = __ffs(tied) - 1;
+                        tied &= tied - 1;
+                        const int fs = __shfl_sync(hmask, f, src);
+                        const uint32_t m16 = __shfl_sync(hmask, fk[q] >> 16, src);
+                        const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * r;
+                        const uint32_t tb = half_resolve16(hi, lo, fs, m16, col, (q & 1) ? 0 : 16, tokens, beg, len,
+                                                           l, hmask, L);
+                        if (lane == src) tk[q] = tb;
+                    }
+                }
+            }
+            const int64_t row = out.row0 + s;
+            if (has) {
+                for (int d = 0; d < out.n; ++d) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int f = (c << 7) + l + 32 * (q >> 1) + 16 * (q & 1);
+                        if (f < F) out.values[d][row * F + f] = tk[q];
+                    }
+                }
+            }
+        }
+    }
+    if (out.n > 1) __threadfence_system();
+}
+
 // length-bucketed visiting order of the half-warp kernels: a counting sort
 // of the sets by min(|x|, 1023), longest first (the last, partial round of
 // the grid-stride loop gets the shortest sets); the order within a bucket
@@ -809,6 +993,22 @@ static DevBuf<int32_t> length_order(cpsj_ctx *ctx, const int64_t *off, int64_t n
         ctx->launches += 3;
     }
     return order;
+}
+
+template <int L>
+static void launch_values_h8(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
+                             int64_t n, const K1Out &out, cudaStream_t stream) {
+    const int smem = L * 256 * 16 * 16 + 16;
+    CPSJ_CUDA(cudaFuncSetAttribute(k_values_h8<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ProfScope prof(ctx, PROF_K1, stream);
+    DevBuf<int32_t> order = length_order(ctx, off, n, stream);
+    const int64_t want = ((n + 1) / 2 + K1H_WARPS - 1) / K1H_WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
+    k_values_h8<L><<<grid, K1H_THREADS, smem, stream>>>(tok, off, n, order.p, fam->d_hi, fam->d_lo,
+                                                        reinterpret_cast<const uint4 *>(fam->d_vimg[L - 1]), fam->F,
+                                                        out);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches++;
 }
 
 template <int L>
@@ -913,6 +1113,15 @@ void minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t 
         }
         return;
     }
+    const char *h8 = getenv("CPSJ_K1_NO_H8");  // A/B switch: values by the full-warp kernel
+    if (want_values && !want_sketch && L < 4 && fam->d_vimg[L - 1] != nullptr && !(h8 && h8[0] == '1')) {
+        switch (L) {
+            case 1: launch_values_h8<1>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+            case 2: launch_values_h8<2>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+            default: launch_values_h8<3>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
+        }
+        return;
+    }
     switch (L) {
         case 1: launch_minhash_k16<1>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
         case 2: launch_minhash_k16<2>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
@@ -960,9 +1169,14 @@ void prepare_family(cpsj_ctx *ctx, cpsj_family *fam, const uint64_t *h_mh, const
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
     }
-    if (fam->d_bitmask != nullptr) {
-        for (int L = 1; L <= 3; ++L) {
-            const int64_t elems8 = (int64_t)nchunks * L * 256 * 16;
+    for (int L = 1; L <= 3; ++L) {
+        const int64_t elems8 = (int64_t)nchunks * L * 256 * 16;
+        CPSJ_CUDA(cudaMalloc(&fam->d_vimg[L - 1], elems8 * sizeof(uint4)));
+        k_build_simg<<<(unsigned)((elems8 + 255) / 256), 256, 0, stream>>>(
+            fam->d_hi, nullptr, fam->F, L, elems8, reinterpret_cast<uint4 *>(fam->d_vimg[L - 1]));
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+        if (fam->d_bitmask != nullptr) {
             CPSJ_CUDA(cudaMalloc(&fam->d_simg[L - 1], elems8 * sizeof(uint4)));
             k_build_simg<<<(unsigned)((elems8 + 255) / 256), 256, 0, stream>>>(
                 fam->d_hi, fam->d_bitmask, fam->F, L, elems8, reinterpret_cast<uint4 *>(fam->d_simg[L - 1]));

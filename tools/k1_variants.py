@@ -45,13 +45,12 @@ def run(fam, vals, sk):
 
 
 VARIANTS = {
-    "k16": {"CPSJ_K1_NO_S16": "1"},
-    "s16": {},
-    "s16_noorder": {"CPSJ_K1_NO_ORDER": "1"},
+    "k16+s16": {"CPSJ_K1_NO_H8": "1"},
+    "h8+s16": {},
 }
 ref_v = ref_s = None
 for name, env in VARIANTS.items():
-    for k in ("CPSJ_K1_K16", "CPSJ_K1_FM", "CPSJ_K1_NO_ORDER", "CPSJ_K1_NO_S16"):
+    for k in ("CPSJ_K1_NO_H8", "CPSJ_K1_NO_ORDER", "CPSJ_K1_NO_S16"):
         os.environ.pop(k, None)
     os.environ.update(env)
     vals = torch.zeros((n, 128), dtype=torch.int32, device=dev)
