@@ -63,11 +63,36 @@ inline unsigned blocks_for(int64_t n, int tpb = TPB) {
 // internal flag + member count; leaf pre-candidates m(m-1)/2 (cps:144)
 // Leaves of <= 32 members go to the pair-packed kernel (one thread per
 // pair), larger leaves to the tile kernel.
+// With `slists` (SMALL_CLASSES lists of N), leaves of 2..32 members are
+// also listed by size class c (segment width 4 << c lanes, k_leaf_small),
+// counts in scount[c].
+constexpr int SMALL_CLASSES = 4;
+__device__ __host__ __forceinline__ int small_class(int64_t m) {
+    return m <= 4 ? 0 : m <= 8 ? 1 : m <= 16 ? 2 : 3;
+}
+
 __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit,
                        int64_t *__restrict__ tiles, int64_t *__restrict__ spairs, int64_t *__restrict__ internal,
-                       int64_t *__restrict__ imem, DevCounters *ctr) {
+                       int64_t *__restrict__ imem, DevCounters *ctr, int64_t *__restrict__ slists = nullptr,
+                       unsigned long long *__restrict__ scount = nullptr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long pre = 0;
+    if (slists != nullptr) {
+        // small leaves straight into their class lists (warp-aggregated
+        // appends; the order inside a class does not matter)
+        const int64_t m = i < N ? cnt[i] : 0;
+        const int c = (i < N && m <= limit && m >= 2 && m <= 32) ? small_class(m) : -1;
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int k = 0; k < SMALL_CLASSES; ++k) {
+            const unsigned mask = __ballot_sync(0xffffffffu, c == k);
+            if (mask == 0) continue;
+            unsigned long long base = 0;
+            if (lane == __ffs(mask) - 1) base = atomicAdd(scount + k, (unsigned long long)__popc(mask));
+            base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+            if (c == k) slists[(int64_t)k * N + base + __popc(mask & ((1u << lane) - 1))] = i;
+        }
+    }
     if (i < N) {
         const int64_t m = cnt[i];
         const bool leaf = m <= limit;
@@ -110,6 +135,107 @@ struct Sk {
     uint64_t w[ELL];
 };
 
+// warp-aggregated candidate append
+__device__ __forceinline__ void emit_pair(bool pass, int32_t a, int32_t b, int2 *cand, unsigned long long cap,
+                                          DevCounters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const unsigned mask = __ballot_sync(0xffffffffu, pass);
+    if (mask) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&ctr->cand_n, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (pass) {
+            const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1));
+            if (slot < cap) cand[slot] = make_int2(a, b);
+        }
+    }
+}
+
+// All pairs of a block of mb <= W members held one per lane of a W-lane
+// segment (sl = lane % W): round k pairs member sl with member (sl + k) mod
+// mb, k = 1 .. floor(mb / 2) (the last round of an even mb only for
+// sl < mb / 2), which visits every unordered pair exactly once with mb of
+// the segment's W lanes busy per round.  The partner's sketch arrives by
+// shuffle, words in order, with warp-wide early exits (the distance only
+// grows).  `kmax` is the warp-uniform round count.
+template <int ELL>
+__device__ __forceinline__ void cyclic_block(int32_t x, int32_t xsize, const uint64_t *__restrict__ sketch, int lane,
+                                             int mb, int W, bool valid, int kmax, const int8_t *__restrict__ side,
+                                             int32_t accept, double lam, int2 *cand, unsigned long long cap,
+                                             DevCounters *ctr) {
+    uint64_t w[ELL];
+#pragma unroll
+    for (int k = 0; k < ELL; ++k) w[k] = valid ? __ldg(sketch + (size_t)x * ELL + k) : 0ull;
+    const int sl = lane & (W - 1), seg0 = lane - sl;
+    for (int k = 1; k <= kmax; ++k) {
+        int ps = sl + k;
+        if (ps >= mb) ps -= mb;
+        const int src = valid ? seg0 + ps : lane;
+        const bool active = valid && (2 * k < mb || (2 * k == mb && sl < k));
+        int dist = 0;
+        if (ELL >= 8) {
+            constexpr int C1 = ELL * 5 / 8, C2 = ELL * 6 / 8;
+#pragma unroll
+            for (int q = 0; q < C1; ++q) dist += __popcll(w[q] ^ __shfl_sync(0xffffffffu, w[q], src));
+            if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
+#pragma unroll
+            for (int q = C1; q < C2; ++q) dist += __popcll(w[q] ^ __shfl_sync(0xffffffffu, w[q], src));
+            if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
+#pragma unroll
+            for (int q = C2; q < ELL; ++q) dist += __popcll(w[q] ^ __shfl_sync(0xffffffffu, w[q], src));
+        } else {
+#pragma unroll
+            for (int q = 0; q < ELL; ++q) dist += __popcll(w[q] ^ __shfl_sync(0xffffffffu, w[q], src));
+        }
+        const int32_t y = __shfl_sync(0xffffffffu, x, src);
+        const int32_t ysize = __shfl_sync(0xffffffffu, xsize, src);
+        bool pass = active && dist <= accept;
+        if (pass) pass = size_filter(xsize, ysize, lam) && (side == nullptr || side[x] != side[y]);
+        emit_pair(pass, x, y, cand, cap, ctr);
+    }
+}
+
+// BruteForce of leaves of 2..32 members (cps:139-157): leaves of size class
+// c (<= 4, 8, 16, 32 members) occupy segments of W = 4 << c lanes, 32 / W
+// leaves per warp, each leaf's pairs by the cyclic schedule above (members'
+// sketches in registers, partners by shuffle).  Warps of class c are
+// [wcum[c], wcum[c + 1]); list[c] holds the class's nodes.
+struct SmallLeaves {
+    const int64_t *list[SMALL_CLASSES];
+    int64_t cnt[SMALL_CLASSES];
+    int64_t wcum[SMALL_CLASSES + 1];
+};
+
+template <int ELL>
+__global__ void __launch_bounds__(TPB) k_leaf_small(SmallLeaves sl, const int64_t *__restrict__ nd_off,
+                                                    const int32_t *__restrict__ nd_cnt,
+                                                    const int32_t *__restrict__ members,
+                                                    const uint64_t *__restrict__ sketch,
+                                                    const int32_t *__restrict__ sizes, const int8_t *__restrict__ side,
+                                                    int32_t accept, double lam, int2 *__restrict__ cand,
+                                                    unsigned long long cap, DevCounters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wg >= sl.wcum[SMALL_CLASSES]) return;
+    int c = 0;
+    while (wg >= sl.wcum[c + 1]) ++c;
+    const int W = 4 << c;
+    const int64_t j = (wg - sl.wcum[c]) * (32 / W) + lane / W;
+    const bool has = j < sl.cnt[c];
+    int m = 0;
+    int32_t x = 0;
+    const int s0 = lane & (W - 1);
+    if (has) {
+        const int64_t node = sl.list[c][j];
+        m = nd_cnt[node];
+        if (s0 < m) x = members[nd_off[node] + s0];
+    }
+    const bool valid = has && s0 < m;
+    const int kmax = __reduce_max_sync(0xffffffffu, (unsigned)(m >> 1));
+    cyclic_block<ELL>(x, valid ? sizes[x] : 0, sketch, lane, m, W, valid, kmax, side, accept, lam, cand, cap, ctr);
+}
+
+
 // one warp per 32x32 tile of a leaf's pair space; lane = column member,
 // loop over the 32 row members; popcount(xor) <= accept passes the sketch
 // filter (matches >= k*), then the size filter; survivors are appended to
@@ -144,6 +270,63 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
     while (local >= T - bi) { local -= T - bi; ++bi; }
     const int bj = bi + (int)local;
     const int32_t *mem = members + nd_off[node];
+    if (ELL > 0) {
+        constexpr int EK = ELL > 0 ? ELL : 1;
+        if (bi == bj) {
+            // diagonal tile: the cyclic schedule of k_leaf_small (~97% of the
+            // lane slots useful instead of 48%)
+            const int mb = min(32, m - (bi << 5));
+            const int jj = (bi << 5) + lane;
+            const int32_t x = lane < mb ? mem[jj] : 0;
+            cyclic_block<EK>(x, lane < mb ? sizes[x] : 0, sketch, lane, mb, 32, lane < mb, mb >> 1, side, accept, lam,
+                             cand, cap, ctr);
+            return;
+        }
+        // off-diagonal tile: block bi is always full; a partial block bj
+        // (the leaf's last) becomes the ROW side so every lane has a column
+        const int nb = min(32, m - (bj << 5));
+        const bool swap = nb < 32;
+        const int cbk = swap ? bi : bj, rbk = swap ? bj : bi, nrows = swap ? nb : 32;
+        const int32_t colx = mem[(cbk << 5) + lane];
+        const int32_t colsz = sizes[colx];
+        Sk<EK> cw;
+#pragma unroll
+        for (int k = 0; k < EK; ++k) cw.w[k] = __ldg(sketch + (size_t)colx * EK + k);
+        __shared__ uint64_t rs2[TPB / 32][32][EK];
+        __shared__ int32_t rid2[TPB / 32][32], rsz2[TPB / 32][32];
+        const int wb = threadIdx.x >> 5;
+        {
+            const int32_t r = lane < nrows ? mem[(rbk << 5) + lane] : 0;
+            rid2[wb][lane] = r;
+            rsz2[wb][lane] = lane < nrows ? sizes[r] : 0;
+#pragma unroll
+            for (int k = 0; k < EK; ++k) rs2[wb][lane][k] = lane < nrows ? __ldg(sketch + (size_t)r * EK + k) : 0ull;
+            __syncwarp();
+        }
+        for (int i = 0; i < nrows; ++i) {
+            const uint64_t *rs = rs2[wb][i];
+            int dist = 0;
+            if (EK >= 8) {
+                constexpr int C1 = EK * 5 / 8, C2 = EK * 6 / 8;
+#pragma unroll
+                for (int k = 0; k < C1; ++k) dist += __popcll(rs[k] ^ cw.w[k]);
+                if (!__any_sync(0xffffffffu, dist <= accept)) continue;
+#pragma unroll
+                for (int k = C1; k < C2; ++k) dist += __popcll(rs[k] ^ cw.w[k]);
+                if (!__any_sync(0xffffffffu, dist <= accept)) continue;
+#pragma unroll
+                for (int k = C2; k < EK; ++k) dist += __popcll(rs[k] ^ cw.w[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < EK; ++k) dist += __popcll(rs[k] ^ cw.w[k]);
+            }
+            const int32_t row = rid2[wb][i];
+            bool pass = dist <= accept;
+            if (pass) pass = size_filter(rsz2[wb][i], colsz, lam) && (side == nullptr || side[row] != side[colx]);
+            emit_pair(pass, row, colx, cand, cap, ctr);
+        }
+        return;
+    }
     const int j = (bj << 5) + lane;
     const bool jvalid = j < m;
     const int32_t col = jvalid ? mem[j] : 0;
@@ -777,6 +960,8 @@ struct LeafWork {
     const int64_t *tile_off = nullptr;
     int64_t pairs = 0;            // pairs of leaves with m <= 32 (pair-packed)
     const int64_t *pair_off = nullptr;
+    bool small = false;           // leaves with m <= 32 by k_leaf_small instead
+    SmallLeaves sl{};
 };
 
 template <int ELL>
@@ -791,7 +976,16 @@ void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
     }
-    if (wk.pairs > 0) {
+    if (wk.small) {
+        if (ELL > 0 && wk.sl.wcum[SMALL_CLASSES] > 0) {
+            constexpr int EK = ELL > 0 ? ELL : 1;
+            k_leaf_small<EK><<<blocks_for(wk.sl.wcum[SMALL_CLASSES] * 32), TPB, 0, st>>>(
+                wk.sl, lv.off.p, lv.cnt.p, lv.members.p, in->d_sketch, in->d_sizes, in->d_side, accept, lam, cand,
+                cap, ctr);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+        }
+    } else if (wk.pairs > 0) {
         k_leaf_pairs<ELL><<<blocks_for(wk.pairs), TPB, 0, st>>>(wk.pairs, wk.pair_off, lv.N, lv.off.p, lv.cnt.p,
                                                                 lv.members.p, in->d_sketch, in->ell, in->d_sizes,
                                                                 in->d_side, accept, lam, cand, cap, ctr);
@@ -1040,7 +1234,12 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     const uint64_t child_off = (uint64_t)t + 64ull * (uint64_t)ell;
     const int vbits = plan->value_bits > 0 && plan->value_bits < 32 ? plan->value_bits : 32;
     // per-level scratch (see above)
-    DevBuf<int64_t> tiles, spairs, internal, imem, tile_off, pair_off, iscan, im_off;
+    DevBuf<int64_t> tiles, spairs, internal, imem, tile_off, pair_off, iscan, im_off, slists;
+    DevBuf<unsigned long long> scount(SMALL_CLASSES, st);
+    // leaves of <= 32 members by size class (k_leaf_small) for compile-time ell
+    const char *small_env = getenv("CPSJ_NO_SMALL_LEAF");  // A/B switch: pair-packed k_leaf_pairs
+    const bool small_kernel = (ell == 1 || ell == 2 || ell == 4 || ell == 8 || ell == 16) &&
+                              !(small_env != nullptr && small_env[0] == '1');
     DevBuf<int64_t> ilist, im_off_c, flags, fscan, nsel, nent, seg_off, e_off, capsz, flist;
     DevBuf<uint64_t> nsk;
     DevBuf<int32_t> surv;
@@ -1070,24 +1269,44 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         std::unique_ptr<ProfScope> prof_plan(new ProfScope(ctx, PROF_PLAN, st));
         for (DevBuf<int64_t> *b : {&tiles, &spairs, &internal, &imem, &tile_off, &pair_off, &iscan, &im_off})
             b->ensure(N + 1, st);
+        if (small_kernel) {
+            slists.ensure((size_t)SMALL_CLASSES * N, st);
+            CPSJ_CUDA(cudaMemsetAsync(scount.p, 0, SMALL_CLASSES * sizeof(unsigned long long), st));
+        }
         k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, spairs.p, internal.p, imem.p,
-                                                  ctr.p);
+                                                  ctr.p, small_kernel ? slists.p : nullptr, scount.p);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
-        drv.scan_multi({tiles.p, spairs.p, internal.p, imem.p}, {tile_off.p, pair_off.p, iscan.p, im_off.p}, N + 1);
         int64_t sc[8];
-        drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, pair_off.p + N}}, 4, dscal.p, sc);
         LeafWork work;
+        if (small_kernel) {
+            drv.scan_multi({tiles.p, internal.p, imem.p}, {tile_off.p, iscan.p, im_off.p}, N + 1);
+            const int64_t *c64 = reinterpret_cast<const int64_t *>(scount.p);
+            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, c64, c64 + 1, c64 + 2, c64 + 3}}, 7, dscal.p,
+                       sc);
+            work.small = true;
+            work.sl.wcum[0] = 0;
+            for (int k = 0; k < SMALL_CLASSES; ++k) {
+                const int W = 4 << k;
+                work.sl.list[k] = slists.p + (size_t)k * N;
+                work.sl.cnt[k] = sc[3 + k];
+                work.sl.wcum[k + 1] = work.sl.wcum[k] + (sc[3 + k] * W + 31) / 32;
+            }
+        } else {
+            drv.scan_multi({tiles.p, spairs.p, internal.p, imem.p}, {tile_off.p, pair_off.p, iscan.p, im_off.p},
+                           N + 1);
+            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, pair_off.p + N}}, 4, dscal.p, sc);
+            work.pairs = sc[3];
+            work.pair_off = pair_off.p;
+        }
         work.tiles = sc[0];
         work.tile_off = tile_off.p;
-        work.pairs = sc[3];
-        work.pair_off = pair_off.p;
         const int64_t n_int = sc[1], Mi = sc[2];
         prof_plan.reset();
 
         // ---- leaves: K4 (candidates verified after sync B)
         auto gen_leaf = [&]() {
-            if (work.tiles > 0 || work.pairs > 0)
+            if (work.tiles > 0 || work.pairs > 0 || (work.small && work.sl.wcum[SMALL_CLASSES] > 0))
                 leaf_dispatch(ctx, st, work, lv, in, plan->accept_dist, lam, em.cand.p, em.cand_cap, ctr.p);
         };
         gen_leaf();
@@ -1239,10 +1458,11 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_level).count();
             fprintf(stderr,
                     "[join] depth %d nodes %lld members %lld internal %lld (members %lld) leaf_tiles %lld "
-                    "leaf_pairs %lld leaf_cand %lld flagged %lld entries %lld children %lld | %.1f us "
+                    "small_leaves|pairs %lld leaf_cand %lld flagged %lld entries %lld children %lld | %.1f us "
                     "(%.1f us blocked in syncs)\n",
                     depth, (long long)N, (long long)lv.M, (long long)n_int, (long long)Mi, (long long)work.tiles,
-                    (long long)work.pairs, (long long)n_leaf_cand, (long long)n_flag, (long long)E,
+                    (long long)(work.small ? work.sl.cnt[0] + work.sl.cnt[1] + work.sl.cnt[2] + work.sl.cnt[3]
+                                           : work.pairs), (long long)n_leaf_cand, (long long)n_flag, (long long)E,
                     (long long)nx.N, us, drv.sync_us);
         }
         std::swap(lv, nx);  // the old level's arrays become the next level's storage
