@@ -407,7 +407,7 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
         trace.append(("k1", kev))
     for c in range(chunks):
         s0, s1 = int(bounds[c]), int(bounds[c + 1])
-        compute.wait_event(events[c])
+        compute.wait_event(events[-1] if _PIPE_SERIAL else events[c])
         if trace is not None:
             e = torch.cuda.Event(enable_timing=True)
             e.record(compute)
@@ -434,11 +434,12 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
 # small; every later chunk must arrive while K1 hashes the previous one.  The
 # H2D rate (pinned, ~44 GB/s of CSR on the B200 box) against K1 (values +
 # sketch, ~30 GB/s of CSR on config 2) allows a growth factor of about 1.5,
-# and every chunk costs ~0.15 ms of K1 launch overhead (table loads, tails),
-# so the schedule trades the exposed first copy against the chunk count
-# (simulated optimum on config 2: 1/32 growing by 1.6, 7 chunks).
+# and every chunk costs ~0.25 ms (K1 launch overhead, and K1 runs slower
+# while a copy is in flight), so the schedule trades the exposed first copy
+# against the chunk count (simulated optimum on config 2 for 7.4-8.9 ms of
+# H2D: 1/32 growing by 1.8, 6 chunks).
 _FIRST_CHUNK = 1.0 / 32
-_CHUNK_GROWTH = 1.6
+_CHUNK_GROWTH = 1.8
 
 
 def _chunk_bounds(n: int, chunks: int | None) -> np.ndarray:
@@ -461,6 +462,7 @@ def _chunk_bounds(n: int, chunks: int | None) -> np.ndarray:
 
 _COPY_STREAMS: dict = {}
 _PIPE_TRACE = None  # diagnostics (tools/embed_probe.py): an empty list collects one call's events
+_PIPE_SERIAL = False  # diagnostics: every chunk waits for the whole copy
 
 
 def _copy_stream(dev):

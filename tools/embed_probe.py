@@ -146,3 +146,26 @@ for c in range(len(cop)):
     print(c, f"{st.elapsed_time(cop[c]):8.3f}", f"{st.elapsed_time(kst[c]):8.3f}")
 print("end", f"{st.elapsed_time(en):.3f}")
 E._PIPE_TRACE = None
+
+E._PIPE_SERIAL = True
+print(f"pipelined embed, K1 after the whole copy: {timed(pipe):.2f} ms")
+E._PIPE_TRACE = []
+torch.cuda.synchronize()
+st.record()
+pipe()
+en.record()
+torch.cuda.synchronize()
+cop = dict(E._PIPE_TRACE)["copies"]; kst = dict(E._PIPE_TRACE)["k1"]
+for c in range(len(cop)):
+    print("serial", c, f"{st.elapsed_time(cop[c]):8.3f}", f"{st.elapsed_time(kst[c]):8.3f}")
+print("serial end", f"{st.elapsed_time(en):.3f}")
+E._PIPE_TRACE = None
+E._PIPE_SERIAL = False
+
+cs = torch.cuda.Stream()
+def pipe_cs():
+    with torch.cuda.stream(cs):
+        embed_dataset(ep, ds, sketch=skey)
+    torch.cuda.current_stream().wait_stream(cs)
+print(f"pipelined embed on a non-default compute stream: {timed(pipe_cs):.2f} ms")
+print("copier stream", E._copy_stream(dev), "default", torch.cuda.current_stream(), torch.cuda.default_stream())
