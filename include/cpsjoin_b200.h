@@ -76,6 +76,19 @@ CPSJ_API int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam,
                         void *stream);
 
 /*
+ * K1 for the embed path: the embedding family's values AND the sketch
+ * family's sketches of the same n_sets CSR sets in one launch (one
+ * length-ordered pass per 128-function chunk of either family).
+ * Replaces embed_dataset (embed.py:117-139) followed by
+ * EmbeddedDataset.sketches (embed.py:90-98 -> build_sketch_matrix,
+ * hashing.py:197-211); outputs as cpsj_minhash_sketch's (both required).
+ */
+CPSJ_API int cpsj_minhash_embed(cpsj_ctx *ctx, const cpsj_family *emb_fam, const cpsj_family *sketch_fam,
+                       const uint32_t *d_tokens, const int64_t *d_offsets,
+                       int64_t n_sets, uint32_t max_token,
+                       uint32_t *d_values_out, uint64_t *d_sketch_out, void *stream);
+
+/*
  * K1 with several output destinations: the n_sets rows computed here (the
  * CSR rows d_offsets[0 .. n_sets]) are written to rows row0 .. row0+n_sets-1
  * of every destination.  With the destinations = the same (n, F) values and

@@ -48,7 +48,8 @@ EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_err
            "cpsj_join_copy_result", "cpsj_join_result_device", "cpsj_profile_enable", "cpsj_profile_read",
            "cpsj_launch_counts", "cpsj_frequency_order", "cpsj_exact_join",
            "cpsj_lsh_join", "cpsj_ingest_lists", "cpsj_parse_text", "cpsj_ingest_result_device", "cpsj_ingest_copy",
-           "cpsj_minhash_sketch_multi", "cpsj_xbuf_create", "cpsj_xbuf_open", "cpsj_xbuf_close"]
+           "cpsj_minhash_sketch_multi", "cpsj_xbuf_create", "cpsj_xbuf_open", "cpsj_xbuf_close",
+           "cpsj_minhash_embed"]
 
 MAX_DSTS = 8
 IPC_HANDLE_BYTES = 64
@@ -85,6 +86,7 @@ def load(path: str | None = None):
         L.cpsj_family_create.argtypes = [P, P, P, i32, ctypes.POINTER(P)]
         L.cpsj_family_destroy.argtypes = [P]
         L.cpsj_minhash_sketch.argtypes = [P, P, P, P, i64, u32, P, P, P]
+        L.cpsj_minhash_embed.argtypes = [P, P, P, P, P, i64, u32, P, P, P]
         L.cpsj_self_join.argtypes = [P, ctypes.POINTER(Inputs), ctypes.POINTER(Plan),
                                      ctypes.POINTER(JoinStats), P]
         L.cpsj_join_copy_result.argtypes = [P, P, P, i64, P, i64, P]

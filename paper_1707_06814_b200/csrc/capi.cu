@@ -130,6 +130,18 @@ int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d
     });
 }
 
+int cpsj_minhash_embed(cpsj_ctx *ctx, const cpsj_family *emb_fam, const cpsj_family *sketch_fam,
+                       const uint32_t *d_tokens, const int64_t *d_offsets, int64_t n_sets, uint32_t max_token,
+                       uint32_t *d_values_out, uint64_t *d_sketch_out, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(n_sets == 0 || (d_tokens && d_offsets), "null CSR pointers");
+        cpsj::require(d_values_out && d_sketch_out, "cpsj_minhash_embed needs both outputs");
+        cpsj::minhash_embed(ctx, emb_fam, sketch_fam, d_tokens, d_offsets, n_sets, max_token, d_values_out,
+                            d_sketch_out, (cudaStream_t)stream);
+    });
+}
+
 int cpsj_minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,
                               const int64_t *d_offsets, int64_t n_sets, uint32_t max_token, const cpsj_k1_dsts *dsts,
                               void *stream) {

@@ -217,6 +217,9 @@ struct K1Out {
 
 void minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens, const int64_t *d_offsets,
                           int64_t n, uint32_t max_token, const K1Out &out, cudaStream_t stream);
+void minhash_embed(cpsj_ctx *ctx, const cpsj_family *efam, const cpsj_family *sfam, const uint32_t *d_tokens,
+                   const int64_t *d_offsets, int64_t n, uint32_t max_token, uint32_t *d_values, uint64_t *d_sketch,
+                   cudaStream_t stream);
 int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,
                    const int64_t *d_offsets, int64_t n, uint32_t max_token, uint32_t *d_values,
                    uint64_t *d_sketch, cudaStream_t stream);

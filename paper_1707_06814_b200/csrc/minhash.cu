@@ -915,6 +915,249 @@ __global__ void __launch_bounds__(K1H_THREADS, 1) k_values_h8(
     if (out.n > 1) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------
+// Values + sketches in ONE launch (the embed path: embed_dataset with a
+// sketch hint, and every pipelined chunk): job 0.. of the embedding family's
+// value chunks, then the sketch family's chunks, one length order and one
+// launch tail for both (k_values_h8 and k_sketch_s16 bodies).
+template <int L>
+__global__ void __launch_bounds__(K1H_THREADS, 1) k_embed_h8(
+    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
+    const int32_t *__restrict__ order, const uint32_t *__restrict__ ehi, const uint32_t *__restrict__ elo,
+    const uint4 *__restrict__ vimg, int FV, const uint32_t *__restrict__ shi, const uint32_t *__restrict__ slo,
+    const uint32_t *__restrict__ bitmask, const uint4 *__restrict__ simg, int FS, const K1Out vout,
+    const K1Out sout) {
+    extern __shared__ __align__(128) uint4 tab4[];  // [L][256][16] x uint4, then the mbarrier
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + L * 256 * 16);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int h = lane >> 4, l = lane & 15;
+    const unsigned hmask = 0xFFFFu << (16 * h);
+    const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tab4);
+    const uint32_t lane_base = smem0 + ((uint32_t)l << 4);
+    const int nv = (FV + 127) >> 7, ns = (FS + 127) >> 7;
+    const int64_t npairs = (n + 1) >> 1;
+    const int64_t p_first = (int64_t)blockIdx.x * K1H_WARPS + warp, p_step = (int64_t)gridDim.x * K1H_WARPS;
+    const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(mbar);
+    if (threadIdx.x == 0) mbar_init(mbar_a, 1);
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int job = 0; job < nv + ns; ++job) {
+        const bool is_val = job < nv;
+        const int c = is_val ? job : job - nv;
+        __syncthreads();  // every warp is done with the previous chunk's tables
+        if (threadIdx.x == 0) {
+            const uint32_t tab_bytes = (uint32_t)L * 65536u;
+            fence_proxy_async_smem();
+            mbar_expect_tx(mbar_a, tab_bytes);
+            const char *src = reinterpret_cast<const char *>(is_val ? vimg : simg) + (size_t)c * tab_bytes;
+            for (uint32_t o = 0; o < tab_bytes; o += 32768u) bulk_g2s(smem0 + o, src + o, 32768u, mbar_a);
+        }
+        mbar_wait(mbar_a, phase);
+        phase ^= 1u;
+        if (is_val) {
+            const uint32_t *hi = ehi, *lo = elo;
+            const int F = FV;
+            const K1Out &out = vout;
+        for (int64_t pr = p_first; pr < npairs; pr += p_step) {
+            const int64_t idx = 2 * pr + h;
+            const bool has = idx < n;
+            int64_t s = 0, beg = 0, end = 0;
+            if (has) {
+                s = order != nullptr ? (int64_t)order[idx] : idx;
+                beg = offsets[s];
+                end = offsets[s + 1];
+            }
+            const int64_t len64 = end - beg;
+            const int len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
+            uint32_t tk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tk[q] = 0;
+            if (len > (int)K16_MASK + 1) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int f = (c << 7) + l + 16 * q;
+                    if (f < F) tk[q] = resolve_tie(hi, lo, f, tokens, beg, end);
+                }
+            } else if (len > 0) {
+                // f[2r] / f[2r+1]: first keys of the high / low function of
+                // register r; g[..]: last keys
+                uint32_t fk[8], gk[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) fk[q] = gk[q] = 0xFFFFFFFFu;
+                for (int base = 0; base < len; base += 16) {
+                    const int cnt = len - base < 16 ? len - base : 16;
+                    const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
+                    int j = 0;
+#pragma unroll 2
+                    for (; j + 1 < cnt; j += 2) {
+                        const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                        const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
+                        const uint4 ha = key_oct<L>(ta, lane_base);
+                        const uint4 hb = key_oct<L>(tb, lane_base);
+                        const uint32_t pa = (uint32_t)(base + j), pb = pa + 1;
+                        const uint32_t qa = K16_MASK - pa, qb = qa - 1;
+                        const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w}, xb[4] = {hb.x, hb.y, hb.z, hb.w};
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const uint32_t ma = xa[r] & 0xFFFF0000u, mb = xb[r] & 0xFFFF0000u;
+                            fk[2 * r] = __vimin3_u32(fk[2 * r], ma | pa, mb | pb);
+                            gk[2 * r] = __vimin3_u32(gk[2 * r], ma | qa, mb | qb);
+                            fk[2 * r + 1] = __vimin3_u32(fk[2 * r + 1], imad16(xa[r], pa), imad16(xb[r], pb));
+                            gk[2 * r + 1] = __vimin3_u32(gk[2 * r + 1], imad16(xa[r], qa), imad16(xb[r], qb));
+                        }
+                    }
+                    if (j < cnt) {
+                        const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                        const uint4 ha = key_oct<L>(ta, lane_base);
+                        const uint32_t pa = (uint32_t)(base + j), qa = K16_MASK - pa;
+                        const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w};
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const uint32_t ma = xa[r] & 0xFFFF0000u;
+                            fk[2 * r] = min(fk[2 * r], ma | pa);
+                            gk[2 * r] = min(gk[2 * r], ma | qa);
+                            fk[2 * r + 1] = min(fk[2 * r + 1], imad16(xa[r], pa));
+                            gk[2 * r + 1] = min(gk[2 * r + 1], imad16(xa[r], qa));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    // slot q = 2r (+1): function l + 32r (+16) of this chunk
+                    const int r = q >> 1;
+                    const int f = (c << 7) + l + 32 * r + 16 * (q & 1);
+                    tk[q] = __ldg(tokens + beg + (fk[q] & K16_MASK));
+                    const bool tie = (fk[q] & K16_MASK) != K16_MASK - (gk[q] & K16_MASK);
+                    unsigned tied = __ballot_sync(hmask, tie && f < F);
+                    while (tied) {
+                        const int src = __ffs(tied) - 1;
+                        tied &= tied - 1;
+                        const int fs = __shfl_sync(hmask, f, src);
+                        const uint32_t m16 = __shfl_sync(hmask, fk[q] >> 16, src);
+                        const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * r;
+                        const uint32_t tb = half_resolve16(hi, lo, fs, m16, col, (q & 1) ? 0 : 16, tokens, beg, len,
+                                                           l, hmask, L);
+                        if (lane == src) tk[q] = tb;
+                    }
+                }
+            }
+            const int64_t row = out.row0 + s;
+            if (has) {
+                for (int d = 0; d < out.n; ++d) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int f = (c << 7) + l + 32 * (q >> 1) + 16 * (q & 1);
+                        if (f < F) out.values[d][row * F + f] = tk[q];
+                    }
+                }
+            }
+        }
+        } else {
+            const uint32_t *hi = shi, *lo = slo;
+            const int F = FS;
+            const int words32 = FS >> 5;
+            const K1Out &out = sout;
+        for (int64_t pr = p_first; pr < npairs; pr += p_step) {
+            const int64_t idx = 2 * pr + h;
+            const bool has = idx < n;
+            int64_t s = 0, beg = 0, end = 0;
+            if (has) {
+                s = order != nullptr ? (int64_t)order[idx] : idx;
+                beg = offsets[s];
+                end = offsets[s + 1];
+            }
+            const int64_t len64 = end - beg;
+            const int len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
+            // m1[r]: min of the (h15 << 1 | bit) keys of functions
+            // (l + 32r, l + 32r + 16) in the high / low halves; m1x[r]: min of
+            // the keys with the bit inverted.  Among the tokens of minimal
+            // h15, both bits occur iff m1 == m1x (both are (h15min, 0));
+            // otherwise they all carry m1's bit and any tie on h15 is harmless.
+            uint32_t m1[4], m1x[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) m1[r] = m1x[r] = 0xFFFFFFFFu;
+            for (int base = 0; base < len; base += 16) {
+                const int cnt = len - base < 16 ? len - base : 16;
+                const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
+                int j = 0;
+#pragma unroll 2
+                for (; j + 1 < cnt; j += 2) {
+                    const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                    const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
+                    const uint4 ha = key_oct<L>(ta, lane_base);
+                    const uint4 hb = key_oct<L>(tb, lane_base);
+                    const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w}, xb[4] = {hb.x, hb.y, hb.z, hb.w};
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        m1[r] = __vimin3_u16x2(m1[r], xa[r], xb[r]);
+                        m1x[r] = __vimin3_u16x2(m1x[r], xa[r] ^ 0x00010001u, xb[r] ^ 0x00010001u);
+                    }
+                }
+                if (j < cnt) {
+                    const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                    const uint4 ha = key_oct<L>(ta, lane_base);
+                    const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w};
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        m1[r] = vmin16x2(m1[r], xa[r]);
+                        m1x[r] = vmin16x2(m1x[r], xa[r] ^ 0x00010001u);
+                    }
+                }
+            }
+            // bits: q = 2j (high half) and 2j+1 (low half) of register j
+            uint32_t bits = 0;  // bit q = sketch bit of function l + 16q
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t a1 = m1[j] >> 16, ax = m1x[j] >> 16, b1 = m1[j] & 0xFFFFu, bx = m1x[j] & 0xFFFFu;
+                bits |= (a1 & 1u) << (2 * j);
+                bits |= (b1 & 1u) << (2 * j + 1);
+                const int fa = (c << 7) + l + 32 * j, fb = fa + 16;
+                const bool tie_a = len > 1 && fa < F && a1 == ax;
+                const bool tie_b = len > 1 && fb < F && b1 == bx;
+                unsigned tied = __ballot_sync(hmask, tie_a);
+                while (tied) {
+                    const int src = __ffs(tied) - 1;
+                    tied &= tied - 1;
+                    const int f = __shfl_sync(hmask, fa, src);
+                    const uint32_t m15 = __shfl_sync(hmask, a1 >> 1, src);
+                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
+                    const uint32_t tw = half_resolve15<L>(hi, lo, f, m15, col, 16, tokens, beg, len, l, hmask);
+                    if (lane == src) bits = (bits & ~(1u << (2 * j))) | (sketch_bit_g(bitmask, f, tw) << (2 * j));
+                }
+                tied = __ballot_sync(hmask, tie_b);
+                while (tied) {
+                    const int src = __ffs(tied) - 1;
+                    tied &= tied - 1;
+                    const int f = __shfl_sync(hmask, fb, src);
+                    const uint32_t m15 = __shfl_sync(hmask, b1 >> 1, src);
+                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
+                    const uint32_t tw = half_resolve15<L>(hi, lo, f, m15, col, 0, tokens, beg, len, l, hmask);
+                    if (lane == src)
+                        bits = (bits & ~(1u << (2 * j + 1))) | (sketch_bit_g(bitmask, f, tw) << (2 * j + 1));
+                }
+            }
+            if (len <= 0) bits = 0;
+            __syncwarp();
+            uint32_t bq[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) bq[q] = __ballot_sync(0xffffffffu, (bits >> q) & 1u);
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                w[k] = h == 0 ? (bq[2 * k] & 0xFFFFu) | (bq[2 * k + 1] << 16)
+                              : (bq[2 * k] >> 16) | (bq[2 * k + 1] & 0xFFFF0000u);
+            const int64_t row = out.row0 + s;
+            if (has && l < 4 && (c << 2) + l < words32) {
+                const uint32_t mine_w = l == 0 ? w[0] : l == 1 ? w[1] : l == 2 ? w[2] : w[3];
+                for (int d = 0; d < out.n; ++d)
+                    reinterpret_cast<uint32_t *>(out.sketch[d])[row * words32 + (c << 2) + l] = mine_w;
+            }
+        }
+        }
+    }
+    if (vout.n > 1) __threadfence_system();
+}
+
 // length-bucketed visiting order of the half-warp kernels: a counting sort
 // of the sets by min(|x|, 1023), longest first (the last, partial round of
 // the grid-stride loop gets the shortest sets); the order within a bucket
@@ -993,6 +1236,24 @@ static DevBuf<int32_t> length_order(cpsj_ctx *ctx, const int64_t *off, int64_t n
         ctx->launches += 3;
     }
     return order;
+}
+
+template <int L>
+static void launch_embed_h8(cpsj_ctx *ctx, const cpsj_family *efam, const cpsj_family *sfam, const uint32_t *tok,
+                            const int64_t *off, int64_t n, const K1Out &vout, const K1Out &sout,
+                            cudaStream_t stream) {
+    const int smem = L * 256 * 16 * 16 + 16;
+    CPSJ_CUDA(cudaFuncSetAttribute(k_embed_h8<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ProfScope prof(ctx, PROF_K1, stream);
+    DevBuf<int32_t> order = length_order(ctx, off, n, stream);
+    const int64_t want = ((n + 1) / 2 + K1H_WARPS - 1) / K1H_WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
+    k_embed_h8<L><<<grid, K1H_THREADS, smem, stream>>>(
+        tok, off, n, order.p, efam->d_hi, efam->d_lo, reinterpret_cast<const uint4 *>(efam->d_vimg[L - 1]), efam->F,
+        sfam->d_hi, sfam->d_lo, sfam->d_bitmask, reinterpret_cast<const uint4 *>(sfam->d_simg[L - 1]), sfam->F, vout,
+        sout);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches++;
 }
 
 template <int L>
@@ -1128,6 +1389,35 @@ void minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t 
         case 3: launch_minhash_k16<3>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
         default: launch_minhash<4>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
     }
+}
+
+// values (embedding family) and sketches (sketch family) of the same CSR in
+// one launch when both fit the half-warp kernels, else two launches
+void minhash_embed(cpsj_ctx *ctx, const cpsj_family *efam, const cpsj_family *sfam, const uint32_t *d_tokens,
+                   const int64_t *d_offsets, int64_t n, uint32_t max_token, uint32_t *d_values, uint64_t *d_sketch,
+                   cudaStream_t stream) {
+    require(efam != nullptr && sfam != nullptr, "family is null");
+    require(n >= 0, "n_sets must be non-negative");
+    require(sfam->d_bitmask != nullptr && sfam->F % 64 == 0, "sketch family needs bit tables and 64k functions");
+    K1Out vout{}, sout{};
+    vout.values[0] = d_values;
+    vout.n = 1;
+    sout.sketch[0] = d_sketch;
+    sout.n = 1;
+    if (n == 0) return;
+    const int L = max_token < (1u << 8) ? 1 : max_token < (1u << 16) ? 2 : max_token < (1u << 24) ? 3 : 4;
+    const char *nf = getenv("CPSJ_K1_NO_FUSE");  // A/B switch: two launches
+    if (L < 4 && efam->d_vimg[L - 1] != nullptr && sfam->d_simg[L - 1] != nullptr && d_values != nullptr &&
+        d_sketch != nullptr && !(nf && nf[0] == '1') && !getenv("CPSJ_K1_NO_H8") && !getenv("CPSJ_K1_NO_S16")) {
+        switch (L) {
+            case 1: launch_embed_h8<1>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
+            case 2: launch_embed_h8<2>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
+            default: launch_embed_h8<3>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
+        }
+        return;
+    }
+    if (d_values) minhash_sketch_multi(ctx, efam, d_tokens, d_offsets, n, max_token, vout, stream);
+    if (d_sketch) minhash_sketch_multi(ctx, sfam, d_tokens, d_offsets, n, max_token, sout, stream);
 }
 
 int minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *d_tokens,

@@ -415,11 +415,14 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
         if s1 <= s0:
             continue
         offp = d_off.data_ptr() + 8 * s0
-        ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, efam.handle, d_tok.data_ptr(), offp, s1 - s0, max_token,
-                                              d_vals.data_ptr() + 4 * t * s0, None, h))
         if sfam is not None:
-            ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, sfam.handle, d_tok.data_ptr(), offp, s1 - s0,
-                                                  max_token, None, d_sk.data_ptr() + 8 * sketch[0] * s0, h))
+            # values and sketches of the chunk in one K1 launch
+            ctx.check(ctx.lib.cpsj_minhash_embed(ctx.handle, efam.handle, sfam.handle, d_tok.data_ptr(), offp,
+                                                 s1 - s0, max_token, d_vals.data_ptr() + 4 * t * s0,
+                                                 d_sk.data_ptr() + 8 * sketch[0] * s0, h))
+        else:
+            ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, efam.handle, d_tok.data_ptr(), offp, s1 - s0,
+                                                  max_token, d_vals.data_ptr() + 4 * t * s0, None, h))
     # the copier's work is consumed on `compute`; keep the buffers alive there
     d_tok.record_stream(copier)
     d_off.record_stream(copier)
