@@ -160,6 +160,9 @@ struct cpsj_ctx {
     int64_t ing_n = 0, ing_nnz = 0;
     // pinned scratch for small device->host reads
     int64_t *h_scalars = nullptr;
+    // side stream + events: a level's leaf BruteForce overlaps its internal-node work
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t launches = 0;
 };
 

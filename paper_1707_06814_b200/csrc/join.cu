@@ -1237,6 +1237,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     DevBuf<int64_t> tiles, spairs, internal, imem, tile_off, pair_off, iscan, im_off, slists;
     DevBuf<unsigned long long> scount(SMALL_CLASSES, st);
     // leaves of <= 32 members by size class (k_leaf_small) for compile-time ell
+    const char *ovl_env = getenv("CPSJ_NO_LEAF_OVERLAP");  // A/B switch: leaves on the main stream
+    const bool overlap_leaves = !(ovl_env != nullptr && ovl_env[0] == '1');
     const char *small_env = getenv("CPSJ_NO_SMALL_LEAF");  // A/B switch: pair-packed k_leaf_pairs
     const bool small_kernel = (ell == 1 || ell == 2 || ell == 4 || ell == 8 || ell == 16) &&
                               !(small_env != nullptr && small_env[0] == '1');
@@ -1305,11 +1307,25 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         prof_plan.reset();
 
         // ---- leaves: K4 (candidates verified after sync B)
+        // the leaves run on the side stream, overlapping the internal-node
+        // kernels below; the main stream joins them before sync (B).  A
+        // regeneration (candidate buffer grown) runs on the main stream.
+        const bool any_leaf = work.tiles > 0 || work.pairs > 0 || (work.small && work.sl.wcum[SMALL_CLASSES] > 0);
+        const bool leaf_forked = any_leaf && overlap_leaves && ctx->side != nullptr;
+        cudaStream_t leaf_st = leaf_forked ? ctx->side : st;
         auto gen_leaf = [&]() {
-            if (work.tiles > 0 || work.pairs > 0 || (work.small && work.sl.wcum[SMALL_CLASSES] > 0))
-                leaf_dispatch(ctx, st, work, lv, in, plan->accept_dist, lam, em.cand.p, em.cand_cap, ctr.p);
+            if (any_leaf)
+                leaf_dispatch(ctx, leaf_st, work, lv, in, plan->accept_dist, lam, em.cand.p, em.cand_cap, ctr.p);
+            leaf_st = st;
         };
-        gen_leaf();
+        if (leaf_forked) {
+            CPSJ_CUDA(cudaEventRecord(ctx->ev_fork, st));
+            CPSJ_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            gen_leaf();
+            CPSJ_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
+        } else {
+            gen_leaf();
+        }
 
         if (n_int > 0) {
             std::unique_ptr<ProfScope> prof_node(new ProfScope(ctx, PROF_NODE, st));
@@ -1355,6 +1371,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             drv.scan_multi({nsel.p, nent.p}, {seg_off.p, e_off.p}, n_int + 1);
         }
         // ---- (B) one read: leaf candidates, flags, split entries, depth caps
+        if (leaf_forked) CPSJ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         {
             const int64_t *cand_n = reinterpret_cast<const int64_t *>(&ctr.p->cand_n);
             const int64_t *cap_n = reinterpret_cast<const int64_t *>(&ctr.p->cap_n);
