@@ -423,6 +423,10 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
         else:
             ctx.check(ctx.lib.cpsj_minhash_sketch(ctx.handle, efam.handle, d_tok.data_ptr(), offp, s1 - s0,
                                                   max_token, d_vals.data_ptr() + 4 * t * s0, None, h))
+        if trace is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(compute)
+            kev.append(e)
     # the copier's work is consumed on `compute`; keep the buffers alive there
     d_tok.record_stream(copier)
     d_off.record_stream(copier)

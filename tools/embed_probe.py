@@ -141,9 +141,10 @@ pipe()
 en.record()
 torch.cuda.synchronize()
 cop = dict(E._PIPE_TRACE)["copies"]; kst = dict(E._PIPE_TRACE)["k1"]
-print("chunk  copy_done_ms  k1_start_ms")
+print("chunk  copy_done_ms  k1_start_ms  k1_end_ms")
 for c in range(len(cop)):
-    print(c, f"{st.elapsed_time(cop[c]):8.3f}", f"{st.elapsed_time(kst[c]):8.3f}")
+    print(c, f"{st.elapsed_time(cop[c]):8.3f}", f"{st.elapsed_time(kst[2 * c]):8.3f}",
+          f"{st.elapsed_time(kst[2 * c + 1]):8.3f}")
 print("end", f"{st.elapsed_time(en):.3f}")
 E._PIPE_TRACE = None
 
@@ -157,7 +158,7 @@ en.record()
 torch.cuda.synchronize()
 cop = dict(E._PIPE_TRACE)["copies"]; kst = dict(E._PIPE_TRACE)["k1"]
 for c in range(len(cop)):
-    print("serial", c, f"{st.elapsed_time(cop[c]):8.3f}", f"{st.elapsed_time(kst[c]):8.3f}")
+    print("serial", c, f"{st.elapsed_time(cop[c]):8.3f}", f"{st.elapsed_time(kst[2 * c]):8.3f}")
 print("serial end", f"{st.elapsed_time(en):.3f}")
 E._PIPE_TRACE = None
 E._PIPE_SERIAL = False
