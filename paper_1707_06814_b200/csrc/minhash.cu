@@ -11,19 +11,23 @@
 //
 // Design.  The work is Sum|x| * F hash evaluations; every evaluation is
 // L table lookups (L = key bytes that vary, chosen from max_token; the
-// constant upper-byte entries are folded into table L-1).  A warp owns one
-// set and its lanes own the functions of the current chunk, so one token
-// (broadcast by SHFL) is hashed by every function of the chunk at once.
-//   k_minhash_k16<L> (L <= 3, the production kernel): 128 functions per
-//     chunk, the top 16 hash bits of 4 functions per lane in one LDS.64,
-//     keys (hash16 << 16 | position) with first/last tie detection and a
-//     warp-cooperative 64-bit resolution of 16-bit ties; tables arrive by
-//     TMA bulk copy from prebuilt images.  Integer-ALU bound (ncu ALU pipe
-//     ~81%); two further variants were measured and rejected (keys built
-//     on the FMA pipe: -16%; PRMT-only table addresses: -1%).
-//   k_minhash<L> (L = 4, tokens >= 2^24, and the CPSJ_K1_NARROW A/B
-//     switch): 32 functions per chunk on the high hash word.
-// HBM traffic is the token stream once per chunk.
+// constant upper-byte entries are folded into table L-1).  Per
+// 128-function chunk a CTA copies the chunk's prebuilt shared-memory image
+// (L x 64 KiB of 16-bit entries) by TMA bulk copy; tokens are broadcast by
+// SHFL so one token is hashed by every function of the chunk at once.
+// Production kernels (L <= 3; half-warp per set, 8 functions per lane, one
+// LDS.128 per key byte, sets visited in a length-bucketed order):
+//   k_sketch_s16<L>: sketches.  Entries carry (top 15 hash bits << 1 |
+//     sketch bit), the minimum key carries the argmin's sketch bit, two
+//     functions per register with VIMNMX3.U16x2; shared-memory bound.
+//   k_values_h8<L>: values.  Position keys (hash16 << 16 | position),
+//     first/last tie detection, pairwise VIMNMX3; integer-ALU bound.
+//   k_embed_h8<L>: both in one launch (the pipelined embed's chunks).
+// Ties on the compared bits are re-resolved on the full 64-bit hash, so
+// every output is bit-exact.  Also kept: k_minhash_k16<L> (full warp per
+// set, 4 functions per lane; values+sketch in one call, A/B reference) and
+// k_minhash<L> (L = 4, tokens >= 2^24: 32 functions per chunk on the high
+// hash word).  HBM traffic is the token stream once per chunk.
 #include <cuda_runtime.h>
 
 #include <algorithm>
