@@ -614,7 +614,10 @@ def run_ours(args, rank: int, world: int):
                      "frac": achieved / float(peaks["hbm_gbs"]), "traffic": ncu_traffic(args.config, "sketch"),
                      "kernel": "k_sketch_s16<L> sketch launch (K1, 64*ell functions)",
                      "algorithmic_bytes": sk_bytes, "avg_launch_ms": k1_sk_ms,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
+                     "note": "the dominant kernel is bound by shared-memory table lookups, not HBM: "
+                             "roofline_smem.frac is its bound; HBM bytes are the CSR read + sketch write "
+                             "(traffic = the token stream re-read once per 128-function chunk)"},
         "roofline_smem": {"bound": "shared-memory lookups (16-bit entries, 126 B/clk/SM measured LDS rate)",
                           "achieved_evals_per_s": evals / (k1_sk_ms / 1e3), "peak_evals_per_s": lookup_peak,
                           "frac": evals / (k1_sk_ms / 1e3) / lookup_peak, "key_bytes": L,
