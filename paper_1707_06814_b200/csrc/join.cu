@@ -636,11 +636,12 @@ __global__ void k_select(int64_t n_int, const int64_t *__restrict__ ilist, const
 // split_buckets: position ascending, value ascending, members ascending.
 // vbits = bits of the largest value (from the token universe), so the radix
 // sort only runs over vbits + bits(#segments) key bits.
+template <typename KT>
 __global__ void k_build_keys(int64_t E, const int64_t *__restrict__ e_off, int64_t n_int,
                              const int64_t *__restrict__ seg_off, const int64_t *__restrict__ nsel,
                              const int64_t *__restrict__ im_off, const int64_t *__restrict__ fscan,
                              const int16_t *__restrict__ sel_pos, int t, const int32_t *__restrict__ surv,
-                             const uint32_t *__restrict__ values, int vbits, uint64_t *__restrict__ keys,
+                             const uint32_t *__restrict__ values, int vbits, KT *__restrict__ keys,
                              int32_t *__restrict__ vals) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
@@ -650,11 +651,12 @@ __global__ void k_build_keys(int64_t E, const int64_t *__restrict__ e_off, int64
     const int64_t r = local / s, p = local - r * s;
     const int pos = sel_pos[k * t + r];
     const int32_t x = surv[(im_off[k] - fscan[im_off[k]]) + p];
-    keys[e] = ((uint64_t)(seg_off[k] + r) << vbits) | values[(size_t)x * t + pos];
+    keys[e] = (KT)(((uint64_t)(seg_off[k] + r) << vbits) | values[(size_t)x * t + pos]);
     vals[e] = x;
 }
 
-__global__ void k_heads(int64_t E, const uint64_t *__restrict__ keys, int64_t *__restrict__ head) {
+template <typename KT>
+__global__ void k_heads(int64_t E, const KT *__restrict__ keys, int64_t *__restrict__ head) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < E) head[e] = (e == 0 || keys[e] != keys[e - 1]) ? 1 : 0;
     else if (e == E) head[e] = 0;
@@ -686,10 +688,11 @@ __global__ void k_group_keep(const int64_t *__restrict__ Gp, int64_t E, const in
 
 // child node records: seed = word(parent seed, t + 64 ell + j) for the
 // parent's j-th child (cps:286,301); S for the DFS-peak replay
+template <typename KT>
 __global__ void k_children(const int64_t *__restrict__ Gp, int64_t E, const int64_t *__restrict__ gstart,
                            const int64_t *__restrict__ keep, const int64_t *__restrict__ kscan,
                            const int64_t *__restrict__ mscan, const int64_t *__restrict__ hscan,
-                           const uint64_t *__restrict__ keys, const int64_t *__restrict__ seg_off,
+                           const KT *__restrict__ keys, const int64_t *__restrict__ seg_off,
                            int64_t n_int, const int64_t *__restrict__ e_off,
                            const int64_t *__restrict__ ilist, const uint64_t *__restrict__ nd_seed,
                            const int64_t *__restrict__ nd_S, uint64_t child_off,
@@ -702,7 +705,7 @@ __global__ void k_children(const int64_t *__restrict__ Gp, int64_t E, const int6
     if (g < G && keep[g]) {
         const int64_t st = gstart[g];
         const int64_t sz = (g + 1 < G ? gstart[g + 1] : E) - st;
-        const int64_t seg = (int64_t)(keys[st] >> vbits);
+        const int64_t seg = (int64_t)((uint64_t)keys[st] >> vbits);
         const int64_t k = upper_bound_i64(seg_off, n_int + 1, seg) - 1;
         const int64_t node = ilist[k];
         const int64_t g0 = hscan[e_off[k]];  // parent's first group
@@ -1060,7 +1063,7 @@ void count_table_flags(cpsj_ctx *ctx, Driver &drv, const cpsj_inputs *in, const 
                                               st));
     ctx->lib_calls++;
     DevBuf<int64_t> head(EN + 1, st), hscan(EN + 1, st), gstart(EN, st);
-    k_heads<<<blocks_for(EN + 1), TPB, 0, st>>>(EN, keys2.p, head.p);
+    k_heads<uint64_t><<<blocks_for(EN + 1), TPB, 0, st>>>(EN, keys2.p, head.p);
     CPSJ_LAUNCH_CHECK();
     drv.scan(head.p, hscan.p, EN + 1);
     k_group_start<<<blocks_for(EN), TPB, 0, st>>>(EN, head.p, hscan.p, gstart.p);
@@ -1412,26 +1415,44 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         }
 
         // ---- split, part 2: stable group-by (K3)
+        bool keys32 = false;
         if (E > 0) {
             ProfScope prof_split(ctx, PROF_SPLIT, st);
             keys.ensure(E, st);
             keys2.ensure(E, st);
             vals.ensure(E, st);
             vals2.ensure(E, st);
-            k_build_keys<<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p, im_off_c.p, fscan.p,
-                                                        sel_pos.p, t, surv.p, in->d_values, vbits, keys.p, vals.p);
-            CPSJ_LAUNCH_CHECK();
             int end_bit = vbits;
             while (end_bit < 64 && ((uint64_t)n_seg >> (end_bit - vbits)) > 0) ++end_bit;
+            // (segment, value) keys: 32-bit when they fit (half the sort traffic)
+            keys32 = end_bit <= 32;
+            uint32_t *k32 = reinterpret_cast<uint32_t *>(keys.p), *k32b = reinterpret_cast<uint32_t *>(keys2.p);
+            if (keys32)
+                k_build_keys<uint32_t><<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p,
+                                                                      im_off_c.p, fscan.p, sel_pos.p, t, surv.p,
+                                                                      in->d_values, vbits, k32, vals.p);
+            else
+                k_build_keys<uint64_t><<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p,
+                                                                      im_off_c.p, fscan.p, sel_pos.p, t, surv.p,
+                                                                      in->d_values, vbits, keys.p, vals.p);
+            CPSJ_LAUNCH_CHECK();
             size_t bytes = 0;
-            CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0, end_bit,
-                                                      st));
+            if (keys32)
+                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k32, k32b, vals.p, vals2.p, E, 0, end_bit, st));
+            else
+                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0,
+                                                          end_bit, st));
             if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
-            CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0,
-                                                      end_bit, st));
+            if (keys32)
+                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, k32, k32b, vals.p, vals2.p, E, 0,
+                                                          end_bit, st));
+            else
+                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
+                                                          0, end_bit, st));
             ctx->lib_calls++;
             for (DevBuf<int64_t> *b : {&head, &hscan, &gstart, &keep, &ksize, &kscan, &mscan}) b->ensure(E + 1, st);
-            k_heads<<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
+            if (keys32) k_heads<uint32_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, k32b, head.p);
+            else k_heads<uint64_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
             CPSJ_LAUNCH_CHECK();
             drv.scan_multi({head.p}, {hscan.p}, E + 1);
             k_group_start<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p);
@@ -1459,10 +1480,15 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             nx.seed.ensure(nx.N, st);
             nx.S.ensure(nx.N, st);
             nx.members.ensure(nx.M, st);
-            k_children<<<blocks_for(E), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p,
-                                                      keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p, lv.S.p,
-                                                      child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, vbits,
-                                                      ctr.p);
+            if (keys32)
+                k_children<uint32_t><<<blocks_for(E), TPB, 0, st>>>(
+                    hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p,
+                    reinterpret_cast<const uint32_t *>(keys2.p), seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p,
+                    lv.S.p, child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, vbits, ctr.p);
+            else
+                k_children<uint64_t><<<blocks_for(E), TPB, 0, st>>>(
+                    hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p, keys2.p, seg_off.p, n_int, e_off.p,
+                    ilist.p, lv.seed.p, lv.S.p, child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, vbits, ctr.p);
             CPSJ_LAUNCH_CHECK();
             k_scatter_children<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p, keep.p, mscan.p, vals2.p,
                                                               nx.members.p);
@@ -1597,7 +1623,7 @@ void lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_plan *plan, c
             vals.release();
             DevBuf<int64_t> head(E + 1, st), hscan(E + 1, st), gstart(E, st), keep(E + 1, st), ksize(E + 1, st),
                 kscan(E + 1, st), mscan(E + 1, st);
-            k_heads<<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
+            k_heads<uint64_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
             CPSJ_LAUNCH_CHECK();
             drv.scan(head.p, hscan.p, E + 1);
             k_group_start<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p);
