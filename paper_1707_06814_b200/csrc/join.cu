@@ -303,27 +303,51 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
             for (int k = 0; k < EK; ++k) rs2[wb][lane][k] = lane < nrows ? __ldg(sketch + (size_t)r * EK + k) : 0ull;
             __syncwarp();
         }
-        for (int i = 0; i < nrows; ++i) {
-            const uint64_t *rs = rs2[wb][i];
-            int dist = 0;
+        // two rows per iteration: independent popcount chains for the
+        // scheduler to interleave (the early exits test both rows at once)
+        for (int i = 0; i < nrows; i += 2) {
+            const bool two = i + 1 < nrows;
+            const uint64_t *ra = rs2[wb][i], *rb = rs2[wb][two ? i + 1 : i];
+            int da = 0, db = 0;
             if (EK >= 8) {
                 constexpr int C1 = EK * 5 / 8, C2 = EK * 6 / 8;
 #pragma unroll
-                for (int k = 0; k < C1; ++k) dist += __popcll(rs[k] ^ cw.w[k]);
-                if (!__any_sync(0xffffffffu, dist <= accept)) continue;
+                for (int k = 0; k < C1; ++k) {
+                    da += __popcll(ra[k] ^ cw.w[k]);
+                    db += __popcll(rb[k] ^ cw.w[k]);
+                }
+                if (!__any_sync(0xffffffffu, da <= accept || (two && db <= accept))) continue;
 #pragma unroll
-                for (int k = C1; k < C2; ++k) dist += __popcll(rs[k] ^ cw.w[k]);
-                if (!__any_sync(0xffffffffu, dist <= accept)) continue;
+                for (int k = C1; k < C2; ++k) {
+                    da += __popcll(ra[k] ^ cw.w[k]);
+                    db += __popcll(rb[k] ^ cw.w[k]);
+                }
+                if (!__any_sync(0xffffffffu, da <= accept || (two && db <= accept))) continue;
 #pragma unroll
-                for (int k = C2; k < EK; ++k) dist += __popcll(rs[k] ^ cw.w[k]);
+                for (int k = C2; k < EK; ++k) {
+                    da += __popcll(ra[k] ^ cw.w[k]);
+                    db += __popcll(rb[k] ^ cw.w[k]);
+                }
             } else {
 #pragma unroll
-                for (int k = 0; k < EK; ++k) dist += __popcll(rs[k] ^ cw.w[k]);
+                for (int k = 0; k < EK; ++k) {
+                    da += __popcll(ra[k] ^ cw.w[k]);
+                    db += __popcll(rb[k] ^ cw.w[k]);
+                }
             }
-            const int32_t row = rid2[wb][i];
-            bool pass = dist <= accept;
-            if (pass) pass = size_filter(rsz2[wb][i], colsz, lam) && (side == nullptr || side[row] != side[colx]);
-            emit_pair(pass, row, colx, cand, cap, ctr);
+            {
+                const int32_t row = rid2[wb][i];
+                bool pass = da <= accept;
+                if (pass) pass = size_filter(rsz2[wb][i], colsz, lam) && (side == nullptr || side[row] != side[colx]);
+                emit_pair(pass, row, colx, cand, cap, ctr);
+            }
+            if (two) {
+                const int32_t row = rid2[wb][i + 1];
+                bool pass = db <= accept;
+                if (pass)
+                    pass = size_filter(rsz2[wb][i + 1], colsz, lam) && (side == nullptr || side[row] != side[colx]);
+                emit_pair(pass, row, colx, cand, cap, ctr);
+            }
         }
         return;
     }
