@@ -51,6 +51,11 @@ struct DevCounters {
     long long peak;              // peak_live_members
     unsigned long long cap_n;    // depth-cap events
     int err;                     // CPSJ_E_PICK
+    int max_depth;               // deepest node created by k_subtree
+    int overflow;                // k_subtree ran out of scratch: relaunch larger
+    unsigned long long leaf_n;   // leaves emitted by k_subtree
+    unsigned long long leaf_m;   // their members
+    long long lvl_max_int;       // largest internal node of the current level
 };
 
 inline unsigned blocks_for(int64_t n, int tpb = TPB) {
@@ -103,6 +108,7 @@ __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit
         internal[i] = leaf ? 0 : 1;
         imem[i] = leaf ? 0 : m;
         if (leaf) pre = (unsigned long long)pairs;
+        else atomicMax(&ctr->lvl_max_int, (long long)m);
     } else if (i == N) {
         tiles[i] = 0;
         spairs[i] = 0;
@@ -807,6 +813,431 @@ __global__ void k_gather8(Gather8 g, int cnt, int64_t *__restrict__ out) {
     if (i < cnt) out[i] = *g.p[i];
 }
 
+// ----------------------------------------------- K7 subtree (CTA per node)
+//
+// Every internal node of <= 8192 members, and everything below it, is
+// processed by k_subtree instead of the level kernels: persistent CTAs pull
+// nodes from a global work queue; a node's members live in shared memory
+// where the node sketch, the flag rule, the point comparisons of flagged
+// members, the survivors, the position selection and the stable split
+// (radix sort of (value, survivor index) items) run; each child is either
+// a leaf -- appended to a global leaf list that the K4 leaf kernels process
+// in bulk afterwards -- or an internal node pushed back on the queue
+// (members in a global bump arena).  Nodes of any depth are independent
+// (SURVEY.md section 3), so the queue keeps every SM busy without level
+// barriers; `pending` counts queued + running nodes and the kernel ends
+// when it drops to zero.  Semantics are exactly those of the level kernels
+// (same seeds, counters, child order j and peak replay S).  Exhausted
+// scratch sets `overflow`; the host restores the counters and relaunches
+// with twice the scratch.
+constexpr int ST_THREADS = 512;
+constexpr int ST_WARPS = ST_THREADS / 32;
+constexpr int ST_MAX_SEL = 256;  // selected positions of one node (t <= 256)
+constexpr int ST_MAX_SUBM = 8192;  // largest node a CTA holds
+
+struct StNode {
+    int64_t S;
+    uint64_t seed;
+    int64_t off;  // >= 0: arena offset; < 0: level member array at -off - 1
+    int32_t cnt, depth;
+    int32_t ready, pad;
+};
+
+struct StQueue {
+    unsigned long long head, tail, arena_top;
+    unsigned long long pending;
+};
+
+struct SubtreeArgs {
+    const int32_t *members;  // the level's member array (roots)
+    const uint64_t *sketch;
+    int ell, t;
+    const uint32_t *values;
+    int vbits;
+    const int32_t *sizes;
+    const int8_t *side;
+    int32_t limit, depth_cap, accept, flag_dist;
+    double split_p, lam;
+    uint64_t child_off;
+    int2 *cand;
+    unsigned long long cand_cap;
+    StNode *q;
+    int64_t q_cap;
+    int32_t *arena;
+    int64_t arena_cap;
+    int32_t *leaf_mem;
+    int64_t leaf_mem_cap;
+    int64_t *leaf_off;
+    int32_t *leaf_cnt;
+    int64_t leaf_cap;
+    int64_t *cap_sizes;
+    int64_t cap_cap;
+    StQueue *qs;
+    DevCounters *ctr;
+    int subm;  // power of two >= the largest root
+};
+
+__global__ void k_subtree_init(int64_t n_roots, const int64_t *__restrict__ slist,
+                               const int64_t *__restrict__ nd_off, const int32_t *__restrict__ nd_cnt,
+                               const uint64_t *__restrict__ nd_seed, const int64_t *__restrict__ nd_S, int32_t depth,
+                               StNode *__restrict__ q, StQueue *qs) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n_roots) {
+        const int64_t node = slist[r];
+        StNode c;
+        c.S = nd_S[node];
+        c.seed = nd_seed[node];
+        c.off = -nd_off[node] - 1;
+        c.cnt = nd_cnt[node];
+        c.depth = depth;
+        c.ready = 1;
+        c.pad = 0;
+        q[r] = c;
+    }
+    if (r == 0) {
+        qs->head = 0;
+        qs->tail = (unsigned long long)n_roots;
+        qs->arena_top = 0;
+        qs->pending = (unsigned long long)n_roots;
+    }
+}
+
+// in-place exclusive scan of a[0..n) by the whole CTA; returns the total to
+// every thread.  `wsum` is 32 ints of shared scratch.
+__device__ int block_excl_scan(int *a, int n, int *wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (n + ST_THREADS - 1) / ST_THREADS;
+    const int b = min(n, tid * per), e = min(n, b + per);
+    int local = 0;
+    for (int i = b; i < e; ++i) local += a[i];
+    int incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int v = lane < ST_WARPS ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane < ST_WARPS) wsum[lane] = v;  // inclusive warp totals
+    }
+    __syncthreads();
+    int run = (wid > 0 ? wsum[wid - 1] : 0) + incl - local;
+    const int total = wsum[ST_WARPS - 1];
+    for (int i = b; i < e; ++i) {
+        const int v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    __syncthreads();
+    return total;
+}
+
+// Stable LSB radix sort (8-bit digits) of n (value, index) items by the
+// low `bits` bits of value, in shared memory: warp w owns the contiguous
+// items [w n/16, (w+1) n/16); per pass a (digit, warp) histogram, one scan,
+// and an in-order scatter where __match_any_sync ranks the lanes sharing a
+// digit.  Items start in (va, ia); returns true when the result ended in
+// (vb, ib).  `hist` holds 256 * ST_WARPS ints.
+__device__ bool block_radix_sort(uint32_t *va, uint16_t *ia, uint32_t *vb, uint16_t *ib, int n, int bits, int *hist,
+                                 int *wsum) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int wn = (n + ST_WARPS - 1) / ST_WARPS;
+    const int beg = min(n, wid * wn), end = min(n, beg + wn);
+    bool flip = false;
+    for (int shift = 0; shift < bits; shift += 8) {
+        for (int d = lane; d < 256; d += 32) hist[d * ST_WARPS + wid] = 0;
+        __syncwarp();
+        for (int i = beg + lane; i < end; i += 32) atomicAdd(&hist[((va[i] >> shift) & 255) * ST_WARPS + wid], 1);
+        __syncthreads();
+        block_excl_scan(hist, 256 * ST_WARPS, wsum);
+        for (int base = beg; base < end; base += 32) {
+            const int i = base + lane;
+            const bool valid = i < end;
+            const uint32_t v = valid ? va[i] : 0u;
+            const int d = valid ? (int)((v >> shift) & 255) : 256 + lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            const int rank = __popc(peers & ((1u << lane) - 1));
+            if (valid) {
+                const int dst = hist[d * ST_WARPS + wid] + rank;
+                vb[dst] = v;
+                ib[dst] = ia[i];
+            }
+            __syncwarp();
+            if (valid && rank == 0) hist[d * ST_WARPS + wid] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        uint32_t *tv = va; va = vb; vb = tv;
+        uint16_t *ti = ia; ia = ib; ib = ti;
+        flip = !flip;
+    }
+    return flip;
+}
+
+__global__ void __launch_bounds__(ST_THREADS, 1) k_subtree(const SubtreeArgs a) {
+    extern __shared__ __align__(16) unsigned char st_smem[];
+    const int subm = a.subm;
+    // [subm] sorted values + [subm] survivor indices (the point phase keeps
+    // its flagged list in the values); mem + fsc double as the radix sort's
+    // second buffer, lsc as its histograms
+    uint32_t *sval = reinterpret_cast<uint32_t *>(st_smem);
+    int32_t *mem = reinterpret_cast<int32_t *>(sval + subm);    // [subm + 2] members, then group starts
+    int32_t *fsc = mem + subm + 2;                              // [subm + 2] scans
+    int32_t *lsc = fsc + subm + 2;                              // [max(subm + 2, 4096)] leaf scans
+    int32_t *surv = lsc + max(subm + 2, 256 * ST_WARPS);        // [subm] survivors
+    uint16_t *sidx = reinterpret_cast<uint16_t *>(surv + subm); // [subm]
+    uint32_t *tval = reinterpret_cast<uint32_t *>(mem);         // radix sort buffer B
+    uint16_t *tidx = reinterpret_cast<uint16_t *>(fsc);
+    __shared__ StNode cur;
+    __shared__ int done, nsel;
+    __shared__ int wsum[32];
+    __shared__ uint32_t nsk32[64];  // node sketch, ell <= 32
+    __shared__ int16_t selpos[ST_MAX_SEL];
+    __shared__ uint32_t selmask[ST_MAX_SEL / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int ell = a.ell, t = a.t, mbits = 64 * ell;
+    DevCounters *ctr = a.ctr;
+    StQueue *qs = a.qs;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            // claim the next queue slot; wait until it is published or no
+            // node is queued or running any more
+            const unsigned long long h = atomicAdd(&qs->head, 1ull);
+            done = 1;
+            for (;;) {
+                if (*(volatile int *)&ctr->overflow) break;
+                if ((int64_t)h < a.q_cap && *(volatile int *)&a.q[h].ready) {
+                    __threadfence();
+                    cur.S = __ldcg(&a.q[h].S);
+                    cur.seed = __ldcg(&a.q[h].seed);
+                    cur.off = __ldcg(&a.q[h].off);
+                    cur.cnt = __ldcg(&a.q[h].cnt);
+                    cur.depth = __ldcg(&a.q[h].depth);
+                    done = 0;
+                    break;
+                }
+                if (*(volatile unsigned long long *)&qs->pending == 0) break;
+                __nanosleep(256);
+            }
+        }
+        __syncthreads();
+        if (done) break;
+        const int m = cur.cnt;
+        const uint64_t seed = cur.seed;
+        const int depth = cur.depth;
+        const int64_t S0 = cur.S;
+        if (cur.off < 0) {
+            const int32_t *src = a.members + (-cur.off - 1);
+            for (int e = tid; e < m; e += ST_THREADS) mem[e] = src[e];
+        } else {
+            const int32_t *src = a.arena + cur.off;
+            for (int e = tid; e < m; e += ST_THREADS) mem[e] = __ldcg(src + e);
+        }
+        // node sketch (cps:182-198): bit i of member floor(u_i m)
+        for (int i0 = 0; i0 < mbits; i0 += ST_THREADS) {
+            const int i = i0 + tid;
+            __syncthreads();
+            uint32_t bit = 0;
+            if (i < mbits) {
+                const double u = stream_uniform(seed, (uint64_t)t + (uint64_t)i);
+                long long idx = (long long)__dmul_rn(u, (double)m);
+                if (idx >= m) { atomicExch(&ctr->err, CPSJ_E_PICK); idx = m - 1; }
+                const int32_t pick = mem[idx];
+                bit = (uint32_t)((__ldg(a.sketch + (size_t)pick * ell + (i >> 6)) >> (i & 63)) & 1ull);
+            }
+            const uint32_t w = __ballot_sync(0xffffffffu, bit);
+            if (lane == 0 && i < mbits) nsk32[i >> 5] = w;
+        }
+        // positions with u_i < 1/(lam t) (cps:233-234), ascending (t <= 256)
+        if (tid < ST_MAX_SEL) {
+            const bool sel = tid < t && stream_uniform(seed, (uint64_t)tid) < a.split_p;
+            const uint32_t w = __ballot_sync(0xffffffffu, sel);
+            if (lane == 0) selmask[wid] = w;
+        }
+        __syncthreads();
+        // flag rule (cps:268): dist(member, node sketch) <= flag_dist
+        const uint64_t *nsk = reinterpret_cast<const uint64_t *>(nsk32);
+        for (int e = tid; e < m; e += ST_THREADS) {
+            const uint64_t *sx = a.sketch + (size_t)mem[e] * ell;
+            int dist = 0;
+            for (int w = 0; w < ell; ++w) dist += __popcll(__ldg(sx + w) ^ nsk[w]);
+            fsc[e] = dist <= a.flag_dist ? 1 : 0;
+        }
+        if (tid == 0) {
+            int c = 0;
+            for (int q = 0; q < ST_MAX_SEL / 32; ++q)
+                for (uint32_t w = selmask[q]; w; w &= w - 1) selpos[c++] = (int16_t)(32 * q + __ffs(w) - 1);
+            nsel = c;
+        }
+        __syncthreads();
+        const int nflag = block_excl_scan(fsc, m, wsum);
+        if (tid == 0) fsc[m] = nflag;
+        __syncthreads();
+        // survivors in member order; flagged positions listed in the sort buffer
+        int32_t *flist = reinterpret_cast<int32_t *>(sval);
+        for (int e = tid; e < m; e += ST_THREADS) {
+            const int f0 = fsc[e], fl = fsc[e + 1] - f0;
+            if (fl) flist[f0] = e;
+            else surv[e - f0] = mem[e];
+        }
+        __syncthreads();
+        // point comparisons (cps:159-171, 271-274): flagged member at
+        // position p with rank r vs every member but itself and the flagged
+        // members before it; pre += m - 1 - r
+        for (int f = wid; f < nflag; f += ST_WARPS) {
+            const int p = flist[f];
+            const int32_t x = mem[p];
+            if (lane == 0 && m - 1 - f > 0) atomicAdd(&ctr->pre, (unsigned long long)(m - 1 - f));
+            const uint64_t *sx = a.sketch + (size_t)x * ell;
+            const int32_t size_x = a.sizes[x];
+            for (int base = 0; base < m; base += 32) {
+                const int j = base + lane;
+                bool pass = false;
+                int32_t y = 0;
+                if (j < m) {
+                    y = mem[j];
+                    const bool removed = (fsc[j + 1] != fsc[j]) && j < p;
+                    if (y != x && !removed) {
+                        const uint64_t *sy = a.sketch + (size_t)y * ell;
+                        int dist = 0;
+                        for (int q = 0; q < ell; ++q) dist += __popcll(__ldg(sx + q) ^ __ldg(sy + q));
+                        pass = dist <= a.accept && size_filter(size_x, a.sizes[y], a.lam) &&
+                               (a.side == nullptr || a.side[x] != a.side[y]);
+                    }
+                }
+                emit_pair(pass, x, y, a.cand, a.cand_cap, ctr);
+            }
+        }
+        const int s = m - nflag;
+        bool split = s >= 2;
+        if (split && depth >= a.depth_cap) {
+            split = false;
+            if (tid == 0) {
+                const unsigned long long slot = atomicAdd(&ctr->cap_n, 1ull);
+                if ((int64_t)slot < a.cap_cap) a.cap_sizes[slot] = s;
+                else atomicExch(&ctr->overflow, 1);
+            }
+        }
+        int jbase = 0, sbase = 0;
+        bool any_child = false;
+        for (int r = 0; split && r < nsel; ++r) {
+            const int pos = selpos[r];
+            __syncthreads();  // flist / the previous position's buffers are free
+            // stable split (cps:236-244): radix sort (value, survivor index)
+            // by value; the index order of equal values is kept
+#pragma unroll 4
+            for (int e = tid; e < s; e += ST_THREADS) {
+                sval[e] = __ldg(a.values + (size_t)surv[e] * t + pos);
+                sidx[e] = (uint16_t)e;
+            }
+            __syncthreads();
+            const bool flip = block_radix_sort(sval, sidx, tval, tidx, s, a.vbits, lsc, wsum);
+            if (flip) {
+                for (int e = tid; e < s; e += ST_THREADS) {
+                    sval[e] = tval[e];
+                    sidx[e] = tidx[e];
+                }
+                __syncthreads();
+            }
+            for (int e = tid; e < s; e += ST_THREADS) fsc[e] = (e == 0 || sval[e] != sval[e - 1]) ? 1 : 0;
+            __syncthreads();
+            const int G = block_excl_scan(fsc, s, wsum);
+            for (int e = tid; e < s; e += ST_THREADS)
+                if (e == 0 || sval[e] != sval[e - 1]) mem[fsc[e]] = e;  // group starts
+            if (tid == 0) mem[G] = s;
+            __syncthreads();
+            // kept groups (>= 2 members): fsc = (child rank << 16) | member
+            // offset over all kept groups, lsc = the same over the leaves
+            for (int g = tid; g < G; g += ST_THREADS) {
+                const int sz = mem[g + 1] - mem[g];
+                fsc[g] = sz >= 2 ? (1 << 16) | sz : 0;
+                lsc[g] = (sz >= 2 && sz <= a.limit) ? (1 << 16) | sz : 0;
+            }
+            __syncthreads();
+            const int ktot = block_excl_scan(fsc, G, wsum);
+            const int ltot = block_excl_scan(lsc, G, wsum);
+            // one allocation per position: leaf records + members, queue
+            // slots + arena members for the internal children
+            __shared__ long long lbase, lmbase, qbase, abase;
+            const int kn = ktot >> 16, ks = ktot & 0xFFFF, ln = ltot >> 16, ls = ltot & 0xFFFF;
+            if (tid == 0) {
+                lbase = lmbase = qbase = abase = -1;
+                if (kn > 0) {
+                    atomicMax(&ctr->peak, (long long)(S0 + sbase + ks));  // max of S(c) + |c| is the last child's
+                    any_child = true;
+                }
+                if (ln > 0) {
+                    const long long b0 = (long long)atomicAdd(&ctr->leaf_n, (unsigned long long)ln);
+                    const long long b1 = (long long)atomicAdd(&ctr->leaf_m, (unsigned long long)ls);
+                    if (b0 + ln > a.leaf_cap || b1 + ls > a.leaf_mem_cap) atomicExch(&ctr->overflow, 1);
+                    else { lbase = b0; lmbase = b1; }
+                }
+                if (kn > ln) {
+                    const long long b0 = (long long)atomicAdd(&qs->tail, (unsigned long long)(kn - ln));
+                    const long long b1 = (long long)atomicAdd(&qs->arena_top, (unsigned long long)(ks - ls));
+                    if (b0 + (kn - ln) > a.q_cap || b1 + (ks - ls) > a.arena_cap) {
+                        atomicExch(&ctr->overflow, 1);
+                    } else {
+                        qbase = b0;
+                        abase = b1;
+                        atomicAdd(&qs->pending, (unsigned long long)(kn - ln));  // before the parent's decrement
+                    }
+                }
+            }
+            __syncthreads();
+            // warp per kept group: members, then (internal) the record and
+            // its ready flag
+            for (int g = wid; g < G; g += ST_WARPS) {
+                const int st0 = mem[g], sz = mem[g + 1] - st0;
+                if (sz < 2) continue;
+                const int jl = fsc[g] >> 16, so = fsc[g] & 0xFFFF;
+                const int lj = lsc[g] >> 16, lo = lsc[g] & 0xFFFF;
+                const bool leaf = sz <= a.limit;
+                int32_t *dst;
+                if (leaf) {
+                    if (lbase < 0) continue;
+                    dst = a.leaf_mem + lmbase + lo;
+                    if (lane == 0) {
+                        a.leaf_off[lbase + lj] = lmbase + lo;
+                        a.leaf_cnt[lbase + lj] = sz;
+                    }
+                } else {
+                    if (qbase < 0) continue;
+                    dst = a.arena + abase + (so - lo);
+                }
+                for (int i = lane; i < sz; i += 32) dst[i] = surv[sidx[st0 + i]];
+                if (!leaf) {
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) {
+                        StNode *c = a.q + qbase + (jl - lj);
+                        c->S = S0 + sbase + so;
+                        c->seed = stream_word(seed, a.child_off + (uint64_t)(jbase + jl));
+                        c->off = abase + (so - lo);
+                        c->cnt = sz;
+                        c->depth = depth + 1;
+                        __threadfence();
+                        *(volatile int *)&c->ready = 1;
+                    }
+                }
+            }
+            jbase += kn;
+            sbase += ks;
+        }
+        if (tid == 0 && any_child) atomicMax(&ctr->max_depth, depth + 1);
+        __syncthreads();
+        if (tid == 0) atomicAdd(&qs->pending, ~0ull);  // this node is done
+    }
+}
+
+// ------------------------------------------------------------ host side
+
 // ------------------------------------------------------------ host side
 
 struct Level {
@@ -1204,6 +1635,175 @@ struct Emitter {
     }
 };
 
+// K7 driver: every internal node of the current level (flagged in
+// `small`, exclusive scan `sscan`) and their subtrees by k_subtree, then the
+// K4 leaf kernels on the leaves it emitted.  Scratch exhaustion restores
+// the device counters and relaunches with twice the scratch.
+void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in, const cpsj_plan *plan,
+                 const Level &lv, const int64_t *small, const int64_t *sscan, int64_t n_small, int64_t max_small,
+                 int depth, DevCounters *ctr, int64_t *dscal, bool trace) {
+    cudaStream_t st = drv.st;
+    const int t = in->t, ell = in->ell;
+    int subm = 512;
+    while (subm < max_small) subm <<= 1;
+    const size_t smem = (size_t)subm * 4 + (size_t)(2 * (subm + 2) + std::max(subm + 2, 256 * ST_WARPS)) * 4 +
+                        (size_t)subm * 4 + (size_t)subm * 2;
+    CPSJ_CUDA(cudaFuncSetAttribute(k_subtree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CPSJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_subtree, ST_THREADS, smem));
+    per_sm = std::max(per_sm, 1);
+    // every CTA must be resident: waiting CTAs spin on the queue
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * n_small, (int64_t)ctx->sm_count * per_sm));
+
+    std::unique_ptr<ProfScope> prof(new ProfScope(ctx, PROF_SPLIT, st));
+    DevBuf<int64_t> slist(n_small, st);
+    k_compact_internal<<<blocks_for(lv.N), TPB, 0, st>>>(lv.N, small, sscan, slist.p);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches++;
+    DevBuf<DevCounters> snap(1, st);
+    CPSJ_CUDA(cudaMemsetAsync(&ctr->leaf_n, 0, 2 * sizeof(unsigned long long), st));
+    CPSJ_CUDA(cudaMemsetAsync(&ctr->overflow, 0, sizeof(int), st));
+    CPSJ_CUDA(cudaMemsetAsync(&ctr->cap_n, 0, sizeof(unsigned long long), st));
+    CPSJ_CUDA(cudaMemcpyAsync(snap.p, ctr, sizeof(DevCounters), cudaMemcpyDeviceToDevice, st));
+
+    // scratch: queue records, internal-node member arena, leaf list
+    int64_t q_cap = std::max<int64_t>(1 << 14, 4 * n_small);
+    int64_t arena_cap = std::max<int64_t>(1 << 20, 2 * n_small * (int64_t)subm / 4);
+    int64_t leaf_mem_cap = std::max<int64_t>(1 << 20, 3 * n_small * (int64_t)subm / 4);
+    const int64_t cap_cap = 1 << 16;
+    DevBuf<StNode> q;
+    DevBuf<int32_t> arena, leaf_mem, leaf_cnt;
+    DevBuf<int64_t> leaf_off, cap_sizes(cap_cap, st);
+    DevBuf<StQueue> qs(1, st);
+    SubtreeArgs a{};
+    a.members = lv.members.p;
+    a.sketch = in->d_sketch;
+    a.ell = ell;
+    a.t = t;
+    a.values = in->d_values;
+    a.vbits = plan->value_bits > 0 && plan->value_bits < 32 ? plan->value_bits : 32;
+    a.sizes = in->d_sizes;
+    a.side = in->d_side;
+    a.limit = plan->limit;
+    a.depth_cap = plan->depth_cap;
+    a.accept = plan->accept_dist;
+    a.flag_dist = plan->flag_dist;
+    a.split_p = plan->split_p;
+    a.lam = plan->lambda_;
+    a.child_off = (uint64_t)t + 64ull * (uint64_t)ell;
+    a.cap_sizes = cap_sizes.p;
+    a.cap_cap = cap_cap;
+    a.qs = qs.p;
+    a.ctr = ctr;
+    a.subm = subm;
+    auto launch = [&]() {
+        CPSJ_CUDA(cudaMemsetAsync(q.p, 0, q_cap * sizeof(StNode), st));
+        k_subtree_init<<<blocks_for(n_small), TPB, 0, st>>>(n_small, slist.p, lv.off.p, lv.cnt.p, lv.seed.p,
+                                                            lv.S.p, depth, q.p, qs.p);
+        CPSJ_LAUNCH_CHECK();
+        a.cand = em.cand.p;
+        a.cand_cap = em.cand_cap;
+        k_subtree<<<grid, ST_THREADS, smem, st>>>(a);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches += 2;
+    };
+    DevCounters hc{};
+    for (int attempt = 0;; ++attempt) {
+        q.alloc(q_cap, st);
+        arena.alloc(arena_cap, st);
+        leaf_mem.alloc(leaf_mem_cap, st);
+        leaf_cnt.alloc(leaf_mem_cap / 2, st);
+        leaf_off.alloc(leaf_mem_cap / 2, st);
+        a.q = q.p;
+        a.q_cap = q_cap;
+        a.arena = arena.p;
+        a.arena_cap = arena_cap;
+        a.leaf_mem = leaf_mem.p;
+        a.leaf_mem_cap = leaf_mem_cap;
+        a.leaf_off = leaf_off.p;
+        a.leaf_cnt = leaf_cnt.p;
+        a.leaf_cap = leaf_mem_cap / 2;
+        launch();
+        CPSJ_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        if (!hc.overflow) break;
+        require(attempt < 8, "k_subtree scratch keeps overflowing");
+        CPSJ_CUDA(cudaMemcpyAsync(ctr, snap.p, sizeof(DevCounters), cudaMemcpyDeviceToDevice, st));
+        q_cap *= 2;
+        arena_cap *= 2;
+        leaf_mem_cap *= 2;
+        if (trace) fprintf(stderr, "[join] subtree scratch overflow at depth %d: retry x2\n", depth);
+    }
+    prof.reset();
+    const int64_t nc = (int64_t)hc.cand_n, NL = (int64_t)hc.leaf_n, ncap = (int64_t)hc.cap_n;
+    require(ncap <= cap_cap, "too many depth-cap events in k_subtree");
+    if (ncap) {
+        std::vector<int64_t> h(ncap);
+        CPSJ_CUDA(cudaMemcpyAsync(h.data(), cap_sizes.p, ncap * 8, cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        ctx->cap_events.insert(ctx->cap_events.end(), h.begin(), h.end());
+    }
+    em.verify(nc, [&]() {
+        // re-emit into the grown candidate buffer from the same start state
+        CPSJ_CUDA(cudaMemcpyAsync(ctr, snap.p, sizeof(DevCounters), cudaMemcpyDeviceToDevice, st));
+        launch();
+    });
+    int64_t sc[8];
+    if (NL > 0) {
+        // the emitted leaves, in bulk through the K4 kernels (k_plan adds
+        // their m(m-1)/2 pre-candidates)
+        Level ll;
+        ll.N = NL;
+        ll.M = (int64_t)hc.leaf_m;
+        ll.off = std::move(leaf_off);
+        ll.cnt = std::move(leaf_cnt);
+        ll.members = std::move(leaf_mem);
+        std::unique_ptr<ProfScope> prof_plan(new ProfScope(ctx, PROF_PLAN, st));
+        DevBuf<int64_t> tiles(NL + 1, st), spairs(NL + 1, st), internal2(NL + 1, st), imem(NL + 1, st);
+        DevBuf<int64_t> tile_off(NL + 1, st), pair_off(NL + 1, st), slists((size_t)SMALL_CLASSES * NL, st);
+        DevBuf<unsigned long long> scount(SMALL_CLASSES, st);
+        CPSJ_CUDA(cudaMemsetAsync(scount.p, 0, SMALL_CLASSES * sizeof(unsigned long long), st));
+        const bool small_kernel = ell == 1 || ell == 2 || ell == 4 || ell == 8 || ell == 16;
+        k_plan<<<blocks_for(NL + 1), TPB, 0, st>>>(NL, ll.cnt.p, plan->limit, tiles.p, spairs.p, internal2.p, imem.p,
+                                                   ctr, small_kernel ? slists.p : nullptr, scount.p);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+        LeafWork work2;
+        if (small_kernel) {
+            drv.scan_multi({tiles.p}, {tile_off.p}, NL + 1);
+            const int64_t *c64 = reinterpret_cast<const int64_t *>(scount.p);
+            drv.gather({{tile_off.p + NL, c64, c64 + 1, c64 + 2, c64 + 3}}, 5, dscal, sc);
+            work2.small = true;
+            work2.sl.wcum[0] = 0;
+            for (int k = 0; k < SMALL_CLASSES; ++k) {
+                work2.sl.list[k] = slists.p + (size_t)k * NL;
+                work2.sl.cnt[k] = sc[1 + k];
+                work2.sl.wcum[k + 1] = work2.sl.wcum[k] + (sc[1 + k] * (4 << k) + 31) / 32;
+            }
+        } else {
+            drv.scan_multi({tiles.p, spairs.p}, {tile_off.p, pair_off.p}, NL + 1);
+            drv.gather({{tile_off.p + NL, pair_off.p + NL}}, 2, dscal, sc);
+            work2.pairs = sc[1];
+            work2.pair_off = pair_off.p;
+        }
+        work2.tiles = sc[0];
+        work2.tile_off = tile_off.p;
+        prof_plan.reset();
+        auto gen = [&]() {
+            if (work2.tiles > 0 || work2.pairs > 0 || (work2.small && work2.sl.wcum[SMALL_CLASSES] > 0))
+                leaf_dispatch(ctx, st, work2, ll, in, plan->accept_dist, plan->lambda_, em.cand.p, em.cand_cap, ctr);
+        };
+        gen();
+        drv.gather({{reinterpret_cast<const int64_t *>(&ctr->cand_n)}}, 1, dscal, sc);
+        em.verify(sc[0], gen);
+    }
+    if (trace)
+        fprintf(stderr, "[join] subtree from depth %d: %lld roots (max %lld members, %d CTAs x %d KB smem) -> "
+                        "%lld point candidates, %lld leaves (%lld members), max depth %d\n",
+                depth, (long long)n_small, (long long)max_small, grid, (int)(smem >> 10), (long long)nc,
+                (long long)NL, (long long)hc.leaf_m, hc.max_depth);
+}
+
 }  // namespace
 
 void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
@@ -1264,6 +1864,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     DevBuf<int64_t> tiles, spairs, internal, imem, tile_off, pair_off, iscan, im_off, slists;
     DevBuf<unsigned long long> scount(SMALL_CLASSES, st);
     // leaves of <= 32 members by size class (k_leaf_small) for compile-time ell
+    const char *sub_env = getenv("CPSJ_NO_SUBTREE");  // A/B switch: every level by the level kernels
+    const bool subtree_on = !(sub_env != nullptr && sub_env[0] == '1');
     const char *ovl_env = getenv("CPSJ_NO_LEAF_OVERLAP");  // A/B switch: leaves on the main stream
     const bool overlap_leaves = !(ovl_env != nullptr && ovl_env[0] == '1');
     const char *small_env = getenv("CPSJ_NO_SMALL_LEAF");  // A/B switch: pair-packed k_leaf_pairs
@@ -1302,17 +1904,21 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             slists.ensure((size_t)SMALL_CLASSES * N, st);
             CPSJ_CUDA(cudaMemsetAsync(scount.p, 0, SMALL_CLASSES * sizeof(unsigned long long), st));
         }
+        CPSJ_CUDA(cudaMemsetAsync(&ctr.p->lvl_max_int, 0, sizeof(long long), st));
+        const int64_t *maxint_p = reinterpret_cast<const int64_t *>(&ctr.p->lvl_max_int);
         k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, spairs.p, internal.p, imem.p,
                                                   ctr.p, small_kernel ? slists.p : nullptr, scount.p);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
         int64_t sc[8];
+        int64_t max_int = 0;
         LeafWork work;
         if (small_kernel) {
             drv.scan_multi({tiles.p, internal.p, imem.p}, {tile_off.p, iscan.p, im_off.p}, N + 1);
             const int64_t *c64 = reinterpret_cast<const int64_t *>(scount.p);
-            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, c64, c64 + 1, c64 + 2, c64 + 3}}, 7, dscal.p,
-                       sc);
+            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, c64, c64 + 1, c64 + 2, c64 + 3, maxint_p}}, 8,
+                       dscal.p, sc);
+            max_int = sc[7];
             work.small = true;
             work.sl.wcum[0] = 0;
             for (int k = 0; k < SMALL_CLASSES; ++k) {
@@ -1324,7 +1930,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         } else {
             drv.scan_multi({tiles.p, spairs.p, internal.p, imem.p}, {tile_off.p, pair_off.p, iscan.p, im_off.p},
                            N + 1);
-            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, pair_off.p + N}}, 4, dscal.p, sc);
+            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, pair_off.p + N, maxint_p}}, 5, dscal.p, sc);
+            max_int = sc[4];
             work.pairs = sc[3];
             work.pair_off = pair_off.p;
         }
@@ -1332,6 +1939,11 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         work.tile_off = tile_off.p;
         const int64_t n_int = sc[1], Mi = sc[2];
         prof_plan.reset();
+        // K7 handoff: once every internal node fits a CTA, k_subtree takes
+        // them and everything below (the level kernels stop here)
+        const bool handoff = subtree_on && n_int > 0 && max_int <= ST_MAX_SUBM && !plan->use_count_table &&
+                             ell <= 32 && t <= ST_MAX_SEL;
+        const bool by_levels = n_int > 0 && !handoff;
 
         // ---- leaves: K4 (candidates verified after sync B)
         // the leaves run on the side stream, overlapping the internal-node
@@ -1354,7 +1966,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             gen_leaf();
         }
 
-        if (n_int > 0) {
+        if (by_levels) {
             std::unique_ptr<ProfScope> prof_node(new ProfScope(ctx, PROF_NODE, st));
             ilist.ensure(n_int, st);
             im_off_c.ensure(n_int + 1, st);
@@ -1402,14 +2014,14 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         {
             const int64_t *cand_n = reinterpret_cast<const int64_t *>(&ctr.p->cand_n);
             const int64_t *cap_n = reinterpret_cast<const int64_t *>(&ctr.p->cap_n);
-            if (n_int > 0)
+            if (by_levels)
                 drv.gather({{cand_n, fscan.p + Mi, e_off.p + n_int, seg_off.p + n_int, cap_n}}, 5, dscal.p, sc);
             else
                 drv.gather({{cand_n}}, 1, dscal.p, sc);
         }
         const int64_t n_leaf_cand = sc[0];
-        const int64_t n_flag = n_int > 0 ? sc[1] : 0, E = n_int > 0 ? sc[2] : 0, n_seg = n_int > 0 ? sc[3] : 0;
-        const int64_t ncap = n_int > 0 ? sc[4] : 0;
+        const int64_t n_flag = by_levels ? sc[1] : 0, E = by_levels ? sc[2] : 0, n_seg = by_levels ? sc[3] : 0;
+        const int64_t ncap = by_levels ? sc[4] : 0;
         if (ncap) {
             std::vector<int64_t> h(ncap);
             CPSJ_CUDA(cudaMemcpyAsync(h.data(), capsz.p, ncap * 8, cudaMemcpyDeviceToHost, st));
@@ -1417,6 +2029,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             ctx->cap_events.insert(ctx->cap_events.end(), h.begin(), h.end());
         }
         em.verify(n_leaf_cand, gen_leaf);
+        if (handoff)
+            run_subtree(ctx, drv, em, in, plan, lv, internal.p, iscan.p, n_int, max_int, depth, ctr.p, dscal.p, trace);
 
         // ---- point comparisons of flagged members (K2)
         int count_pre = 1;
@@ -1544,7 +2158,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     stats->pre_candidates = (int64_t)hc.pre;
     stats->candidates = em.total_cand;
     stats->results = nres;
-    stats->max_depth = max_depth;
+    stats->max_depth = std::max<int64_t>(max_depth, hc.max_depth);
     stats->peak_live_members = (n >= 2 && R > 0) ? hc.peak : 0;
     stats->n_depth_cap_events = (int64_t)ctx->cap_events.size();
     stats->n_levels = levels;
