@@ -1670,6 +1670,11 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
     int64_t q_cap = std::max<int64_t>(1 << 14, 4 * n_small);
     int64_t arena_cap = std::max<int64_t>(1 << 20, 2 * n_small * (int64_t)subm / 4);
     int64_t leaf_mem_cap = std::max<int64_t>(1 << 20, 3 * n_small * (int64_t)subm / 4);
+    if (getenv("CPSJ_K7_TINY_SCRATCH") != nullptr) {  // test hook: exercise the overflow retry
+        q_cap = std::max<int64_t>(8, n_small);
+        arena_cap = 64;
+        leaf_mem_cap = 64;
+    }
     const int64_t cap_cap = 1 << 16;
     DevBuf<StNode> q;
     DevBuf<int32_t> arena, leaf_mem, leaf_cnt;
@@ -1727,7 +1732,7 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
         CPSJ_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
         CPSJ_CUDA(cudaStreamSynchronize(st));
         if (!hc.overflow) break;
-        require(attempt < 8, "k_subtree scratch keeps overflowing");
+        require(attempt < 24, "k_subtree scratch keeps overflowing");
         CPSJ_CUDA(cudaMemcpyAsync(ctr, snap.p, sizeof(DevCounters), cudaMemcpyDeviceToDevice, st));
         q_cap *= 2;
         arena_cap *= 2;

@@ -153,6 +153,23 @@ def test_join_matches_reference_golden(name):
         _check_join(cpsjoin_self_arrays(emb, p), z, k)
 
 
+@pytest.mark.parametrize("env", [{"CPSJ_NO_SUBTREE": "1"}, {"CPSJ_K7_TINY_SCRATCH": "1"},
+                                 {"CPSJ_NO_SMALL_LEAF": "1", "CPSJ_NO_LEAF_OVERLAP": "1"}])
+@pytest.mark.parametrize("name", ["planted_880", "dense_cluster", "c1_sample"])
+def test_join_alternate_paths_match_reference_golden(name, env, monkeypatch):
+    """The same trees through the level kernels only (no K7 handoff), through
+    K7 with scratch small enough to overflow and retry, and through the
+    pair-packed small-leaf kernel on the main stream: identical results."""
+    from paper_1707_06814_b200 import Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    z = load(name)
+    ds = Dataset.from_csr(z["tokens"], z["offsets"], int(z["d"]))
+    emb = embed_dataset(EmbeddingParams(t=int(z["t"]), seed=int(z["emb_seed"])), ds)
+    for k in range(int(z["n_joins"])):
+        _check_join(cpsjoin_self_arrays(emb, _params(z, k)), z, k)
+
+
 def _synthetic_emb(z):
     from scipy.sparse import csr_matrix
 
