@@ -136,6 +136,38 @@ def test_sketch_15bit_ties_and_bit_disagreement(L, n_sets):
     assert np.array_equal(got, O.sketch(tok, off, mh, bt))
 
 
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_fused_embed_launch_matches_oracle(L):
+    # cpsj_minhash_embed: values of one family and sketches of another in one
+    # K1 launch (the pipelined embed's per-chunk call)
+    import torch
+
+    from oracle import oracle as O
+    from paper_1707_06814_b200._native import Context, Family
+    rng = np.random.default_rng(200 + L)
+    hi = (1 << (8 * L)) - 1
+    rows = [np.unique(rng.integers(0, hi + 1, size=int(rng.integers(1, 300)), dtype=np.uint64))
+            for _ in range(700)]
+    tok = np.concatenate(rows).astype(np.uint32)
+    off = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    g = O.derive_rng(21, L)
+    et = g.integers(0, 2 ** 64, size=(128, 4, 256), dtype=np.uint64)
+    mh = g.integers(0, 2 ** 64, size=(256, 4, 256), dtype=np.uint64)
+    bt = g.integers(0, 2 ** 64, size=(256, 4, 256), dtype=np.uint64)
+    ctx = Context.get()
+    efam, sfam = Family(ctx, et), Family(ctx, mh, bt)
+    dev = torch.device("cuda", ctx.device)
+    n = len(off) - 1
+    t = torch.from_numpy(tok.view(np.int32)).to(dev)
+    o = torch.from_numpy(off).to(dev)
+    vals = torch.empty((n, 128), dtype=torch.int32, device=dev)
+    sk = torch.empty((n, 4), dtype=torch.int64, device=dev)
+    ctx.check(ctx.lib.cpsj_minhash_embed(ctx.handle, efam.handle, sfam.handle, t.data_ptr(), o.data_ptr(), n, hi,
+                                         vals.data_ptr(), sk.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    assert np.array_equal(vals.cpu().numpy().view(np.uint32), O.minhash(tok, off, et))
+    assert np.array_equal(sk.cpu().numpy().view(np.uint64), O.sketch(tok, off, mh, bt))
+
+
 EMB_FIXTURES = ["planted_small", "planted_880", "dense_cluster", "c1_sample", "c3_sample", "c4_sample",
                 "ct_planted", "ct_dense", "ct_c1_sample"]
 
