@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--clock-ms", type=int, default=1000)
     ap.add_argument("--k1-transport", default="p2p", choices=["p2p", "collective"],
                     help="N>1: K1 rows stored on every GPU by the kernel (p2p) or an NCCL all-gather after it")
+    ap.add_argument("--join-shard", default="frontier", choices=["frontier", "reps"],
+                    help="N>1: split each tree's frontier at --frontier-depth across ranks, or whole repetitions")
+    ap.add_argument("--frontier-depth", type=int, default=1)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional multi-rank run through host-staged collectives (not a bench number)")
     return ap.parse_args()
@@ -407,7 +410,7 @@ def run_ours(args, rank: int, world: int):
     from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
     from paper_1707_06814_b200._native import Context
     from paper_1707_06814_b200.distributed import (PeerArrays, embed_sharded, embed_sharded_p2p,
-                                                   embedded_from_parts, shard_reps)
+                                                   embedded_from_parts, shard_frontier, shard_reps)
     from paper_1707_06814_b200.embed import embed_device_csr
     from paper_1707_06814_b200.workloads import CONFIGS, generate
 
@@ -471,6 +474,11 @@ def run_ours(args, rank: int, world: int):
             _, sk = embed_sharded(None, t_tok, t_off, w.d, skey, rank, world)
         return embedded_from_parts(eparams, t_tok, t_off, w.d, vals, sk, skey)
 
+    def join_sharded(emb):
+        if args.join_shard == "reps":
+            return shard_reps(emb, params, rank, world)
+        return shard_frontier(emb, params, rank, world, depth=args.frontier_depth)
+
     def step_device():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
@@ -482,7 +490,7 @@ def run_ours(args, rank: int, world: int):
             emb = k1_sharded(d_tok, d_off, ev)
         ev[2].record(stream)
         k1_events.append(ev)
-        return shard_reps(emb, params, rank, world)
+        return join_sharded(emb)
 
     def step_e2e():
         if world == 1:
@@ -491,7 +499,7 @@ def run_ours(args, rank: int, world: int):
             t_tok = tok_pin.to(dev, non_blocking=True)
             t_off = off_pin.to(dev, non_blocking=True)
             emb = k1_sharded(t_tok, t_off)
-        return shard_reps(emb, params, rank, world)
+        return join_sharded(emb)
 
     def timed(fn, steps, probe=None):
         if world > 1:
@@ -608,7 +616,9 @@ def run_ours(args, rank: int, world: int):
                                     "single GPU" if world == 1 else
                                     f"K1 set-sharded over {world} GPUs, rows stored to every GPU "
                                     f"{'by the kernel over NVLink (fused all-gather)' if args.k1_transport == 'p2p' else 'by an NCCL all-gather'}; "
-                                    f"repetitions sharded round-robin + pair gather"),
+                                    + (f"join frontier sharded at depth {args.frontier_depth} (every rank builds the levels "
+                                     f"above it) + pair gather" if args.join_shard == "frontier" else
+                                     "repetitions sharded round-robin + pair gather")),
                                                      "recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
                      "frac": achieved / float(peaks["hbm_gbs"]), "traffic": ncu_traffic(args.config, "sketch"),

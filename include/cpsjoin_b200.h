@@ -159,6 +159,15 @@ typedef struct {
                                 instead of the node sketch                    */
     double count_threshold;  /* (1 - epsilon) * lambda_, compared as
                                 (double)(sum - t) / (double)(t (m - 1)) > it */
+    /* frontier sharding across ranks: with frontier_ranks > 1,
+     * every rank builds the levels above frontier_depth, then keeps the nodes
+     * of that level with index % frontier_ranks == frontier_rank (nodes and
+     * their order are identical on every rank).  Ranks != 0 report only what
+     * they found below the cut, so summing counters over ranks and taking the
+     * union of the pairs gives the unsharded join. */
+    int32_t frontier_rank;
+    int32_t frontier_ranks;  /* <= 1: no sharding */
+    int32_t frontier_depth;
 } cpsj_plan;
 
 typedef struct {

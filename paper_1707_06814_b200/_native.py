@@ -25,7 +25,8 @@ class Inputs(ctypes.Structure):
 class Plan(ctypes.Structure):
     _fields_ = [("lambda_", dbl), ("limit", i32), ("depth_cap", i32), ("accept_dist", i32),
                 ("flag_dist", i32), ("split_p", dbl), ("h_rep_seeds", P), ("n_reps", i32), ("value_bits", i32),
-                ("use_count_table", i32), ("count_threshold", dbl)]
+                ("use_count_table", i32), ("count_threshold", dbl), ("frontier_rank", i32),
+                ("frontier_ranks", i32), ("frontier_depth", i32)]
 
 
 class LshPlan(ctypes.Structure):

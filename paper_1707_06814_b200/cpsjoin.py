@@ -106,7 +106,8 @@ class JoinArrays:
     stats: dict
 
 
-def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None, map_ids: bool = True) -> JoinArrays:
+def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None, map_ids: bool = True,
+         frontier=None) -> JoinArrays:
     import torch
 
     from ._native import Context, Inputs, JoinStats, Plan
@@ -133,7 +134,8 @@ def _run(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None, map_ids:
     seeds = np.ascontiguousarray(seeds)
     cplan = Plan(float(params.lambda_), int(params.limit), int(params.depth_cap), plan.accept_dist,
                  plan.flag_dist, float(plan.split_p), seeds.ctypes.data, int(len(seeds)), _value_bits(emb),
-                 1 if params.use_count_table else 0, (1.0 - params.epsilon) * params.lambda_)
+                 1 if params.use_count_table else 0, (1.0 - params.epsilon) * params.lambda_,
+                 *(frontier if frontier is not None else (0, 1, 0)))
     st = JoinStats()
     ctx.check(ctx.lib.cpsj_self_join(ctx.handle, ctypes.byref(inputs), ctypes.byref(cplan), ctypes.byref(st),
                                      stream))
@@ -185,11 +187,18 @@ def _emit_warnings(res: JoinArrays, params: CPSJoinParams, n: int) -> None:
                            res.counters.max_depth, bound, n)
 
 
-def cpsjoin_self_arrays(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None) -> JoinArrays:
+def cpsjoin_self_arrays(emb: EmbeddedDataset, params: CPSJoinParams, rep_indices=None,
+                        frontier: tuple[int, int, int] | None = None) -> JoinArrays:
     """cpsjoin_self returning numpy arrays instead of ResultPair objects.
-    ``rep_indices`` restricts the run to a subset of the repetition trees
-    (used to shard repetitions across GPUs)."""
-    res = _run(emb, params, rep_indices)
+    ``rep_indices`` restricts the run to a subset of the repetition trees;
+    ``frontier=(rank, ranks, depth)`` keeps this rank's share of the nodes at
+    ``depth`` (both used to shard the join across GPUs, distributed.py)."""
+    if frontier is not None:
+        rank, ranks, depth = (int(x) for x in frontier)
+        if not (0 <= rank < ranks and depth >= 0):
+            raise ValueError("frontier must be (rank, ranks, depth) with 0 <= rank < ranks and depth >= 0")
+        frontier = (rank, ranks, depth)
+    res = _run(emb, params, rep_indices, frontier=frontier)
     _emit_warnings(res, params, len(emb))
     return res
 

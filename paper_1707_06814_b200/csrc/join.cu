@@ -799,6 +799,21 @@ __global__ void k_verify(int64_t nc, const int2 *__restrict__ cand, const uint32
     }
 }
 
+// frontier cut: keep nodes rank, rank + ranks, ... of the level (node
+// records only; members stay where they are)
+__global__ void k_frontier_keep(int64_t Nk, int32_t rank, int32_t ranks, const int64_t *__restrict__ off,
+                                const int32_t *__restrict__ cnt, const uint64_t *__restrict__ seed,
+                                const int64_t *__restrict__ S, int64_t *__restrict__ off2, int32_t *__restrict__ cnt2,
+                                uint64_t *__restrict__ seed2, int64_t *__restrict__ S2) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= Nk) return;
+    const int64_t i = j * ranks + rank;
+    off2[j] = off[i];
+    cnt2[j] = cnt[i];
+    seed2[j] = seed[i];
+    S2[j] = S[i];
+}
+
 __global__ void k_fill_roots(int64_t n, int32_t R, int32_t *__restrict__ members) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < n * R) members[e] = (int32_t)(e % n);
@@ -1869,6 +1884,11 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     DevBuf<int64_t> tiles, spairs, internal, imem, tile_off, pair_off, iscan, im_off, slists;
     DevBuf<unsigned long long> scount(SMALL_CLASSES, st);
     // leaves of <= 32 members by size class (k_leaf_small) for compile-time ell
+    const bool frontier = plan->frontier_ranks > 1 && plan->frontier_rank >= 0 &&
+                          plan->frontier_rank < plan->frontier_ranks && plan->frontier_depth >= 0;
+    DevCounters snap_ctr{};
+    int64_t snap_cand = 0, snap_caps = 0;
+    bool cut_done = false;
     const char *sub_env = getenv("CPSJ_NO_SUBTREE");  // A/B switch: every level by the level kernels
     const bool subtree_on = !(sub_env != nullptr && sub_env[0] == '1');
     const char *ovl_env = getenv("CPSJ_NO_LEAF_OVERLAP");  // A/B switch: leaves on the main stream
@@ -1895,6 +1915,35 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     for (int depth = 0; lv.N > 0; ++depth) {
         levels++;
         max_depth = depth;
+        if (frontier && depth == plan->frontier_depth) {
+            // frontier cut (see cpsj_plan): remember what every rank counted
+            // above it, then keep this rank's share of the level's nodes
+            CPSJ_CUDA(cudaMemcpyAsync(&snap_ctr, ctr.p, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+            CPSJ_CUDA(cudaStreamSynchronize(st));
+            snap_cand = em.total_cand;
+            snap_caps = (int64_t)ctx->cap_events.size();
+            cut_done = true;
+            const int64_t Nk = lv.N > plan->frontier_rank
+                                   ? (lv.N - plan->frontier_rank + plan->frontier_ranks - 1) / plan->frontier_ranks
+                                   : 0;
+            nx.off.ensure(std::max<int64_t>(Nk, 1), st);
+            nx.cnt.ensure(std::max<int64_t>(Nk, 1), st);
+            nx.seed.ensure(std::max<int64_t>(Nk, 1), st);
+            nx.S.ensure(std::max<int64_t>(Nk, 1), st);
+            if (Nk > 0) {
+                k_frontier_keep<<<blocks_for(Nk), TPB, 0, st>>>(Nk, plan->frontier_rank, plan->frontier_ranks,
+                                                               lv.off.p, lv.cnt.p, lv.seed.p, lv.S.p, nx.off.p,
+                                                               nx.cnt.p, nx.seed.p, nx.S.p);
+                CPSJ_LAUNCH_CHECK();
+                ctx->launches++;
+            }
+            std::swap(lv.off, nx.off);
+            std::swap(lv.cnt, nx.cnt);
+            std::swap(lv.seed, nx.seed);
+            std::swap(lv.S, nx.S);
+            lv.N = Nk;
+            if (Nk == 0) break;
+        }
         const int64_t N = lv.N;
         if (trace) {
             CPSJ_CUDA(cudaStreamSynchronize(st));
@@ -2165,6 +2214,20 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     stats->results = nres;
     stats->max_depth = std::max<int64_t>(max_depth, hc.max_depth);
     stats->peak_live_members = (n >= 2 && R > 0) ? hc.peak : 0;
+    if (frontier && plan->frontier_rank != 0) {
+        // counted by every rank above the cut: rank 0 reports it
+        if (cut_done) {
+            stats->pre_candidates -= (int64_t)snap_ctr.pre;
+            stats->candidates -= snap_cand;
+            stats->results -= (int64_t)snap_ctr.res_n;
+            ctx->cap_events.erase(ctx->cap_events.begin(), ctx->cap_events.begin() + snap_caps);
+        } else {
+            // the tree ended above the cut: rank 0 has all of it
+            stats->pre_candidates = stats->candidates = stats->results = 0;
+            stats->n_pairs = ctx->n_pairs = 0;
+            ctx->cap_events.clear();
+        }
+    }
     stats->n_depth_cap_events = (int64_t)ctx->cap_events.size();
     stats->n_levels = levels;
     stats->gpu_launches = ctx->launches - launches0;

@@ -264,13 +264,39 @@ def merge_results(parts_keys: np.ndarray, parts_sims: np.ndarray):
 
 def shard_reps(emb, params: CPSJoinParams, rank: int, world: int, group=None, device=None,
                local_join=None) -> JoinArrays:
-    """cpsjoin_self over `world` ranks; every rank returns the full result."""
+    """cpsjoin_self over `world` ranks, repetition trees round-robin; every
+    rank returns the full result."""
     if world <= 1:
         return (local_join or _gpu_local)(emb, params, None)
-    import torch
-    import torch.distributed as dist
     idx = np.arange(rank, params.repetitions, world, dtype=np.int64)
     local = (local_join or _gpu_local)(emb, params, idx)
+    return merge_ranks(local, world, group, device)
+
+
+def shard_frontier(emb, params: CPSJoinParams, rank: int, world: int, depth: int = 1, group=None, device=None,
+                   local_join=None) -> JoinArrays:
+    """cpsjoin_self over `world` ranks, sharding the tree frontier: every
+    rank builds every repetition's levels above `depth` (the root split is
+    cheap and identical everywhere), then keeps the nodes of level `depth`
+    with index % world == rank and everything below them (SURVEY.md 8(e):
+    scales past R GPUs, where repetition sharding stops).  Ranks != 0 count
+    only what they found below the cut, so the counter sums and the pair
+    union equal the unsharded join."""
+    if world <= 1:
+        return (local_join or _gpu_local)(emb, params, None)
+    local = (local_join or _gpu_frontier)(emb, params, (rank, world, depth))
+    return merge_ranks(local, world, group, device)
+
+
+def _gpu_frontier(emb, params: CPSJoinParams, frontier):
+    return cpsjoin_self_arrays(emb, params, frontier=frontier)
+
+
+def merge_ranks(local: JoinArrays, world: int, group=None, device=None) -> JoinArrays:
+    """Union of the ranks' pairs (gather + sort/unique) and their counters
+    (sum of pre/candidates/results, max of depth and peak)."""
+    import torch
+    import torch.distributed as dist
     if device is None:
         device = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
             else torch.device("cpu")

@@ -202,6 +202,35 @@ def test_join_alternate_paths_match_reference_golden(name, env, monkeypatch):
         _check_join(cpsjoin_self_arrays(emb, _params(z, k)), z, k)
 
 
+@pytest.mark.parametrize("no_k7", [False, True])
+@pytest.mark.parametrize("ranks,depth", [(2, 1), (3, 1), (3, 2)])
+@pytest.mark.parametrize("name", ["dense_cluster", "c1_sample", "c4_sample"])
+def test_frontier_sharding_equals_unsharded(name, ranks, depth, no_k7, monkeypatch):
+    """Frontier sharding (distributed.shard_frontier): the ranks' pair union
+    and counter sums equal the unsharded join, simulated in one process."""
+    from paper_1707_06814_b200 import Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    if no_k7:
+        monkeypatch.setenv("CPSJ_NO_SUBTREE", "1")
+    z = load(name)
+    ds = Dataset.from_csr(z["tokens"], z["offsets"], int(z["d"]))
+    emb = embed_dataset(EmbeddingParams(t=int(z["t"]), seed=int(z["emb_seed"])), ds)
+    p = _params(z, 0)
+    ref = cpsjoin_self_arrays(emb, p)
+    parts = [cpsjoin_self_arrays(emb, p, frontier=(r, ranks, depth)) for r in range(ranks)]
+    keys = np.concatenate([(x.a.astype(np.uint64) << np.uint64(32)) | x.b.astype(np.uint64) for x in parts])
+    sims = np.concatenate([x.similarity for x in parts])
+    uk, first = np.unique(keys, return_index=True)
+    assert np.array_equal(uk, (ref.a.astype(np.uint64) << np.uint64(32)) | ref.b.astype(np.uint64))
+    assert np.array_equal(sims[first], ref.similarity)
+    c = ref.counters
+    assert sum(x.counters.pre_candidates for x in parts) == c.pre_candidates
+    assert sum(x.counters.candidates for x in parts) == c.candidates
+    assert sum(x.counters.results for x in parts) == c.results
+    assert max(x.counters.max_depth for x in parts) == c.max_depth
+    assert max(x.counters.peak_live_members for x in parts) == c.peak_live_members
+    assert sum(len(x.depth_cap_sizes) for x in parts) == len(ref.depth_cap_sizes)
+
+
 def _synthetic_emb(z):
     from scipy.sparse import csr_matrix
 
