@@ -56,6 +56,10 @@ struct DevCounters {
     unsigned long long leaf_n;   // leaves emitted by k_subtree
     unsigned long long leaf_m;   // their members
     long long lvl_max_int;       // largest internal node of the current level
+    unsigned long long def_n;    // internal nodes deferred to K7 (cumulative)
+    unsigned long long def_m;    // their members
+    unsigned long long def_slot; // allocation cursors of k_defer_copy
+    unsigned long long def_mtop;
 };
 
 inline unsigned blocks_for(int64_t n, int tpb = TPB) {
@@ -79,7 +83,7 @@ __device__ __host__ __forceinline__ int small_class(int64_t m) {
 __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit,
                        int64_t *__restrict__ tiles, int64_t *__restrict__ spairs, int64_t *__restrict__ internal,
                        int64_t *__restrict__ imem, DevCounters *ctr, int64_t *__restrict__ slists = nullptr,
-                       unsigned long long *__restrict__ scount = nullptr) {
+                       unsigned long long *__restrict__ scount = nullptr, int32_t defer_max = 0) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long pre = 0;
     if (slists != nullptr) {
@@ -105,10 +109,15 @@ __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit
         const int64_t pairs = m * (m - 1) / 2;
         tiles[i] = (leaf && m > 32) ? T * (T + 1) / 2 : 0;
         spairs[i] = (leaf && m <= 32) ? pairs : 0;
-        internal[i] = leaf ? 0 : 1;
-        imem[i] = leaf ? 0 : m;
+        const bool defer = !leaf && m <= defer_max;
+        internal[i] = (leaf || defer) ? 0 : 1;
+        imem[i] = (leaf || defer) ? 0 : m;
         if (leaf) pre = (unsigned long long)pairs;
         else atomicMax(&ctr->lvl_max_int, (long long)m);
+        if (defer) {
+            atomicAdd(&ctr->def_n, 1ull);
+            atomicAdd(&ctr->def_m, (unsigned long long)m);
+        }
     } else if (i == N) {
         tiles[i] = 0;
         spairs[i] = 0;
@@ -814,13 +823,42 @@ __global__ void k_frontier_keep(int64_t Nk, int32_t rank, int32_t ranks, const i
     S2[j] = S[i];
 }
 
+// K7 deferral: warp per node; the internal nodes of <= defer_max members
+// (the same predicate as k_plan) get a record in the deferred root list
+// and a copy of their members (the level's arrays are reused next level)
+__global__ void k_defer_copy(int64_t N, int32_t limit, int32_t defer_max, int32_t depth,
+                             const int64_t *__restrict__ off, const int32_t *__restrict__ cnt,
+                             const uint64_t *__restrict__ seed, const int64_t *__restrict__ S,
+                             const int32_t *__restrict__ members, int64_t *__restrict__ d_off,
+                             int32_t *__restrict__ d_cnt, uint64_t *__restrict__ d_seed, int64_t *__restrict__ d_S,
+                             int32_t *__restrict__ d_depth, int32_t *__restrict__ d_members, DevCounters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= N) return;
+    const int m = cnt[i];
+    if (m <= limit || m > defer_max) return;
+    unsigned long long slot = 0, moff = 0;
+    if (lane == 0) {
+        slot = atomicAdd(&ctr->def_slot, 1ull);
+        moff = atomicAdd(&ctr->def_mtop, (unsigned long long)m);
+        d_off[slot] = (int64_t)moff;
+        d_cnt[slot] = m;
+        d_seed[slot] = seed[i];
+        d_S[slot] = S[i];
+        d_depth[slot] = depth;
+    }
+    moff = __shfl_sync(0xffffffffu, moff, 0);
+    const int32_t *src = members + off[i];
+    for (int e = lane; e < m; e += 32) d_members[moff + e] = src[e];
+}
+
 __global__ void k_fill_roots(int64_t n, int32_t R, int32_t *__restrict__ members) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < n * R) members[e] = (int32_t)(e % n);
 }
 
 struct Gather8 {
-    const int64_t *p[8];
+    const int64_t *p[12];
 };
 
 __global__ void k_gather8(Gather8 g, int cnt, int64_t *__restrict__ out) {
@@ -849,6 +887,7 @@ constexpr int ST_THREADS = 512;
 constexpr int ST_WARPS = ST_THREADS / 32;
 constexpr int ST_MAX_SEL = 256;  // selected positions of one node (t <= 256)
 constexpr int ST_MAX_SUBM = 8192;  // largest node a CTA holds
+constexpr int64_t DEFER_LEVEL_MEMBERS = 1 << 20;  // levels this small defer their nodes to K7
 
 struct StNode {
     int64_t S;
@@ -895,16 +934,16 @@ struct SubtreeArgs {
 __global__ void k_subtree_init(int64_t n_roots, const int64_t *__restrict__ slist,
                                const int64_t *__restrict__ nd_off, const int32_t *__restrict__ nd_cnt,
                                const uint64_t *__restrict__ nd_seed, const int64_t *__restrict__ nd_S, int32_t depth,
-                               StNode *__restrict__ q, StQueue *qs) {
+                               StNode *__restrict__ q, StQueue *qs, const int32_t *__restrict__ nd_depth = nullptr) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r < n_roots) {
-        const int64_t node = slist[r];
+        const int64_t node = slist != nullptr ? slist[r] : r;
         StNode c;
         c.S = nd_S[node];
         c.seed = nd_seed[node];
         c.off = -nd_off[node] - 1;
         c.cnt = nd_cnt[node];
-        c.depth = depth;
+        c.depth = nd_depth != nullptr ? nd_depth[node] : depth;
         c.ready = 1;
         c.pad = 0;
         q[r] = c;
@@ -1656,7 +1695,7 @@ struct Emitter {
 // the device counters and relaunches with twice the scratch.
 void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in, const cpsj_plan *plan,
                  const Level &lv, const int64_t *small, const int64_t *sscan, int64_t n_small, int64_t max_small,
-                 int depth, DevCounters *ctr, int64_t *dscal, bool trace) {
+                 int depth, DevCounters *ctr, int64_t *dscal, bool trace, const int32_t *root_depth = nullptr) {
     cudaStream_t st = drv.st;
     const int t = in->t, ell = in->ell;
     int subm = 512;
@@ -1671,10 +1710,13 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * n_small, (int64_t)ctx->sm_count * per_sm));
 
     std::unique_ptr<ProfScope> prof(new ProfScope(ctx, PROF_SPLIT, st));
-    DevBuf<int64_t> slist(n_small, st);
-    k_compact_internal<<<blocks_for(lv.N), TPB, 0, st>>>(lv.N, small, sscan, slist.p);
-    CPSJ_LAUNCH_CHECK();
-    ctx->launches++;
+    DevBuf<int64_t> slist;
+    if (small != nullptr) {  // roots = the flagged nodes of lv; else every node of lv
+        slist.alloc(n_small, st);
+        k_compact_internal<<<blocks_for(lv.N), TPB, 0, st>>>(lv.N, small, sscan, slist.p);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+    }
     DevBuf<DevCounters> snap(1, st);
     CPSJ_CUDA(cudaMemsetAsync(&ctr->leaf_n, 0, 2 * sizeof(unsigned long long), st));
     CPSJ_CUDA(cudaMemsetAsync(&ctr->overflow, 0, sizeof(int), st));
@@ -1719,7 +1761,7 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
     auto launch = [&]() {
         CPSJ_CUDA(cudaMemsetAsync(q.p, 0, q_cap * sizeof(StNode), st));
         k_subtree_init<<<blocks_for(n_small), TPB, 0, st>>>(n_small, slist.p, lv.off.p, lv.cnt.p, lv.seed.p,
-                                                            lv.S.p, depth, q.p, qs.p);
+                                                            lv.S.p, depth, q.p, qs.p, root_depth);
         CPSJ_LAUNCH_CHECK();
         a.cand = em.cand.p;
         a.cand_cap = em.cand_cap;
@@ -1818,9 +1860,10 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
         em.verify(sc[0], gen);
     }
     if (trace)
-        fprintf(stderr, "[join] subtree from depth %d: %lld roots (max %lld members, %d CTAs x %d KB smem) -> "
+        fprintf(stderr, "[join] K7 (roots from depth %s%d): %lld roots (max %lld members, %d CTAs x %d KB smem) -> "
                         "%lld point candidates, %lld leaves (%lld members), max depth %d\n",
-                depth, (long long)n_small, (long long)max_small, grid, (int)(smem >> 10), (long long)nc,
+                root_depth != nullptr ? ">= " : "", depth, (long long)n_small, (long long)max_small, grid,
+                (int)(smem >> 10), (long long)nc,
                 (long long)NL, (long long)hc.leaf_m, hc.max_depth);
 }
 
@@ -1842,7 +1885,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
 
     Driver drv{ctx, st};
     DevBuf<DevCounters> ctr(1, st);
-    DevBuf<int64_t> dscal(8, st);
+    DevBuf<int64_t> dscal(16, st);
     CPSJ_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(DevCounters), st));
     {
         DevCounters init{};
@@ -1884,13 +1927,26 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     DevBuf<int64_t> tiles, spairs, internal, imem, tile_off, pair_off, iscan, im_off, slists;
     DevBuf<unsigned long long> scount(SMALL_CLASSES, st);
     // leaves of <= 32 members by size class (k_leaf_small) for compile-time ell
+    // K7 deferral state (see the level loop)
+    Level defl;
+    DevBuf<int32_t> def_depth;
+    int64_t def_n = 0, def_m = 0, def_done = 0, def_m_done = 0;
+    int first_defer_depth = 0;
     const bool frontier = plan->frontier_ranks > 1 && plan->frontier_rank >= 0 &&
                           plan->frontier_rank < plan->frontier_ranks && plan->frontier_depth >= 0;
     DevCounters snap_ctr{};
     int64_t snap_cand = 0, snap_caps = 0;
     bool cut_done = false;
     const char *sub_env = getenv("CPSJ_NO_SUBTREE");  // A/B switch: every level by the level kernels
-    const bool subtree_on = !(sub_env != nullptr && sub_env[0] == '1');
+    const bool subtree_on = !(sub_env != nullptr && sub_env[0] == '1') && !plan->use_count_table && ell <= 32 &&
+                            t <= ST_MAX_SEL;
+    // deferral starts at this depth (below the frontier cut when sharded:
+    // nodes above it are built by every rank); CPSJ_DEFER_DEPTH overrides
+    const char *dd_env = getenv("CPSJ_DEFER_DEPTH");
+    int defer_depth = dd_env != nullptr ? atoi(dd_env) : 0;
+    const bool defer_forced = dd_env != nullptr;
+    if (frontier) defer_depth = std::max(defer_depth, plan->frontier_depth);
+    bool defer_active = false;
     const char *ovl_env = getenv("CPSJ_NO_LEAF_OVERLAP");  // A/B switch: leaves on the main stream
     const bool overlap_leaves = !(ovl_env != nullptr && ovl_env[0] == '1');
     const char *small_env = getenv("CPSJ_NO_SMALL_LEAF");  // A/B switch: pair-packed k_leaf_pairs
@@ -1960,19 +2016,28 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         }
         CPSJ_CUDA(cudaMemsetAsync(&ctr.p->lvl_max_int, 0, sizeof(long long), st));
         const int64_t *maxint_p = reinterpret_cast<const int64_t *>(&ctr.p->lvl_max_int);
+        const int64_t *defn_p = reinterpret_cast<const int64_t *>(&ctr.p->def_n);
+        const int64_t *defm_p = reinterpret_cast<const int64_t *>(&ctr.p->def_m);
+        // deferral starts once a level is small (the level kernels are the
+        // better tool for big levels, K7 where launch latency dominates)
+        defer_active = defer_active || (depth >= defer_depth && (defer_forced || lv.M <= DEFER_LEVEL_MEMBERS));
+        const int32_t defer_max = (subtree_on && defer_active) ? ST_MAX_SUBM : 0;
         k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, spairs.p, internal.p, imem.p,
-                                                  ctr.p, small_kernel ? slists.p : nullptr, scount.p);
+                                                  ctr.p, small_kernel ? slists.p : nullptr, scount.p, defer_max);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
-        int64_t sc[8];
-        int64_t max_int = 0;
+        int64_t sc[12];
+        int64_t max_int = 0;  // largest internal node (trace)
         LeafWork work;
         if (small_kernel) {
             drv.scan_multi({tiles.p, internal.p, imem.p}, {tile_off.p, iscan.p, im_off.p}, N + 1);
             const int64_t *c64 = reinterpret_cast<const int64_t *>(scount.p);
-            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, c64, c64 + 1, c64 + 2, c64 + 3, maxint_p}}, 8,
-                       dscal.p, sc);
+            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, c64, c64 + 1, c64 + 2, c64 + 3, maxint_p,
+                         defn_p, defm_p}},
+                       10, dscal.p, sc);
             max_int = sc[7];
+            def_n = sc[8];
+            def_m = sc[9];
             work.small = true;
             work.sl.wcum[0] = 0;
             for (int k = 0; k < SMALL_CLASSES; ++k) {
@@ -1984,8 +2049,11 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         } else {
             drv.scan_multi({tiles.p, spairs.p, internal.p, imem.p}, {tile_off.p, pair_off.p, iscan.p, im_off.p},
                            N + 1);
-            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, pair_off.p + N, maxint_p}}, 5, dscal.p, sc);
+            drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, pair_off.p + N, maxint_p, defn_p, defm_p}}, 7,
+                       dscal.p, sc);
             max_int = sc[4];
+            def_n = sc[5];
+            def_m = sc[6];
             work.pairs = sc[3];
             work.pair_off = pair_off.p;
         }
@@ -1993,11 +2061,29 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         work.tile_off = tile_off.p;
         const int64_t n_int = sc[1], Mi = sc[2];
         prof_plan.reset();
-        // K7 handoff: once every internal node fits a CTA, k_subtree takes
-        // them and everything below (the level kernels stop here)
-        const bool handoff = subtree_on && n_int > 0 && max_int <= ST_MAX_SUBM && !plan->use_count_table &&
-                             ell <= 32 && t <= ST_MAX_SEL;
-        const bool by_levels = n_int > 0 && !handoff;
+        // K7 deferral: this level's internal nodes of <= 8192 members (not in
+        // n_int) join the deferred root list that one k_subtree launch takes
+        // after the last level; only the larger ones continue here
+        if (def_n > def_done) {
+            ProfScope prof_def(ctx, PROF_SPLIT, st);
+            const size_t keepn = (size_t)def_done, keepm = (size_t)def_m_done;
+            defl.off.grow(def_n + def_n / 2 + 64, keepn, st);
+            defl.cnt.grow(def_n + def_n / 2 + 64, keepn, st);
+            defl.seed.grow(def_n + def_n / 2 + 64, keepn, st);
+            defl.S.grow(def_n + def_n / 2 + 64, keepn, st);
+            def_depth.grow(def_n + def_n / 2 + 64, keepn, st);
+            defl.members.grow(def_m + def_m / 2 + 4096, keepm, st);
+            k_defer_copy<<<blocks_for(N * 32), TPB, 0, st>>>(N, plan->limit, defer_max, depth, lv.off.p, lv.cnt.p,
+                                                             lv.seed.p, lv.S.p, lv.members.p, defl.off.p, defl.cnt.p,
+                                                             defl.seed.p, defl.S.p, def_depth.p, defl.members.p,
+                                                             ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            if (def_done == 0) first_defer_depth = depth;
+            def_done = def_n;
+            def_m_done = def_m;
+        }
+        const bool by_levels = n_int > 0;
 
         // ---- leaves: K4 (candidates verified after sync B)
         // the leaves run on the side stream, overlapping the internal-node
@@ -2083,8 +2169,6 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             ctx->cap_events.insert(ctx->cap_events.end(), h.begin(), h.end());
         }
         em.verify(n_leaf_cand, gen_leaf);
-        if (handoff)
-            run_subtree(ctx, drv, em, in, plan, lv, internal.p, iscan.p, n_int, max_int, depth, ctr.p, dscal.p, trace);
 
         // ---- point comparisons of flagged members (K2)
         int count_pre = 1;
@@ -2194,14 +2278,22 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             fprintf(stderr,
                     "[join] depth %d nodes %lld members %lld internal %lld (members %lld) leaf_tiles %lld "
                     "small_leaves|pairs %lld leaf_cand %lld flagged %lld entries %lld children %lld | %.1f us "
-                    "(%.1f us blocked in syncs)\n",
+                    "(%.1f us blocked in syncs, largest internal node %lld)\n",
                     depth, (long long)N, (long long)lv.M, (long long)n_int, (long long)Mi, (long long)work.tiles,
                     (long long)(work.small ? work.sl.cnt[0] + work.sl.cnt[1] + work.sl.cnt[2] + work.sl.cnt[3]
                                            : work.pairs), (long long)n_leaf_cand, (long long)n_flag, (long long)E,
-                    (long long)nx.N, us, drv.sync_us);
+                    (long long)nx.N, us, drv.sync_us, (long long)max_int);
         }
         std::swap(lv, nx);  // the old level's arrays become the next level's storage
         nx.N = nx.M = 0;
+    }
+
+    // ---- K7 on every deferred internal node (and everything below them)
+    if (def_done > 0) {
+        defl.N = def_done;
+        defl.M = def_m_done;
+        run_subtree(ctx, drv, em, in, plan, defl, nullptr, nullptr, def_done, ST_MAX_SUBM, first_defer_depth, ctr.p,
+                    dscal.p, trace, def_depth.p);
     }
 
     // ---- K6: sort + unique of the verified pairs
