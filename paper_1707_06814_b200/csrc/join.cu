@@ -262,12 +262,14 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
     const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch, int ell_rt,
     const int32_t *__restrict__ sizes, const int8_t *__restrict__ side, int32_t accept, double lam,
     int2 *__restrict__ cand,
-    unsigned long long cap, DevCounters *ctr) {
+    unsigned long long cap, DevCounters *ctr, const int32_t *__restrict__ tile_node = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (tile >= total_tiles) return;
     const int ell = ELL > 0 ? ELL : ell_rt;
-    const int64_t node = upper_bound_i64(tile_off, N + 1, tile) - 1;
+    // the tile's leaf: one load from the tile -> node map (a binary search
+    // over tile_off is ~log2(N) dependent loads)
+    const int64_t node = tile_node != nullptr ? (int64_t)tile_node[tile] : upper_bound_i64(tile_off, N + 1, tile) - 1;
     int64_t local = tile - tile_off[node];
     const int m = nd_cnt[node];
     const int T = (m + 31) >> 5;
@@ -434,6 +436,13 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
             }
         }
     }
+}
+
+// tile -> leaf map for k_leaf_tiles (thread per node)
+__global__ void k_tile_nodes(int64_t N, const int64_t *__restrict__ tile_off, int32_t *__restrict__ tile_node) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    for (int64_t t = tile_off[i]; t < tile_off[i + 1]; ++t) tile_node[t] = (int32_t)i;
 }
 
 // Pair-packed BruteForce for leaves of <= 32 members: thread per pair
@@ -1481,10 +1490,17 @@ void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level
                  int32_t accept, double lam, int2 *cand, unsigned long long cap, DevCounters *ctr) {
     ProfScope prof(ctx, PROF_LEAF, st);
     if (wk.tiles > 0) {
+        DevBuf<int32_t> tile_node;
+        if (lv.N < INT32_MAX) {
+            tile_node.alloc(wk.tiles, st);
+            k_tile_nodes<<<blocks_for(lv.N), TPB, 0, st>>>(lv.N, wk.tile_off, tile_node.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+        }
         k_leaf_tiles<ELL><<<blocks_for(wk.tiles * 32), TPB, 0, st>>>(wk.tiles, wk.tile_off, lv.N, lv.off.p,
                                                                      lv.cnt.p, lv.members.p, in->d_sketch, in->ell,
                                                                      in->d_sizes, in->d_side, accept, lam, cand, cap,
-                                                                     ctr);
+                                                                     ctr, tile_node.p);
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
     }
