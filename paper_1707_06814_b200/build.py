@@ -22,7 +22,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr", "--extended-lambda",
     "-Xptxas", "-v" if os.environ.get("CPSJ_PTXAS_VERBOSE") else "-O3",
-]
+] + os.environ.get("CPSJ_NVCC_EXTRA", "").split()  # experiments (e.g. -DVAL_FMA_REGS=1)
 
 
 def _stale() -> bool:
