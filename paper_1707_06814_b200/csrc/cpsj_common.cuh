@@ -118,6 +118,22 @@ __device__ __forceinline__ int64_t upper_bound_i64(const int64_t *a, int64_t n, 
     return lo;
 }
 
+// upper_bound_i64(a, n, x) - 1 (the segment of x) for a full warp whose x
+// ascend with the lane: lane 0 searches for the warp's first x and lanes
+// still inside that segment reuse it, so a warp inside one large segment
+// does one binary search instead of 32 (all 32 lanes must call).
+__device__ __forceinline__ int64_t warp_segment(const int64_t *a, int64_t n, int64_t x) {
+    const int64_t x0 = __shfl_sync(0xffffffffu, x, 0);
+    int64_t k0 = 0, hi0 = 0;
+    if ((threadIdx.x & 31) == 0) {
+        k0 = upper_bound_i64(a, n, x0) - 1;
+        hi0 = k0 + 1 < n ? a[k0 + 1] : INT64_MAX;
+    }
+    k0 = __shfl_sync(0xffffffffu, k0, 0);
+    hi0 = __shfl_sync(0xffffffffu, hi0, 0);
+    return (x >= x0 && x < hi0) ? k0 : upper_bound_i64(a, n, x) - 1;
+}
+
 }  // namespace cpsj
 
 // -------------------------------------------------------------- context

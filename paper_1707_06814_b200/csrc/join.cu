@@ -554,13 +554,21 @@ __global__ void k_flags(int64_t Mi, const int64_t *__restrict__ im_off, int64_t 
                         const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch, int ell,
                         const uint64_t *__restrict__ nsk, int32_t flag_dist, int64_t *__restrict__ flags) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = warp_segment(im_off, n_int + 1, e);
     if (e > Mi) return;
     if (e == Mi) { flags[e] = 0; return; }
-    const int64_t k = upper_bound_i64(im_off, n_int + 1, e) - 1;
     const int32_t x = members[nd_off[ilist[k]] + (e - im_off[k])];
     const uint64_t *a = sketch + (size_t)x * ell, *b = nsk + (size_t)k * ell;
     int dist = 0;
-    for (int w = 0; w < ell; ++w) dist += __popcll(a[w] ^ b[w]);
+    if ((ell & 1) == 0 && (reinterpret_cast<uintptr_t>(sketch) & 15) == 0) {  // 16-byte rows: vector loads
+        const ulonglong2 *a2 = reinterpret_cast<const ulonglong2 *>(a), *b2 = reinterpret_cast<const ulonglong2 *>(b);
+        for (int w = 0; w < (ell >> 1); ++w) {
+            const ulonglong2 u = a2[w], v = b2[w];
+            dist += __popcll(u.x ^ v.x) + __popcll(u.y ^ v.y);
+        }
+    } else {
+        for (int w = 0; w < ell; ++w) dist += __popcll(a[w] ^ b[w]);
+    }
     flags[e] = dist <= flag_dist ? 1 : 0;
 }
 
@@ -629,8 +637,8 @@ __global__ void k_survivors(int64_t Mi, const int64_t *__restrict__ im_off, int6
                             const int32_t *__restrict__ members, const int64_t *__restrict__ flags,
                             const int64_t *__restrict__ fscan, int32_t *__restrict__ surv) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = warp_segment(im_off, n_int + 1, e);
     if (e >= Mi || flags[e]) return;
-    const int64_t k = upper_bound_i64(im_off, n_int + 1, e) - 1;
     surv[e - fscan[e]] = members[nd_off[ilist[k]] + (e - im_off[k])];
 }
 
@@ -692,8 +700,8 @@ __global__ void k_build_keys(int64_t E, const int64_t *__restrict__ e_off, int64
                              const uint32_t *__restrict__ values, int vbits, KT *__restrict__ keys,
                              int32_t *__restrict__ vals) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = warp_segment(e_off, n_int + 1, e);
     if (e >= E) return;
-    const int64_t k = upper_bound_i64(e_off, n_int + 1, e) - 1;
     const int64_t local = e - e_off[k];
     const int64_t s = (e_off[k + 1] - e_off[k]) / nsel[k];
     const int64_t r = local / s, p = local - r * s;

@@ -10,7 +10,10 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1707_06814_b200 import CPSJoinParams, EmbeddingParams, cpsjoin_self_arrays  # noqa
-from paper_1707_06814_b200._native import Context  # noqa
+from paper_1707_06814_b200._native import Context, load  # noqa
+
+if os.environ.get("CPSJ_LIB"):  # A/B against another build of the library
+    load(os.environ["CPSJ_LIB"])
 from paper_1707_06814_b200.embed import embed_device_csr  # noqa
 from paper_1707_06814_b200.workloads import CONFIGS, generate  # noqa
 
