@@ -150,6 +150,41 @@ struct Sk {
     uint64_t w[ELL];
 };
 
+// popcount of the N 32-bit words v (XORs of two sketches) in triplets:
+// popc(x) + popc(y) + popc(z) = popc(x ^ y ^ z) + 2 popc(maj(x, y, z)), two
+// POPC per three words instead of three.  POPC issues on the XU pipe
+// (15.4 lanes/clk/SM measured), the bound of the BruteForce kernels; the
+// two LOP3 go to the wider ALU pipe.  Exact.
+template <int N>
+__device__ __forceinline__ int popc_csa(const uint32_t *v) {
+    int d = 0;
+#pragma unroll
+    for (int k = 0; k + 2 < N; k += 3) {
+        const uint32_t x = v[k], y = v[k + 1], z = v[k + 2];
+        d += __popc(x ^ y ^ z) + 2 * __popc((x & y) | (z & (x ^ y)));
+    }
+#pragma unroll
+    for (int k = N - N % 3; k < N; ++k) d += __popc(v[k]);
+    return d;
+}
+
+// XOR-distance of sketch words [B, E) of a and b (u64) through popc_csa
+template <int B, int E>
+__device__ __forceinline__ int xdist(const uint64_t *a, const uint64_t *b) {
+    if constexpr (E <= B) {
+        return 0;
+    } else {
+        uint32_t v[2 * (E - B)];
+#pragma unroll
+        for (int k = B; k < E; ++k) {
+            const uint64_t x = a[k] ^ b[k];
+            v[2 * (k - B)] = (uint32_t)x;
+            v[2 * (k - B) + 1] = (uint32_t)(x >> 32);
+        }
+        return popc_csa<2 * (E - B)>(v);
+    }
+}
+
 // warp-aggregated candidate append
 __device__ __forceinline__ void emit_pair(bool pass, int32_t a, int32_t b, int2 *cand, unsigned long long cap,
                                           DevCounters *ctr) {
@@ -190,14 +225,18 @@ __device__ __forceinline__ void cyclic_block(int32_t x, int32_t xsize, const uin
         int dist = 0;
         if (ELL >= 8) {
             constexpr int C1 = ELL * 5 / 8, C2 = ELL * 6 / 8;
+            uint64_t pw[ELL];
 #pragma unroll
-            for (int q = 0; q < C1; ++q) dist += __popcll(w[q] ^ __shfl_sync(0xffffffffu, w[q], src));
+            for (int q = 0; q < C1; ++q) pw[q] = __shfl_sync(0xffffffffu, w[q], src);
+            dist = xdist<0, C1>(w, pw);
             if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
 #pragma unroll
-            for (int q = C1; q < C2; ++q) dist += __popcll(w[q] ^ __shfl_sync(0xffffffffu, w[q], src));
+            for (int q = C1; q < C2; ++q) pw[q] = __shfl_sync(0xffffffffu, w[q], src);
+            dist += xdist<C1, C2>(w, pw);
             if (!__any_sync(0xffffffffu, active && dist <= accept)) continue;
 #pragma unroll
-            for (int q = C2; q < ELL; ++q) dist += __popcll(w[q] ^ __shfl_sync(0xffffffffu, w[q], src));
+            for (int q = C2; q < ELL; ++q) pw[q] = __shfl_sync(0xffffffffu, w[q], src);
+            dist += xdist<C2, ELL>(w, pw);
         } else {
 #pragma unroll
             for (int q = 0; q < ELL; ++q) dist += __popcll(w[q] ^ __shfl_sync(0xffffffffu, w[q], src));
@@ -328,23 +367,14 @@ __global__ void __launch_bounds__(TPB) k_leaf_tiles(
             int da = 0, db = 0;
             if (EK >= 8) {
                 constexpr int C1 = EK * 5 / 8, C2 = EK * 6 / 8;
-#pragma unroll
-                for (int k = 0; k < C1; ++k) {
-                    da += __popcll(ra[k] ^ cw.w[k]);
-                    db += __popcll(rb[k] ^ cw.w[k]);
-                }
+                da = xdist<0, C1>(ra, cw.w);
+                db = xdist<0, C1>(rb, cw.w);
                 if (!__any_sync(0xffffffffu, da <= accept || (two && db <= accept))) continue;
-#pragma unroll
-                for (int k = C1; k < C2; ++k) {
-                    da += __popcll(ra[k] ^ cw.w[k]);
-                    db += __popcll(rb[k] ^ cw.w[k]);
-                }
+                da += xdist<C1, C2>(ra, cw.w);
+                db += xdist<C1, C2>(rb, cw.w);
                 if (!__any_sync(0xffffffffu, da <= accept || (two && db <= accept))) continue;
-#pragma unroll
-                for (int k = C2; k < EK; ++k) {
-                    da += __popcll(ra[k] ^ cw.w[k]);
-                    db += __popcll(rb[k] ^ cw.w[k]);
-                }
+                da += xdist<C2, EK>(ra, cw.w);
+                db += xdist<C2, EK>(rb, cw.w);
             } else {
 #pragma unroll
                 for (int k = 0; k < EK; ++k) {
