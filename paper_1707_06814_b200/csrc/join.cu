@@ -11,7 +11,7 @@
 //   _size_side_filter   cpsjoin.py:129-137  -> size_filter()
 //   _verify_and_emit    cpsjoin.py:114-127  -> k_verify (K5)
 //   split_buckets       cpsjoin.py:222-245  -> k_select / k_build_keys /
-//                                              radix sort / k_children (K3)
+//                                              radix sort / k_marks / k_children_e (K3)
 //   _build_self_pairs   cpsjoin.py:308-319  -> sort + unique (K6)
 //
 // Why a BFS is exact: a node's processing depends only on (members, depth,
@@ -772,40 +772,64 @@ __global__ void k_group_keep(const int64_t *__restrict__ Gp, int64_t E, const in
     }
 }
 
-// child node records: seed = word(parent seed, t + 64 ell + j) for the
-// parent's j-th child (cps:286,301); S for the DFS-peak replay
+// Entry-level group marks after the sort (the self-join level path): kh =
+// first entry of a group of >= 2 equal keys (one child, cps:242-244), inm =
+// entry lies in such a group.  Scans of the two give each child its index and
+// member offset directly, without group-level arrays.
 template <typename KT>
-__global__ void k_children(const int64_t *__restrict__ Gp, int64_t E, const int64_t *__restrict__ gstart,
-                           const int64_t *__restrict__ keep, const int64_t *__restrict__ kscan,
-                           const int64_t *__restrict__ mscan, const int64_t *__restrict__ hscan,
-                           const KT *__restrict__ keys, const int64_t *__restrict__ seg_off,
-                           int64_t n_int, const int64_t *__restrict__ e_off,
-                           const int64_t *__restrict__ ilist, const uint64_t *__restrict__ nd_seed,
-                           const int64_t *__restrict__ nd_S, uint64_t child_off,
-                           int64_t *__restrict__ c_off, int32_t *__restrict__ c_cnt,
-                           uint64_t *__restrict__ c_seed, int64_t *__restrict__ c_S, int vbits,
-                           DevCounters *ctr) {
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t G = *Gp;
+__global__ void k_marks(int64_t E, const KT *__restrict__ keys, int64_t *__restrict__ kh, int64_t *__restrict__ inm) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e > E) return;
+    if (e == E) {
+        kh[e] = 0;
+        inm[e] = 0;
+        return;
+    }
+    const KT k = keys[e];
+    const bool sp = e > 0 && keys[e - 1] == k, sn = e + 1 < E && keys[e + 1] == k;
+    kh[e] = !sp && sn;
+    inm[e] = sp || sn;
+}
+
+// child records from the kept group heads: member offset, seed = word(parent
+// seed, t + 64 ell + j) for the parent's j-th child (cps:286,301), S for the
+// DFS-peak replay; the sizes follow from consecutive offsets (k_child_sizes)
+template <typename KT>
+__global__ void k_children_e(int64_t E, const int64_t *__restrict__ kh, const int64_t *__restrict__ kscan,
+                             const int64_t *__restrict__ mscan, const KT *__restrict__ keys,
+                             const int64_t *__restrict__ seg_off, int64_t n_int, const int64_t *__restrict__ e_off,
+                             const int64_t *__restrict__ ilist, const uint64_t *__restrict__ nd_seed,
+                             const int64_t *__restrict__ nd_S, uint64_t child_off, int64_t *__restrict__ c_off,
+                             uint64_t *__restrict__ c_seed, int64_t *__restrict__ c_S, int vbits) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E || !kh[e]) return;
+    const int64_t seg = (int64_t)((uint64_t)keys[e] >> vbits);
+    const int64_t k = upper_bound_i64(seg_off, n_int + 1, seg) - 1;
+    const int64_t node = ilist[k];
+    const int64_t e0 = e_off[k];  // the parent's first entry
+    const int64_t ci = kscan[e];
+    c_off[ci] = mscan[e];
+    c_seed[ci] = stream_word(nd_seed[node], child_off + (uint64_t)(ci - kscan[e0]));
+    c_S[ci] = nd_S[node] + (mscan[e] - mscan[e0]);
+}
+
+__global__ void k_child_sizes(int64_t N, int64_t M, const int64_t *__restrict__ c_off,
+                              const int64_t *__restrict__ c_S, int32_t *__restrict__ c_cnt, DevCounters *ctr) {
+    const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     long long cand_peak = 0;
-    if (g < G && keep[g]) {
-        const int64_t st = gstart[g];
-        const int64_t sz = (g + 1 < G ? gstart[g + 1] : E) - st;
-        const int64_t seg = (int64_t)((uint64_t)keys[st] >> vbits);
-        const int64_t k = upper_bound_i64(seg_off, n_int + 1, seg) - 1;
-        const int64_t node = ilist[k];
-        const int64_t g0 = hscan[e_off[k]];  // parent's first group
-        const int64_t ci = kscan[g];
-        const int64_t j = ci - kscan[g0];
-        const int64_t S = nd_S[node] + (mscan[g] - mscan[g0]);
-        c_off[ci] = mscan[g];
+    if (ci < N) {
+        const int64_t sz = (ci + 1 < N ? c_off[ci + 1] : M) - c_off[ci];
         c_cnt[ci] = (int32_t)sz;
-        c_seed[ci] = stream_word(nd_seed[node], child_off + (uint64_t)j);
-        c_S[ci] = S;
-        cand_peak = S + sz;
+        cand_peak = c_S[ci] + sz;
     }
     for (int o = 16; o > 0; o >>= 1) cand_peak = max(cand_peak, __shfl_down_sync(0xffffffffu, cand_peak, o));
     if ((threadIdx.x & 31) == 0 && cand_peak) atomicMax(&ctr->peak, cand_peak);
+}
+
+__global__ void k_scatter_e(int64_t E, const int64_t *__restrict__ inm, const int64_t *__restrict__ mscan,
+                            const int32_t *__restrict__ vals, int32_t *__restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E && inm[e]) out[mscan[e]] = vals[e];
 }
 
 __global__ void k_scatter_children(int64_t E, const int64_t *__restrict__ head, const int64_t *__restrict__ hscan,
@@ -2280,17 +2304,13 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
                                                           0, end_bit, st));
             ctx->lib_calls++;
-            for (DevBuf<int64_t> *b : {&head, &hscan, &gstart, &keep, &ksize, &kscan, &mscan}) b->ensure(E + 1, st);
-            if (keys32) k_heads<uint32_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, k32b, head.p);
-            else k_heads<uint64_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p);
+            // head = kept-group heads, keep = members of kept groups (entry level)
+            for (DevBuf<int64_t> *b : {&head, &keep, &kscan, &mscan}) b->ensure(E + 1, st);
+            if (keys32) k_marks<uint32_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, k32b, head.p, keep.p);
+            else k_marks<uint64_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p, keep.p);
             CPSJ_LAUNCH_CHECK();
-            drv.scan_multi({head.p}, {hscan.p}, E + 1);
-            k_group_start<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p);
-            CPSJ_LAUNCH_CHECK();
-            k_group_keep<<<blocks_for(E + 1), TPB, 0, st>>>(hscan.p + E, E, gstart.p, keep.p, ksize.p);
-            CPSJ_LAUNCH_CHECK();
-            ctx->launches += 4;
-            drv.scan_multi({keep.p, ksize.p}, {kscan.p, mscan.p}, E + 1);
+            ctx->launches++;
+            drv.scan_multi({head.p, keep.p}, {kscan.p, mscan.p}, E + 1);
         }
         // ---- (C) one read: point candidates, children totals
         {
@@ -2311,19 +2331,19 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             nx.S.ensure(nx.N, st);
             nx.members.ensure(nx.M, st);
             if (keys32)
-                k_children<uint32_t><<<blocks_for(E), TPB, 0, st>>>(
-                    hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p,
-                    reinterpret_cast<const uint32_t *>(keys2.p), seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p,
-                    lv.S.p, child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, vbits, ctr.p);
+                k_children_e<uint32_t><<<blocks_for(E), TPB, 0, st>>>(
+                    E, head.p, kscan.p, mscan.p, reinterpret_cast<const uint32_t *>(keys2.p), seg_off.p, n_int,
+                    e_off.p, ilist.p, lv.seed.p, lv.S.p, child_off, nx.off.p, nx.seed.p, nx.S.p, vbits);
             else
-                k_children<uint64_t><<<blocks_for(E), TPB, 0, st>>>(
-                    hscan.p + E, E, gstart.p, keep.p, kscan.p, mscan.p, hscan.p, keys2.p, seg_off.p, n_int, e_off.p,
-                    ilist.p, lv.seed.p, lv.S.p, child_off, nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p, vbits, ctr.p);
+                k_children_e<uint64_t><<<blocks_for(E), TPB, 0, st>>>(
+                    E, head.p, kscan.p, mscan.p, keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p, lv.S.p,
+                    child_off, nx.off.p, nx.seed.p, nx.S.p, vbits);
             CPSJ_LAUNCH_CHECK();
-            k_scatter_children<<<blocks_for(E), TPB, 0, st>>>(E, head.p, hscan.p, gstart.p, keep.p, mscan.p, vals2.p,
-                                                              nx.members.p);
+            k_child_sizes<<<blocks_for(nx.N), TPB, 0, st>>>(nx.N, nx.M, nx.off.p, nx.S.p, nx.cnt.p, ctr.p);
             CPSJ_LAUNCH_CHECK();
-            ctx->launches += 2;
+            k_scatter_e<<<blocks_for(E), TPB, 0, st>>>(E, keep.p, mscan.p, vals2.p, nx.members.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 3;
         }
         if (trace) {
             CPSJ_CUDA(cudaStreamSynchronize(st));
