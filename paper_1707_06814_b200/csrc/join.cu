@@ -11,7 +11,7 @@
 //   _size_side_filter   cpsjoin.py:129-137  -> size_filter()
 //   _verify_and_emit    cpsjoin.py:114-127  -> k_verify (K5)
 //   split_buckets       cpsjoin.py:222-245  -> k_select / k_build_keys /
-//                                              radix sort / k_marks / k_children_e (K3)
+//                                              radix sort + group-mark scan / k_children_e (K3)
 //   _build_self_pairs   cpsjoin.py:308-319  -> sort + unique (K6)
 //
 // Why a BFS is exact: a node's processing depends only on (members, depth,
@@ -772,37 +772,24 @@ __global__ void k_group_keep(const int64_t *__restrict__ Gp, int64_t E, const in
     }
 }
 
-// Entry-level group marks after the sort (the self-join level path): kh =
-// first entry of a group of >= 2 equal keys (one child, cps:242-244), inm =
-// entry lies in such a group.  Scans of the two give each child its index and
-// member offset directly, without group-level arrays.
-template <typename KT>
-__global__ void k_marks(int64_t E, const KT *__restrict__ keys, int64_t *__restrict__ kh, int64_t *__restrict__ inm) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e > E) return;
-    if (e == E) {
-        kh[e] = 0;
-        inm[e] = 0;
-        return;
-    }
-    const KT k = keys[e];
-    const bool sp = e > 0 && keys[e - 1] == k, sn = e + 1 < E && keys[e + 1] == k;
-    kh[e] = !sp && sn;
-    inm[e] = sp || sn;
-}
+// Entry-level group marks after the sort (the self-join level path): a
+// kept head is the first entry of a group of >= 2 equal keys (one child,
+// cps:242-244).  The scans of the marks (computed inside the scan, ScanSet::
+// mkeys) give each child its index (kscan) and member offset (mscan); a mark
+// itself is the scan's step, kscan[e + 1] - kscan[e].
 
 // child records from the kept group heads: member offset, seed = word(parent
 // seed, t + 64 ell + j) for the parent's j-th child (cps:286,301), S for the
 // DFS-peak replay; the sizes follow from consecutive offsets (k_child_sizes)
 template <typename KT>
-__global__ void k_children_e(int64_t E, const int64_t *__restrict__ kh, const int64_t *__restrict__ kscan,
+__global__ void k_children_e(int64_t E, const int64_t *__restrict__ kscan,
                              const int64_t *__restrict__ mscan, const KT *__restrict__ keys,
                              const int64_t *__restrict__ seg_off, int64_t n_int, const int64_t *__restrict__ e_off,
                              const int64_t *__restrict__ ilist, const uint64_t *__restrict__ nd_seed,
                              const int64_t *__restrict__ nd_S, uint64_t child_off, int64_t *__restrict__ c_off,
                              uint64_t *__restrict__ c_seed, int64_t *__restrict__ c_S, int vbits) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E || !kh[e]) return;
+    if (e >= E || kscan[e + 1] == kscan[e]) return;
     const int64_t seg = (int64_t)((uint64_t)keys[e] >> vbits);
     const int64_t k = upper_bound_i64(seg_off, n_int + 1, seg) - 1;
     const int64_t node = ilist[k];
@@ -826,10 +813,10 @@ __global__ void k_child_sizes(int64_t N, int64_t M, const int64_t *__restrict__ 
     if ((threadIdx.x & 31) == 0 && cand_peak) atomicMax(&ctr->peak, cand_peak);
 }
 
-__global__ void k_scatter_e(int64_t E, const int64_t *__restrict__ inm, const int64_t *__restrict__ mscan,
-                            const int32_t *__restrict__ vals, int32_t *__restrict__ out) {
+__global__ void k_scatter_e(int64_t E, const int64_t *__restrict__ mscan, const int32_t *__restrict__ vals,
+                            int32_t *__restrict__ out) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < E && inm[e]) out[mscan[e]] = vals[e];
+    if (e < E && mscan[e + 1] != mscan[e]) out[mscan[e]] = vals[e];
 }
 
 __global__ void k_scatter_children(int64_t E, const int64_t *__restrict__ head, const int64_t *__restrict__ hscan,
@@ -1385,10 +1372,40 @@ struct ScanSet {
     const int64_t *in[4];
     int64_t *out[4];
     int64_t *part;  // [K][tiles] tile sums, then their exclusive scan
+    // K == 2 with mkeys set: the inputs are the group marks of the mE sorted
+    // split keys (32-bit keys if mkey32), computed on the fly: in[0] = first
+    // entry of a group of >= 2 equal keys, in[1] = entry inside such a group
+    const void *mkeys;
+    int mkey32;
+    int64_t mE;
 };
+
+template <typename KT>
+__device__ __forceinline__ void group_marks(const KT *keys, int64_t E, int64_t i, int64_t &kh, int64_t &inm) {
+    if (i >= E) {
+        kh = inm = 0;
+        return;
+    }
+    const KT c = keys[i];
+    const bool sp = i > 0 && keys[i - 1] == c, sn = i + 1 < E && keys[i + 1] == c;
+    kh = !sp && sn;
+    inm = sp || sn;
+}
 
 template <int K>
 __device__ __forceinline__ void scan_load(const ScanSet &a, int64_t n, int64_t base, int64_t (&v)[K][4]) {
+    if constexpr (K == 2) {
+        if (a.mkeys != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (a.mkey32)
+                    group_marks(static_cast<const uint32_t *>(a.mkeys), a.mE, base + j, v[0][j], v[1][j]);
+                else
+                    group_marks(static_cast<const uint64_t *>(a.mkeys), a.mE, base + j, v[0][j], v[1][j]);
+            }
+            return;
+        }
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k)
 #pragma unroll
@@ -1482,8 +1499,12 @@ struct Driver {
     DevBuf<int64_t> scan_part;
 
     // exclusive scans of k <= 4 arrays of length n (see k_scan_apply)
-    void scan_multi(std::initializer_list<const int64_t *> ins, std::initializer_list<int64_t *> outs, int64_t n) {
+    void scan_multi(std::initializer_list<const int64_t *> ins, std::initializer_list<int64_t *> outs, int64_t n,
+                    const void *mkeys = nullptr, int mkey32 = 0) {
         ScanSet a{};
+        a.mkeys = mkeys;
+        a.mkey32 = mkey32;
+        a.mE = n - 1;
         int k = 0;
         for (const int64_t *p : ins) a.in[k++] = p;
         k = 0;
@@ -2304,13 +2325,13 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                 CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
                                                           0, end_bit, st));
             ctx->lib_calls++;
-            // head = kept-group heads, keep = members of kept groups (entry level)
-            for (DevBuf<int64_t> *b : {&head, &keep, &kscan, &mscan}) b->ensure(E + 1, st);
-            if (keys32) k_marks<uint32_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, k32b, head.p, keep.p);
-            else k_marks<uint64_t><<<blocks_for(E + 1), TPB, 0, st>>>(E, keys2.p, head.p, keep.p);
-            CPSJ_LAUNCH_CHECK();
-            ctx->launches++;
-            drv.scan_multi({head.p, keep.p}, {kscan.p, mscan.p}, E + 1);
+            // kscan / mscan = exclusive scans of the entry-level group marks
+            // (kept-group heads, members of kept groups), marks computed
+            // inside the scan from the sorted keys
+            for (DevBuf<int64_t> *b : {&kscan, &mscan}) b->ensure(E + 1, st);
+            drv.scan_multi({nullptr, nullptr}, {kscan.p, mscan.p}, E + 1,
+                           keys32 ? static_cast<const void *>(k32b) : static_cast<const void *>(keys2.p),
+                           keys32 ? 1 : 0);
         }
         // ---- (C) one read: point candidates, children totals
         {
@@ -2332,16 +2353,16 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             nx.members.ensure(nx.M, st);
             if (keys32)
                 k_children_e<uint32_t><<<blocks_for(E), TPB, 0, st>>>(
-                    E, head.p, kscan.p, mscan.p, reinterpret_cast<const uint32_t *>(keys2.p), seg_off.p, n_int,
+                    E, kscan.p, mscan.p, reinterpret_cast<const uint32_t *>(keys2.p), seg_off.p, n_int,
                     e_off.p, ilist.p, lv.seed.p, lv.S.p, child_off, nx.off.p, nx.seed.p, nx.S.p, vbits);
             else
                 k_children_e<uint64_t><<<blocks_for(E), TPB, 0, st>>>(
-                    E, head.p, kscan.p, mscan.p, keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p, lv.S.p,
+                    E, kscan.p, mscan.p, keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p, lv.S.p,
                     child_off, nx.off.p, nx.seed.p, nx.S.p, vbits);
             CPSJ_LAUNCH_CHECK();
             k_child_sizes<<<blocks_for(nx.N), TPB, 0, st>>>(nx.N, nx.M, nx.off.p, nx.S.p, nx.cnt.p, ctr.p);
             CPSJ_LAUNCH_CHECK();
-            k_scatter_e<<<blocks_for(E), TPB, 0, st>>>(E, keep.p, mscan.p, vals2.p, nx.members.p);
+            k_scatter_e<<<blocks_for(E), TPB, 0, st>>>(E, mscan.p, vals2.p, nx.members.p);
             CPSJ_LAUNCH_CHECK();
             ctx->launches += 3;
         }
