@@ -781,23 +781,24 @@ __global__ void k_group_keep(const int64_t *__restrict__ Gp, int64_t E, const in
 // child records from the kept group heads: member offset, seed = word(parent
 // seed, t + 64 ell + j) for the parent's j-th child (cps:286,301), S for the
 // DFS-peak replay; the sizes follow from consecutive offsets (k_child_sizes)
-template <typename KT>
-__global__ void k_children_e(int64_t E, const int64_t *__restrict__ kscan,
-                             const int64_t *__restrict__ mscan, const KT *__restrict__ keys,
-                             const int64_t *__restrict__ seg_off, int64_t n_int, const int64_t *__restrict__ e_off,
-                             const int64_t *__restrict__ ilist, const uint64_t *__restrict__ nd_seed,
-                             const int64_t *__restrict__ nd_S, uint64_t child_off, int64_t *__restrict__ c_off,
-                             uint64_t *__restrict__ c_seed, int64_t *__restrict__ c_S, int vbits) {
+__global__ void k_children_e(int64_t E, const int64_t *__restrict__ kscan, const int64_t *__restrict__ mscan,
+                             int64_t n_int, const int64_t *__restrict__ e_off, const int64_t *__restrict__ ilist,
+                             const uint64_t *__restrict__ nd_seed, const int64_t *__restrict__ nd_S,
+                             uint64_t child_off, int64_t *__restrict__ c_off, uint64_t *__restrict__ c_seed,
+                             int64_t *__restrict__ c_S, const int32_t *__restrict__ vals,
+                             int32_t *__restrict__ c_members) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E || kscan[e + 1] == kscan[e]) return;
-    const int64_t seg = (int64_t)((uint64_t)keys[e] >> vbits);
-    const int64_t k = upper_bound_i64(seg_off, n_int + 1, seg) - 1;
+    const int64_t k = warp_segment(e_off, n_int + 1, e);  // the entry's parent (internal node k)
+    if (e >= E) return;
+    const int64_t mo = mscan[e];
+    if (mscan[e + 1] != mo) c_members[mo] = vals[e];  // entry of a kept group: the child's member
+    if (kscan[e + 1] == kscan[e]) return;
     const int64_t node = ilist[k];
     const int64_t e0 = e_off[k];  // the parent's first entry
     const int64_t ci = kscan[e];
-    c_off[ci] = mscan[e];
+    c_off[ci] = mo;
     c_seed[ci] = stream_word(nd_seed[node], child_off + (uint64_t)(ci - kscan[e0]));
-    c_S[ci] = nd_S[node] + (mscan[e] - mscan[e0]);
+    c_S[ci] = nd_S[node] + (mo - mscan[e0]);
 }
 
 __global__ void k_child_sizes(int64_t N, int64_t M, const int64_t *__restrict__ c_off,
@@ -811,12 +812,6 @@ __global__ void k_child_sizes(int64_t N, int64_t M, const int64_t *__restrict__ 
     }
     for (int o = 16; o > 0; o >>= 1) cand_peak = max(cand_peak, __shfl_down_sync(0xffffffffu, cand_peak, o));
     if ((threadIdx.x & 31) == 0 && cand_peak) atomicMax(&ctr->peak, cand_peak);
-}
-
-__global__ void k_scatter_e(int64_t E, const int64_t *__restrict__ mscan, const int32_t *__restrict__ vals,
-                            int32_t *__restrict__ out) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < E && mscan[e + 1] != mscan[e]) out[mscan[e]] = vals[e];
 }
 
 __global__ void k_scatter_children(int64_t E, const int64_t *__restrict__ head, const int64_t *__restrict__ hscan,
@@ -2351,20 +2346,13 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             nx.seed.ensure(nx.N, st);
             nx.S.ensure(nx.N, st);
             nx.members.ensure(nx.M, st);
-            if (keys32)
-                k_children_e<uint32_t><<<blocks_for(E), TPB, 0, st>>>(
-                    E, kscan.p, mscan.p, reinterpret_cast<const uint32_t *>(keys2.p), seg_off.p, n_int,
-                    e_off.p, ilist.p, lv.seed.p, lv.S.p, child_off, nx.off.p, nx.seed.p, nx.S.p, vbits);
-            else
-                k_children_e<uint64_t><<<blocks_for(E), TPB, 0, st>>>(
-                    E, kscan.p, mscan.p, keys2.p, seg_off.p, n_int, e_off.p, ilist.p, lv.seed.p, lv.S.p,
-                    child_off, nx.off.p, nx.seed.p, nx.S.p, vbits);
+            k_children_e<<<blocks_for(E), TPB, 0, st>>>(E, kscan.p, mscan.p, n_int, e_off.p, ilist.p, lv.seed.p,
+                                                        lv.S.p, child_off, nx.off.p, nx.seed.p, nx.S.p, vals2.p,
+                                                        nx.members.p);
             CPSJ_LAUNCH_CHECK();
             k_child_sizes<<<blocks_for(nx.N), TPB, 0, st>>>(nx.N, nx.M, nx.off.p, nx.S.p, nx.cnt.p, ctr.p);
             CPSJ_LAUNCH_CHECK();
-            k_scatter_e<<<blocks_for(E), TPB, 0, st>>>(E, mscan.p, vals2.p, nx.members.p);
-            CPSJ_LAUNCH_CHECK();
-            ctx->launches += 3;
+            ctx->launches += 2;
         }
         if (trace) {
             CPSJ_CUDA(cudaStreamSynchronize(st));
