@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", default="auto")
+    ap.add_argument("--lambda", dest="lam", type=float, default=None,
+                    help="similarity threshold (default: the config's first lambda, BASELINE.json)")
     ap.add_argument("--cpu-scale", type=float, default=None, help="CPU sample scale (default: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # nvidia-smi in its own process at 500 ms; an in-process NVML thread
@@ -57,6 +59,7 @@ def parse():
     ap.add_argument("--frontier-depth", type=int, default=1)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional multi-rank run through host-staged collectives (not a bench number)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-workload oracle comparison")
     return ap.parse_args()
 
 
@@ -366,21 +369,23 @@ def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
+    lam = args.lam if args.lam is not None else cfg.lambdas[0]
     threads = cpu_threads()
     # the GPU arm's exact workload when its recall truth is on file (c2: ~10 s
     # per step on 16 host threads), else a sample sized to ~15 s per step
     from oracle.make_truth import truth_path
     if args.cpu_scale:
         scale = args.cpu_scale
-    elif os.path.exists(truth_path(args.config, args.scale, cfg.lambdas[0])):
+    elif os.path.exists(truth_path(args.config, args.scale, lam)):
         scale = args.scale
     else:
         scale = cpu_sample_scale(args.config, threads) * args.scale
         if scale > 0.8 * args.scale:
             scale = args.scale
     w = generate(args.config, scale=scale)
-    truth, truth_src = recall_truth(args.config, scale, w, cfg.lambdas[0])
+    truth, truth_src = recall_truth(args.config, scale, w, lam)
     arm = CpuArm(w, cfg, threads)
+    arm.lam = lam
     R, rec = arm.choose_reps(truth)
     for _ in range(max(0, min(args.warmup, 1))):  # one warm-up: the port has no JIT or caches to warm
         arm.pipeline(R)
@@ -393,8 +398,11 @@ def run_reference(args, rank: int, world: int):
             "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded generator for the BASELINE.json config)",
-            "config": {"workload": f"{cfg.name} x{scale:g}", "n_sets": int(w.n), "repetitions": R, "recall": rec,
-                       "recall_truth": truth_src, "lambda": cfg.lambdas[0], "ell": cfg.ell, "t": 128},
+            # the GPU arm's config dict (same workload keys) when the sample is the whole workload
+            "config": workload_dict(w, cfg, R, rec, lam, {
+                "parallelism": f"host CPU, {threads} threads (C port of the reference, oracle/cpsj_oracle.c)",
+                "recall_truth": truth_src, "n_true_pairs": int(len(truth)),
+                **({} if scale == args.scale else {"sample_scale": scale})}),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "sets/s", "cores": threads, "kind": "port",
                              "sample": sample},
@@ -404,18 +412,32 @@ def run_reference(args, rank: int, world: int):
 
 # ----------------------------------------------------------------- GPU arm
 
+def parity_check(res, ref_keys, ref_sims, ref_counters) -> dict:
+    """Bit-exact comparison of a GPU join result with another result: the
+    unique pair keys, the f64 similarities and the five counters."""
+    keys = (np.asarray(res.a).astype(np.uint64) << np.uint64(32)) | np.asarray(res.b).astype(np.uint64)
+    c = res.counters
+    got_c = [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members]
+    same_keys = bool(np.array_equal(keys, ref_keys))
+    same_sims = bool(same_keys and np.array_equal(np.asarray(res.similarity).view(np.uint64),
+                                                  np.asarray(ref_sims).view(np.uint64)))
+    return {"bit_exact": bool(same_keys and same_sims and got_c == list(ref_counters)), "keys": same_keys,
+            "sims": same_sims, "counters": got_c == list(ref_counters), "n_pairs": int(len(keys))}
+
+
 def run_ours(args, rank: int, world: int):
     import torch
 
     from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
     from paper_1707_06814_b200._native import Context
     from paper_1707_06814_b200.distributed import (PeerArrays, embed_sharded, embed_sharded_p2p,
-                                                   embedded_from_parts, shard_frontier, shard_reps)
+                                                   embed_sharded_p2p_from_host, embedded_from_parts,
+                                                   shard_frontier, shard_reps)
     from paper_1707_06814_b200.embed import embed_device_csr
     from paper_1707_06814_b200.workloads import CONFIGS, generate
 
     cfg = CONFIGS[args.config]
-    lam = cfg.lambdas[0]
+    lam = args.lam if args.lam is not None else cfg.lambdas[0]
     dev = torch.device("cuda", torch.cuda.current_device())
     t0 = time.time()
     w = generate(args.config, scale=args.scale)
@@ -446,6 +468,7 @@ def run_ours(args, rank: int, world: int):
             if rec >= cfg.recall:
                 break
     log(f"[rank {rank}] R={R} recall={rec:.4f} truth={None if truth is None else len(truth)}")
+    single = res  # the single-GPU join of this workload (every rank computes it once, untimed)
     del emb0
     params = CPSJoinParams(lambda_=lam, ell=cfg.ell, seed=cfg.join_seed, repetitions=R)
 
@@ -455,9 +478,11 @@ def run_ours(args, rank: int, world: int):
     skey = (cfg.ell, cfg.join_seed)
 
     peers = None
+    side = torch.cuda.Stream(dev) if world > 1 else None
     if world > 1 and args.k1_transport == "p2p":
-        # node-wide exchange buffers: K1 stores every row on every GPU
-        peers = PeerArrays(ctx, n, 128, cfg.ell, rank, world)
+        # node-wide exchange buffers: K1 stores every row on every GPU, and
+        # every rank pushes its CSR slice to every GPU (end to end)
+        peers = PeerArrays(ctx, n, 128, cfg.ell, rank, world, nnz=len(w.tokens))
 
     def k1_sharded(t_tok, t_off, ev=None):
         if peers is not None:
@@ -492,9 +517,16 @@ def run_ours(args, rank: int, world: int):
         k1_events.append(ev)
         return join_sharded(emb)
 
+    h2d_rank = [int(w.tokens.nbytes + w.offsets.nbytes)]
+
     def step_e2e():
         if world == 1:
             emb = embed_dataset(eparams, ds, sketch=skey)
+        elif peers is not None:
+            # only this rank's CSR slice crosses PCIe; NVLink replicates it
+            t_tok, t_off, vals, sk, h2d_rank[0] = embed_sharded_p2p_from_host(
+                eparams, tok_pin, off_pin, w.d, skey, rank, world, peers, side_stream=side)
+            emb = embedded_from_parts(eparams, t_tok, t_off, w.d, vals, sk, skey)
         else:
             t_tok = tok_pin.to(dev, non_blocking=True)
             t_off = off_pin.to(dev, non_blocking=True)
@@ -527,7 +559,7 @@ def run_ours(args, rank: int, world: int):
         log(f"[rank {rank}] {getattr(fn, '__name__', 'step')}: per-step ms min {min(per):.2f} "
             f"median {statistics.median(per):.2f} max {max(per):.2f} | " + " ".join(f"{x:.1f}" for x in per))
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=dev) if torch.distributed.get_backend() == "nccl" else torch.tensor([ms])
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms = float(t.item())
         return ms, out
@@ -558,6 +590,17 @@ def run_ours(args, rank: int, world: int):
         ms_e2e, res_e2e = timed(step_e2e, args.steps, probe)
     value = n * args.steps / (ms_dev / 1e3)
     e2e_value = n * args.steps / (ms_e2e / 1e3)
+    # the drop-in entry point (list[ResultPair]) once, outside the timed
+    # region: what cpsjoin_self adds on top of the arrays form timed in e2e
+    dropin_ms = None
+    if world == 1:
+        from paper_1707_06814_b200 import cpsjoin_self
+        emb_d = embed_dataset(eparams, ds, sketch=skey)
+        torch.cuda.synchronize()
+        td = time.perf_counter()
+        pairs_d, _ = cpsjoin_self(emb_d, params)
+        dropin_ms = (time.perf_counter() - td) * 1e3
+        del emb_d, pairs_d
     # per-kernel-class device time from one extra, separately profiled step
     ctx.profile(True)
     torch.cuda.synchronize()
@@ -590,8 +633,15 @@ def run_ours(args, rank: int, world: int):
     pairs_per_s = pre / (k4_ms / 1e3) if k4_ms > 0 else None
     popc_rate, popc_basis = int_peak("POPC", 16.0)
     popc_peak = 148 * popc_rate * f_clk / (2 * cfg.ell)  # 2 POPC per u64 word
-    h2d = int(w.tokens.nbytes + w.offsets.nbytes)
-    d2h = int(len(res_e2e.a) * 16)
+
+    # ---- parity at benchmark scale: the timed device result, the e2e result
+    # and the single-GPU join must agree bit for bit, and (one rank, N = 1,
+    # full workload) with the C oracle port of the reference
+    skeys = (single.a.astype(np.uint64) << np.uint64(32)) | single.b.astype(np.uint64)
+    sc = single.counters
+    scnt = [sc.pre_candidates, sc.candidates, sc.results, sc.max_depth, sc.peak_live_members]
+    parity = {"device_vs_single_gpu": parity_check(res, skeys, single.similarity, scnt),
+              "e2e_vs_single_gpu": parity_check(res_e2e, skeys, single.similarity, scnt)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the same algorithm on the host: the oracle port, all threads, same
@@ -602,11 +652,35 @@ def run_ours(args, rank: int, world: int):
         if cscale > 0.8 * args.scale:
             cscale = args.scale
         cw = w if cscale == args.scale else generate(args.config, scale=cscale)
-        cdt, cout = CpuArm(cw, cfg, threads).pipeline(R)
+        arm = CpuArm(cw, cfg, threads)
+        arm.lam = lam
+        cdt, cout = arm.pipeline(R)
         crec = recall_of(cout.a, cout.b, truth) if cw is w else None
         cpu = {"value": cw.n / cdt, "unit": "sets/s", "cores": threads, "kind": "port",
                "sample": f"{cfg.name} x{cscale:g}: {cw.n} sets, embed+sketch+join R={R}"
                          + (f" (recall {crec:.3f})" if crec is not None else "") + f", {cdt:.2f} s"}
+        if cw is w and not args.no_parity:
+            ocnt = [cout.pre_candidates, cout.candidates, cout.results, cout.max_depth, cout.peak_live_members]
+            parity["device_vs_oracle"] = parity_check(res, cout.keys, cout.sims, ocnt)
+            parity["vs"] = "C oracle port of the reference on the full workload (same seeds, R)"
+    elif rank == 0 and world == 1 and not args.no_parity:
+        arm = CpuArm(w, cfg, cpu_threads())
+        arm.lam = lam
+        _, cout = arm.pipeline(R)
+        ocnt = [cout.pre_candidates, cout.candidates, cout.results, cout.max_depth, cout.peak_live_members]
+        parity["device_vs_oracle"] = parity_check(res, cout.keys, cout.sims, ocnt)
+        parity["vs"] = "C oracle port of the reference on the full workload (same seeds, R)"
+    parity["bit_exact"] = all(v["bit_exact"] for k, v in parity.items() if isinstance(v, dict))
+    if not parity["bit_exact"]:
+        log(f"[rank {rank}] PARITY FAILURE: {parity}")
+
+    h2d_total = int(w.tokens.nbytes + w.offsets.nbytes)
+    if world > 1:
+        hb = torch.tensor([h2d_rank[0]], dtype=torch.int64,
+                          device=dev if torch.distributed.get_backend() == "nccl" else "cpu")
+        torch.distributed.all_reduce(hb)
+        h2d_total = int(hb.item())
+    d2h = int(len(res_e2e.a) * 16)
     line = {
         "metric": METRIC, "value": value, "unit": "sets/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
@@ -616,9 +690,9 @@ def run_ours(args, rank: int, world: int):
                                     "single GPU" if world == 1 else
                                     f"K1 set-sharded over {world} GPUs, rows stored to every GPU "
                                     f"{'by the kernel over NVLink (fused all-gather)' if args.k1_transport == 'p2p' else 'by an NCCL all-gather'}; "
-                                    + (f"join frontier sharded at depth {args.frontier_depth} (every rank builds the levels "
-                                     f"above it) + pair gather" if args.join_shard == "frontier" else
-                                     "repetitions sharded round-robin + pair gather")),
+                                    + (f"join frontier sharded at depth {args.frontier_depth} (size-balanced cut; every "
+                                       f"rank builds the levels above it) + pair gather" if args.join_shard == "frontier"
+                                       else "repetitions sharded round-robin + pair gather")),
                                                      "recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
                      "frac": achieved / float(peaks["hbm_gbs"]), "traffic": ncu_traffic(args.config, "sketch"),
@@ -644,13 +718,23 @@ def run_ours(args, rank: int, world: int):
         "join_counters": {"pre_candidates": pre, "candidates": res.counters.candidates,
                           "results": res.counters.results, "max_depth": res.counters.max_depth,
                           "pairs": int(len(res.a))},
-        "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": ms_e2e / args.steps},
+        "parity": parity,
+        "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d_total, "d2h_bytes_per_step": d2h,
+                "ms_per_step": ms_e2e / args.steps,
+                "api": ("embed_dataset(EmbeddingParams, Dataset, sketch=(ell, seed)) + cpsjoin_self_arrays "
+                        "(the drop-in's array form; cpsjoin_self builds list[ResultPair] from it)" if world == 1 else
+                        "embed_sharded_p2p_from_host (each rank copies only its CSR slice host->device, "
+                        "NVLink replicates it) + shard_frontier"),
+                "h2d_bytes_per_rank": h2d_rank[0],
+                "dropin_cpsjoin_self_ms": dropin_ms},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "impl": "ours",
     }
+    if args.dist_backend == "gloo" and world > 1:
+        line["functional_only"] = ("gloo backend: collectives staged through the host, possibly several ranks on "
+                                   "one GPU -- a functional check of the N-rank path, not a bench number")
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -660,15 +744,39 @@ def ctx_launch_count(ctx) -> int:
     return ctx.launch_counts()[0]
 
 
+def relaunch_under_torchrun(n: int) -> None:
+    """`python bench.py --gpus N` (N > 1) without a launcher: re-execute
+    this command under torch.distributed.run with N ranks on this node (the
+    same launch the driver uses), so --gpus always means N processes."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log(f"bench: --gpus {n} without WORLD_SIZE: relaunching as {' '.join(cmd[1:6])} ...")
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
     import torch
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > torch.cuda.device_count() and args.dist_backend == "nccl":
+        raise SystemExit(f"bench: {world} ranks but {torch.cuda.device_count()} GPU(s); NCCL needs one GPU per "
+                         "rank (--dist-backend gloo runs the N-rank path functionally on fewer GPUs)")
     if args.dist_backend == "gloo":
         local %= torch.cuda.device_count()
     torch.cuda.set_device(local)

@@ -33,6 +33,17 @@ extern "C" {
 #define CPSJ_E_OOM -3      /* device allocation failed                      */
 #define CPSJ_E_PICK -4     /* node-sketch pick index == m (reference raises
                               IndexError at cpsjoin.py:193; p ~ 2^-54)      */
+#define CPSJ_E_ABI -5      /* struct_size of a parameter struct does not
+                              match this library (caller built against a
+                              different header)                             */
+
+/* ABI version: cpsj_version() == CPSJ_ABI_VERSION.  Every parameter struct
+ * begins with `int64_t struct_size`, which the caller sets to
+ * sizeof(struct) of ITS header; the library rejects any other size with
+ * CPSJ_E_ABI instead of reading past the caller's struct. */
+#define CPSJ_ABI_MAJOR 2
+#define CPSJ_ABI_MINOR 0
+#define CPSJ_ABI_VERSION ((CPSJ_ABI_MAJOR << 16) | CPSJ_ABI_MINOR)
 
 typedef struct cpsj_ctx cpsj_ctx;
 typedef struct cpsj_family cpsj_family;
@@ -100,6 +111,7 @@ CPSJ_API int cpsj_minhash_embed(cpsj_ctx *ctx, const cpsj_family *emb_fam, const
  */
 #define CPSJ_MAX_DSTS 8
 typedef struct {
+    int64_t struct_size;        /* = sizeof(cpsj_k1_dsts)                */
     uint32_t *d_values[CPSJ_MAX_DSTS];
     uint64_t *d_sketch[CPSJ_MAX_DSTS];
     int32_t n_dsts;
@@ -122,10 +134,17 @@ CPSJ_API int cpsj_minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam,
 CPSJ_API int cpsj_xbuf_create(cpsj_ctx *ctx, int64_t bytes, void **d_ptr, uint8_t *h_ipc_handle);
 CPSJ_API int cpsj_xbuf_open(cpsj_ctx *ctx, const uint8_t *h_ipc_handle, void **d_ptr);
 CPSJ_API int cpsj_xbuf_close(cpsj_ctx *ctx, void *d_ptr, int32_t opened);
+/* stream-ordered byte copy between any two addresses this context's device
+ * reaches (pinned host, local device, peer buffers from cpsj_xbuf_open;
+ * cudaMemcpyDefault over UVA): the set-sharded end-to-end path pushes each
+ * rank's CSR slice to every peer with it (copy engines over NVLink, so the
+ * replication overlaps K1 without taking SMs) */
+CPSJ_API int cpsj_copy_async(cpsj_ctx *ctx, void *dst, const void *src, int64_t bytes, void *stream);
 
 /* device inputs of a self-join: the EmbeddedDataset fields the engine reads
  * (cpsjoin.py:95-108) */
 typedef struct {
+    int64_t struct_size;        /* = sizeof(cpsj_inputs)                */
     const uint32_t *d_tokens;   /* verify_csr.indices  (nnz)            */
     const int64_t *d_offsets;   /* verify_csr.indptr   (n + 1)          */
     const int32_t *d_sizes;     /* emb.sizes           (n)              */
@@ -142,6 +161,7 @@ typedef struct {
 /* host-derived plan; every float rule is pre-reduced to an integer
  * threshold by the host with numpy semantics */
 typedef struct {
+    int64_t struct_size;     /* = sizeof(cpsj_plan)                           */
     double lambda_;          /* verification threshold J >= lambda_           */
     int32_t limit;           /* brute-force size limit (cpsjoin.py:259)        */
     int32_t depth_cap;       /* cpsjoin.py:294                                 */
@@ -160,11 +180,16 @@ typedef struct {
     double count_threshold;  /* (1 - epsilon) * lambda_, compared as
                                 (double)(sum - t) / (double)(t (m - 1)) > it */
     /* frontier sharding across ranks: with frontier_ranks > 1,
-     * every rank builds the levels above frontier_depth, then keeps the nodes
-     * of that level with index % frontier_ranks == frontier_rank (nodes and
-     * their order are identical on every rank).  Ranks != 0 report only what
-     * they found below the cut, so summing counters over ranks and taking the
-     * union of the pairs gives the unsharded join. */
+     * every rank builds the levels above frontier_depth (nodes and their
+     * order are identical on every rank), then keeps its share of that
+     * level's nodes: a size-balanced contiguous cut, node i (of N, in level
+     * order) belongs to rank floor(ranks * (2 C_i + c_i) / (2 C_N)) where
+     * C_i = c_0 + ... + c_{i-1} and the cost estimate of a node of m members
+     * is c = m + floor(m (m - 1) / 64) for a leaf (m <= limit: BruteForce
+     * pairs) and c = m * bit_length(m) for an internal node (its subtree's
+     * member visits), integer arithmetic throughout.  Ranks != 0 report only what they found below the cut,
+     * so summing counters over ranks and taking the union of the pairs gives
+     * the unsharded join. */
     int32_t frontier_rank;
     int32_t frontier_ranks;  /* <= 1: no sharding */
     int32_t frontier_depth;
@@ -219,6 +244,7 @@ CPSJ_API int cpsj_join_result_device(cpsj_ctx *ctx, const uint64_t **d_keys,
  * and d_sketch are required; d_side may be NULL.
  */
 typedef struct {
+    int64_t struct_size;          /* = sizeof(cpsj_lsh_plan)                */
     double lambda_;
     int32_t accept_dist;          /* as cpsj_plan.accept_dist               */
     int32_t k;                    /* concatenation length                   */

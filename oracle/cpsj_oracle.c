@@ -327,7 +327,12 @@ static int64_t brute_force_step(const Ctx *c, Acc *acc, const int64_t *mem, int6
     return ns;
 }
 
-typedef struct { int64_t *mem; int64_t m; int64_t depth; uint64_t seed; } Node;
+typedef struct { int64_t *mem; int64_t m; int64_t depth; uint64_t seed; int64_t S; } Node;
+typedef struct { Node *v; int64_t len, cap; } NodeVec;
+static void nv_push(NodeVec *q, Node nd) {
+    if (q->len == q->cap) { q->cap = q->cap ? 2 * q->cap : 64; q->v = realloc(q->v, q->cap * sizeof(Node)); }
+    q->v[q->len++] = nd;
+}
 
 typedef struct { uint32_t v; int64_t idx; } VI;
 static int cmp_vi(const void *a, const void *b) {
@@ -336,65 +341,89 @@ static int cmp_vi(const void *a, const void *b) {
     return x->idx < y->idx ? -1 : (x->idx > y->idx);  /* stable */
 }
 
-/* one tree, depth first: cps:278-305; splitting cps:222-245 */
-static void run_tree(const Ctx *c, Acc *acc, uint64_t tree_seed) {
-    int64_t n = c->n;
-    int64_t scap = 64, sp = 0;
-    Node *stack = malloc(scap * sizeof(Node));
-    int64_t *root = malloc(n * sizeof(int64_t));
-    for (int64_t i = 0; i < n; i++) root[i] = i;
-    stack[sp++] = (Node){root, n, 0, tree_seed};
-    int64_t stack_total = n;
-    if (stack_total > acc->peak) acc->peak = stack_total;
+typedef struct { int64_t *surv; VI *buf; int32_t *sel; } Scratch;
+
+/* one node of _run_tree (cps:288-305): max_depth at pop, BruteForce step,
+ * depth cap, then split_buckets (cps:222-245) appending the children to
+ * `out` in the reference's order (position asc, value asc, groups >= 2)
+ * with seeds mix64(seed ^ mix64(t + 64 ell + k)) (cps:301).  Frees nd.mem.
+ * Returns the number of children appended. */
+static int64_t process_node(const Ctx *c, Acc *acc, Node nd, Scratch *w, NodeVec *out) {
+    if (nd.depth > acc->max_depth) acc->max_depth = nd.depth;
+    int64_t ns = brute_force_step(c, acc, nd.mem, nd.m, nd.seed, w->surv);
+    free(nd.mem);
+    if (ns < 2) return 0;
+    if (nd.depth >= c->depth_cap) {
+        if (acc->n_cap_events == acc->cap_events_cap) {
+            acc->cap_events_cap = acc->cap_events_cap ? 2 * acc->cap_events_cap : 16;
+            acc->cap_events = realloc(acc->cap_events, acc->cap_events_cap * sizeof(int64_t));
+        }
+        acc->cap_events[acc->n_cap_events++] = ns;
+        return 0;
+    }
     double p_sel = 1.0 / (c->lam * (double)c->t);
     uint64_t child_off = (uint64_t)c->t + 64ULL * (uint64_t)c->ell;
-    int64_t *surv = malloc(n * sizeof(int64_t));
-    VI *buf = malloc(n * sizeof(VI));
-    int32_t *sel = malloc(c->t * sizeof(int32_t));
-    while (sp) {
-        Node nd = stack[--sp];
-        stack_total -= nd.m;
-        if (nd.depth > acc->max_depth) acc->max_depth = nd.depth;
-        int64_t ns = brute_force_step(c, acc, nd.mem, nd.m, nd.seed, surv);
-        free(nd.mem);
-        if (ns < 2) continue;
-        if (nd.depth >= c->depth_cap) {
-            if (acc->n_cap_events == acc->cap_events_cap) {
-                acc->cap_events_cap = acc->cap_events_cap ? 2 * acc->cap_events_cap : 16;
-                acc->cap_events = realloc(acc->cap_events, acc->cap_events_cap * sizeof(int64_t));
-            }
-            acc->cap_events[acc->n_cap_events++] = ns;
-            continue;
+    int32_t nsel = 0;
+    for (int32_t i = 0; i < c->t; i++)
+        if (stream_uniform(nd.seed, (uint64_t)i) < p_sel) w->sel[nsel++] = i;
+    int64_t nchild = 0;
+    for (int32_t s = 0; s < nsel; s++) {
+        for (int64_t k = 0; k < ns; k++) {
+            w->buf[k].v = c->values[w->surv[k] * c->t + w->sel[s]];
+            w->buf[k].idx = k;
         }
-        int32_t nsel = 0;
-        for (int32_t i = 0; i < c->t; i++)
-            if (stream_uniform(nd.seed, (uint64_t)i) < p_sel) sel[nsel++] = i;
-        int64_t nchild = 0;
-        for (int32_t s = 0; s < nsel; s++) {
-            for (int64_t k = 0; k < ns; k++) {
-                buf[k].v = c->values[surv[k] * c->t + sel[s]];
-                buf[k].idx = k;
+        qsort(w->buf, ns, sizeof(VI), cmp_vi);
+        int64_t g = 0;
+        while (g < ns) {
+            int64_t e = g + 1;
+            while (e < ns && w->buf[e].v == w->buf[g].v) e++;
+            if (e - g >= 2) {
+                int64_t *cm = malloc((e - g) * sizeof(int64_t));
+                for (int64_t k = g; k < e; k++) cm[k - g] = w->surv[w->buf[k].idx];
+                nv_push(out, (Node){cm, e - g, nd.depth + 1, stream_word(nd.seed, child_off + (uint64_t)nchild), 0});
+                nchild++;
             }
-            qsort(buf, ns, sizeof(VI), cmp_vi);
-            int64_t g = 0;
-            while (g < ns) {
-                int64_t e = g + 1;
-                while (e < ns && buf[e].v == buf[g].v) e++;
-                if (e - g >= 2) {
-                    int64_t *cm = malloc((e - g) * sizeof(int64_t));
-                    for (int64_t k = g; k < e; k++) cm[k - g] = surv[buf[k].idx];
-                    if (sp == scap) { scap *= 2; stack = realloc(stack, scap * sizeof(Node)); }
-                    stack[sp++] = (Node){cm, e - g, nd.depth + 1,
-                                         stream_word(nd.seed, child_off + (uint64_t)nchild)};
-                    stack_total += e - g;
-                    nchild++;
-                }
-                g = e;
-            }
+            g = e;
         }
+    }
+    return nchild;
+}
+
+static Scratch scratch_new(const Ctx *c) {
+    Scratch w = {malloc((c->n ? c->n : 1) * sizeof(int64_t)), malloc((c->n ? c->n : 1) * sizeof(VI)),
+                 malloc(c->t * sizeof(int32_t))};
+    return w;
+}
+static void scratch_free(Scratch *w) { free(w->surv); free(w->buf); free(w->sel); }
+
+/* depth-first run of the subtree below node `nd` (cps:278-305).  `base` is
+ * the total size of the nodes below nd on the reference's stack when nd is
+ * popped, so the stack totals (peak_live_members, cps:292-304) are the
+ * reference's own. */
+static void run_subtree(const Ctx *c, Acc *acc, Node nd, int64_t base, Scratch *w) {
+    NodeVec stack = {0, 0, 0};
+    nv_push(&stack, nd);
+    int64_t stack_total = base + nd.m;
+    if (stack_total > acc->peak) acc->peak = stack_total;
+    while (stack.len) {
+        Node top = stack.v[--stack.len];
+        stack_total -= top.m;
+        int64_t before = stack.len;
+        int64_t nchild = process_node(c, acc, top, w, &stack);
+        for (int64_t k = before; k < stack.len; k++) stack_total += stack.v[k].m;
         if (nchild && stack_total > acc->peak) acc->peak = stack_total;
     }
-    free(stack); free(surv); free(buf); free(sel);
+    free(stack.v);
+}
+
+/* one tree, depth first: cps:278-305 */
+static void run_tree(const Ctx *c, Acc *acc, uint64_t tree_seed) {
+    int64_t n = c->n;
+    int64_t *root = malloc(n * sizeof(int64_t));
+    for (int64_t i = 0; i < n; i++) root[i] = i;
+    Scratch w = scratch_new(c);
+    run_subtree(c, acc, (Node){root, n, 0, tree_seed, 0}, 0, &w);
+    scratch_free(&w);
 }
 
 typedef struct { const Ctx *c; Acc *accs; const uint64_t *seeds; } TreeArgs;
@@ -436,6 +465,54 @@ int orc_self_join(const uint32_t *tok, const int64_t *off, const int64_t *sizes,
                             n_cap_events, 0);
 }
 
+/* merge per-repetition (or per-thread) accumulators: counters by sum/max,
+ * the pair union sorted by key and deduplicated (cps:308-319).  An
+ * accumulator with counted == 0 contributes its pairs, max_depth and peak
+ * but not pre/cand/res or depth-cap events (the frontier mode's part above
+ * the cut on ranks != 0). */
+static int merge_accs(Acc *accs, const int *counted, int64_t nacc, uint64_t **out_keys, double **out_sims,
+                      int64_t *out_n, int64_t *counters, int64_t **cap_events, int64_t *n_cap_events) {
+    int64_t total = 0, nev = 0;
+    for (int64_t r = 0; r < nacc; r++) {
+        total += accs[r].len;
+        if (!counted || counted[r]) nev += accs[r].n_cap_events;
+    }
+    KS *ks = malloc((total ? total : 1) * sizeof(KS));
+    int64_t *ev = malloc((nev ? nev : 1) * sizeof(int64_t));
+    int64_t k = 0, e = 0;
+    int err = 0;
+    memset(counters, 0, 5 * sizeof(int64_t));
+    for (int64_t r = 0; r < nacc; r++) {
+        Acc *a = &accs[r];
+        for (int64_t i = 0; i < a->len; i++) {
+            uint64_t lo = (uint64_t)(a->a[i] < a->b[i] ? a->a[i] : a->b[i]);
+            uint64_t hi = (uint64_t)(a->a[i] < a->b[i] ? a->b[i] : a->a[i]);
+            ks[k].key = (lo << 32) | hi;
+            ks[k].sim = a->sim[i];
+            k++;
+        }
+        if (!counted || counted[r]) {
+            for (int64_t i = 0; i < a->n_cap_events; i++) ev[e++] = a->cap_events[i];
+            counters[0] += a->pre; counters[1] += a->cand; counters[2] += a->res;
+        }
+        if (a->max_depth > counters[3]) counters[3] = a->max_depth;
+        if (a->peak > counters[4]) counters[4] = a->peak;
+        err |= a->error;
+        free(a->a); free(a->b); free(a->sim); free(a->cap_events);
+    }
+    qsort(ks, total, sizeof(KS), cmp_ks);
+    int64_t u = 0;
+    for (int64_t i = 0; i < total; i++)
+        if (u == 0 || ks[u - 1].key != ks[i].key) ks[u++] = ks[i];
+    uint64_t *keys = malloc((u ? u : 1) * sizeof(uint64_t));
+    double *sims = malloc((u ? u : 1) * sizeof(double));
+    for (int64_t i = 0; i < u; i++) { keys[i] = ks[i].key; sims[i] = ks[i].sim; }
+    free(ks);
+    *out_keys = keys; *out_sims = sims; *out_n = u;
+    *cap_events = ev; *n_cap_events = nev;
+    return err;
+}
+
 int orc_self_join_ct(const uint32_t *tok, const int64_t *off, const int64_t *sizes, int64_t n,
                      const uint32_t *values, int32_t t, const uint64_t *sketch, int32_t ell,
                      double lam, double eps, int32_t limit, int32_t kstar, int32_t depth_cap,
@@ -449,40 +526,106 @@ int orc_self_join_ct(const uint32_t *tok, const int64_t *off, const int64_t *siz
         TreeArgs ta = {&c, accs, rep_seeds};
         parallel_for(reps, 1, nthreads, tree_body, &ta);
     }
-    int64_t total = 0, nev = 0;
-    for (int32_t r = 0; r < reps; r++) { total += accs[r].len; nev += accs[r].n_cap_events; }
-    KS *ks = malloc((total ? total : 1) * sizeof(KS));
-    int64_t *ev = malloc((nev ? nev : 1) * sizeof(int64_t));
-    int64_t k = 0, e = 0;
-    int err = 0;
-    memset(counters, 0, 5 * sizeof(int64_t));
-    for (int32_t r = 0; r < reps; r++) {
-        Acc *a = &accs[r];
-        for (int64_t i = 0; i < a->len; i++) {
-            uint64_t lo = (uint64_t)(a->a[i] < a->b[i] ? a->a[i] : a->b[i]);
-            uint64_t hi = (uint64_t)(a->a[i] < a->b[i] ? a->b[i] : a->a[i]);
-            ks[k].key = (lo << 32) | hi;
-            ks[k].sim = a->sim[i];
-            k++;
-        }
-        for (int64_t i = 0; i < a->n_cap_events; i++) ev[e++] = a->cap_events[i];
-        counters[0] += a->pre; counters[1] += a->cand; counters[2] += a->res;
-        if (a->max_depth > counters[3]) counters[3] = a->max_depth;
-        if (a->peak > counters[4]) counters[4] = a->peak;
-        err |= a->error;
-        free(a->a); free(a->b); free(a->sim); free(a->cap_events);
-    }
+    int err = merge_accs(accs, NULL, reps, out_keys, out_sims, out_n, counters, cap_events, n_cap_events);
     free(accs);
-    qsort(ks, total, sizeof(KS), cmp_ks);
-    int64_t u = 0;
-    for (int64_t i = 0; i < total; i++)
-        if (u == 0 || ks[u - 1].key != ks[i].key) ks[u++] = ks[i];
-    uint64_t *keys = malloc((u ? u : 1) * sizeof(uint64_t));
-    double *sims = malloc((u ? u : 1) * sizeof(double));
-    for (int64_t i = 0; i < u; i++) { keys[i] = ks[i].key; sims[i] = ks[i].sim; }
-    free(ks);
-    *out_keys = keys; *out_sims = sims; *out_n = u;
-    *cap_events = ev; *n_cap_events = nev;
+    return err;
+}
+
+/* Frontier sharding (the B200 library's cpsj_plan.frontier_*; SURVEY 8(e);
+ * not a reference feature -- its contract is that the union over ranks is
+ * cpsjoin_self, cps:331-351).  Every rank expands all repetition trees
+ * breadth-first down to depth `fdepth` (level order: repetitions in order,
+ * children in parent order, each parent's children in the reference's
+ * order), then keeps its share of that level -- node i belongs to rank
+ * floor(ranks (2 C_i + c_i) / (2 C_N)), c = m + m (m - 1) / 64 for a leaf
+ * (m <= limit), m * bit_length(m) otherwise, C_i the cost of nodes before i
+ * -- and runs the kept subtrees depth first with their reference stack
+ * base S (S(child_j) = S(parent) + sizes of children before j).  Rank 0
+ * reports the counters of the part above the cut; every rank reports its
+ * pairs (ranks != 0 none from above the cut when no node reaches it), the
+ * cut depth as reached, and the stack peak of what it expanded. */
+typedef struct { const Ctx *c; Acc *accs; Node *nodes; const int64_t *kept; Scratch *w; } KeptArgs;
+static void kept_body(void *p, int64_t lo, int64_t hi, int tid) {
+    KeptArgs *a = p;
+    for (int64_t i = lo; i < hi; i++) {
+        Node nd = a->nodes[a->kept[i]];
+        run_subtree(a->c, &a->accs[tid], nd, nd.S, &a->w[tid]);
+    }
+}
+
+static int64_t frontier_cost(int64_t m, int32_t limit) {
+    if (m <= limit) return m + m * (m - 1) / 64;
+    int64_t b = 0;
+    while ((m >> b) != 0) ++b;
+    return m * b;
+}
+
+int orc_self_join_frontier(const uint32_t *tok, const int64_t *off, const int64_t *sizes, int64_t n,
+                           const uint32_t *values, int32_t t, const uint64_t *sketch, int32_t ell,
+                           double lam, double eps, int32_t limit, int32_t kstar, int32_t depth_cap,
+                           const uint64_t *rep_seeds, int32_t reps, int nthreads,
+                           int32_t rank, int32_t ranks, int32_t fdepth,
+                           uint64_t **out_keys, double **out_sims, int64_t *out_n,
+                           int64_t *counters, int64_t **cap_events, int64_t *n_cap_events) {
+    Ctx c = {tok, off, sizes, n, values, t, sketch, ell, lam, eps, limit, kstar, depth_cap, 0};
+    int nt = resolve_threads(nthreads);
+    Acc *accs = calloc(nt + 1, sizeof(Acc));   /* [0] = above the cut, [1 + tid] = kept subtrees */
+    int *counted = calloc(nt + 1, sizeof(int));
+    counted[0] = rank == 0;
+    for (int i = 1; i <= nt; i++) counted[i] = 1;
+    if (n >= 2 && reps > 0) {
+        Acc *top = &accs[0];
+        top->peak = n;
+        Scratch w = scratch_new(&c);
+        NodeVec level = {0, 0, 0};
+        for (int32_t r = 0; r < reps; r++) {
+            int64_t *root = malloc(n * sizeof(int64_t));
+            for (int64_t i = 0; i < n; i++) root[i] = i;
+            nv_push(&level, (Node){root, n, 0, rep_seeds[r], 0});
+        }
+        for (int32_t d = 0; d < fdepth && level.len; d++) {
+            NodeVec next = {0, 0, 0};
+            for (int64_t i = 0; i < level.len; i++) {
+                Node nd = level.v[i];
+                int64_t before = next.len;
+                int64_t nchild = process_node(&c, top, nd, &w, &next);
+                int64_t S = nd.S;
+                for (int64_t k = before; k < next.len; k++) { next.v[k].S = S; S += next.v[k].m; }
+                if (nchild && S > top->peak) top->peak = S;
+            }
+            free(level.v);
+            level = next;
+        }
+        scratch_free(&w);
+        if (level.len) {
+            if (fdepth > top->max_depth) top->max_depth = fdepth;
+            int64_t total = 0;
+            for (int64_t i = 0; i < level.len; i++) total += frontier_cost(level.v[i].m, limit);
+            int64_t *kept = malloc(level.len * sizeof(int64_t));
+            int64_t nk = 0, before = 0;
+            for (int64_t i = 0; i < level.len; i++) {
+                int64_t cst = frontier_cost(level.v[i].m, limit);
+                __int128 num = (__int128)ranks * (__int128)(2 * before + cst);
+                int64_t owner = (int64_t)(num / (__int128)(2 * total));
+                if (owner == rank) kept[nk++] = i;
+                else free(level.v[i].mem);
+                before += cst;
+            }
+            Scratch *ws = malloc(nt * sizeof(Scratch));
+            for (int i = 0; i < nt; i++) ws[i] = scratch_new(&c);
+            KeptArgs ka = {&c, accs + 1, level.v, kept, ws};
+            parallel_for(nk, 1, nt, kept_body, &ka);
+            for (int i = 0; i < nt; i++) scratch_free(&ws[i]);
+            free(ws);
+            free(kept);
+        } else if (rank != 0) {
+            top->len = 0;  /* the trees ended above the cut: rank 0 reports all of them */
+        }
+        free(level.v);
+    }
+    int err = merge_accs(accs, counted, nt + 1, out_keys, out_sims, out_n, counters, cap_events, n_cap_events);
+    free(accs);
+    free(counted);
     return err;
 }
 

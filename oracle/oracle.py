@@ -31,8 +31,7 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_SO):
-            build()
+        build()  # rebuilds only when the source is newer than the library
         L = ctypes.CDLL(_SO)
         P = ctypes.c_void_p
         i64, i32, u64, dbl = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
@@ -48,6 +47,9 @@ def lib():
                                     P, ctypes.POINTER(P), ctypes.POINTER(i64)]
         L.orc_self_join_ct.restype = ctypes.c_int
         L.orc_self_join_ct.argtypes = L.orc_self_join.argtypes + [ctypes.c_int]
+        L.orc_self_join_frontier.restype = ctypes.c_int
+        L.orc_self_join_frontier.argtypes = L.orc_self_join.argtypes[:16] + [i32, i32, i32] + \
+            L.orc_self_join.argtypes[16:]
         L.orc_exact_join.restype = ctypes.c_int
         L.orc_exact_join.argtypes = [P, P, i64, ctypes.c_uint32, dbl, ctypes.c_int,
                                      ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)]
@@ -162,8 +164,11 @@ def _take(ptr, n, dtype):
 
 def self_join(tokens, offsets, sizes, values, sketches, lam: float, *, epsilon=0.1, limit=250,
               delta=0.05, repetitions=10, seed=0, depth_cap=64, threads: int = 0,
-              use_count_table: bool = False) -> JoinOut:
-    """cpsjoin.py:331-351 on explicit arrays (self-join, source_ids = arange)."""
+              use_count_table: bool = False, frontier=None, rep_seed_list=None) -> JoinOut:
+    """cpsjoin.py:331-351 on explicit arrays (self-join, source_ids = arange).
+    ``frontier=(rank, ranks, depth)``: this rank's share of a frontier-sharded
+    join (orc_self_join_frontier; the union over ranks is the join itself).
+    ``rep_seed_list`` replaces the derived repetition seeds."""
     tok, off = _csr(tokens, offsets)
     sizes = np.ascontiguousarray(sizes, dtype=np.int64)
     values = np.ascontiguousarray(values, dtype=np.uint32)
@@ -171,10 +176,24 @@ def self_join(tokens, offsets, sizes, values, sketches, lam: float, *, epsilon=0
     n, t = values.shape
     ell = sk.shape[1]
     ks = kstar(lam, delta, 64 * ell)
-    seeds = rep_seeds(seed, repetitions)
+    seeds = rep_seeds(seed, repetitions) if rep_seed_list is None else \
+        np.ascontiguousarray(rep_seed_list, dtype=np.uint64)
+    repetitions = len(seeds)
     kp, sp, cp = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
     nk, nc = ctypes.c_int64(), ctypes.c_int64()
     counters = np.zeros(5, dtype=np.int64)
+    if frontier is not None:
+        if use_count_table:
+            raise ValueError("frontier mode has no count-table rule")
+        rank, ranks, fdepth = (int(x) for x in frontier)
+        err = lib().orc_self_join_frontier(_p(tok), _p(off), _p(sizes), n, _p(values), t, _p(sk), ell,
+                                           float(lam), float(epsilon), int(limit), ks, int(depth_cap),
+                                           _p(seeds), int(repetitions), threads, rank, ranks, fdepth,
+                                           ctypes.byref(kp), ctypes.byref(sp), ctypes.byref(nk),
+                                           _p(counters), ctypes.byref(cp), ctypes.byref(nc))
+        return JoinOut(_take(kp, nk.value, np.uint64), _take(sp, nk.value, np.float64), int(counters[0]),
+                       int(counters[1]), int(counters[2]), int(counters[3]), int(counters[4]),
+                       _take(cp, nc.value, np.int64), int(err))
     err = lib().orc_self_join_ct(_p(tok), _p(off), _p(sizes), n, _p(values), t, _p(sk), ell,
                                  float(lam), float(epsilon), int(limit), ks, int(depth_cap),
                                  _p(seeds), int(repetitions), threads,

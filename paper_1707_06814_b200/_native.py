@@ -14,24 +14,34 @@ from .build import SO
 P = ctypes.c_void_p
 i32, i64, u32, u64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double
 
-CPSJ_E_ARG, CPSJ_E_CUDA, CPSJ_E_OOM, CPSJ_E_PICK = -1, -2, -3, -4
+CPSJ_E_ARG, CPSJ_E_CUDA, CPSJ_E_OOM, CPSJ_E_PICK, CPSJ_E_ABI = -1, -2, -3, -4, -5
+ABI_VERSION = (2 << 16) | 0      # CPSJ_ABI_VERSION of include/cpsjoin_b200.h
 
 
-class Inputs(ctypes.Structure):
-    _fields_ = [("d_tokens", P), ("d_offsets", P), ("d_sizes", P), ("n", i64),
+class _Sized(ctypes.Structure):
+    """A parameter struct whose first field is ``struct_size`` (the ABI
+    guard of include/cpsjoin_b200.h): filled in automatically, so positional
+    construction takes the remaining fields in header order."""
+
+    def __init__(self, *args, **kw):
+        super().__init__(ctypes.sizeof(type(self)), *args, **kw)
+
+
+class Inputs(_Sized):
+    _fields_ = [("struct_size", i64), ("d_tokens", P), ("d_offsets", P), ("d_sizes", P), ("n", i64),
                 ("d_values", P), ("t", i32), ("d_sketch", P), ("ell", i32), ("d_side", P)]
 
 
-class Plan(ctypes.Structure):
-    _fields_ = [("lambda_", dbl), ("limit", i32), ("depth_cap", i32), ("accept_dist", i32),
+class Plan(_Sized):
+    _fields_ = [("struct_size", i64), ("lambda_", dbl), ("limit", i32), ("depth_cap", i32), ("accept_dist", i32),
                 ("flag_dist", i32), ("split_p", dbl), ("h_rep_seeds", P), ("n_reps", i32), ("value_bits", i32),
                 ("use_count_table", i32), ("count_threshold", dbl), ("frontier_rank", i32),
                 ("frontier_ranks", i32), ("frontier_depth", i32)]
 
 
-class LshPlan(ctypes.Structure):
-    _fields_ = [("lambda_", dbl), ("accept_dist", i32), ("k", i32), ("n_reps", i32), ("h_positions", P),
-                ("h_rep_seeds", P), ("cost_only", i32)]
+class LshPlan(_Sized):
+    _fields_ = [("struct_size", i64), ("lambda_", dbl), ("accept_dist", i32), ("k", i32), ("n_reps", i32),
+                ("h_positions", P), ("h_rep_seeds", P), ("cost_only", i32)]
 
 
 class IngestStats(ctypes.Structure):
@@ -50,14 +60,15 @@ EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_err
            "cpsj_launch_counts", "cpsj_frequency_order", "cpsj_exact_join",
            "cpsj_lsh_join", "cpsj_ingest_lists", "cpsj_parse_text", "cpsj_ingest_result_device", "cpsj_ingest_copy",
            "cpsj_minhash_sketch_multi", "cpsj_xbuf_create", "cpsj_xbuf_open", "cpsj_xbuf_close",
-           "cpsj_minhash_embed"]
+           "cpsj_minhash_embed", "cpsj_copy_async"]
 
 MAX_DSTS = 8
 IPC_HANDLE_BYTES = 64
 
 
-class K1Dsts(ctypes.Structure):
-    _fields_ = [("d_values", P * MAX_DSTS), ("d_sketch", P * MAX_DSTS), ("n_dsts", i32), ("row0", i64)]
+class K1Dsts(_Sized):
+    _fields_ = [("struct_size", i64), ("d_values", P * MAX_DSTS), ("d_sketch", P * MAX_DSTS), ("n_dsts", i32),
+                ("row0", i64)]
 
 PROF_CLASSES = ["k1_minhash", "k4_leaf", "point", "node", "split", "k5_verify", "k6_dedup", "plan"]
 
@@ -80,6 +91,9 @@ def load(path: str | None = None):
             raise ImportError(f"CUDA library not built: {so} (run python -m paper_1707_06814_b200.build)")
         L = ctypes.CDLL(so)
         L.cpsj_version.restype = ctypes.c_int
+        if L.cpsj_version() != ABI_VERSION:
+            raise ImportError(f"{so}: ABI version {L.cpsj_version():#x}, this binding expects {ABI_VERSION:#x} "
+                              "(rebuild with python -m paper_1707_06814_b200.build)")
         L.cpsj_ctx_create.argtypes = [ctypes.c_int, ctypes.POINTER(P)]
         L.cpsj_ctx_destroy.argtypes = [P]
         L.cpsj_last_error.restype = ctypes.c_char_p
@@ -105,6 +119,7 @@ def load(path: str | None = None):
         L.cpsj_xbuf_create.argtypes = [P, i64, ctypes.POINTER(P), P]
         L.cpsj_xbuf_open.argtypes = [P, P, ctypes.POINTER(P)]
         L.cpsj_xbuf_close.argtypes = [P, P, i32]
+        L.cpsj_copy_async.argtypes = [P, P, P, i64, P]
         L.cpsj_exact_join.argtypes = [P, P, P, i64, i64, dbl, i32, ctypes.POINTER(JoinStats), P]
         _lib = L
         return L
@@ -116,6 +131,8 @@ def check(ctx, rc: int) -> None:
     msg = load().cpsj_last_error(ctx).decode(errors="replace") if ctx else "error"
     if rc == CPSJ_E_ARG:
         raise ValueError(msg)
+    if rc == CPSJ_E_ABI:
+        raise TypeError(msg)
     if rc == CPSJ_E_PICK:
         raise IndexError(msg)
     if rc == CPSJ_E_OOM:

@@ -4,6 +4,7 @@
 
 #include <cstring>
 #include <new>
+#include <string>
 
 #include "cpsj_common.cuh"
 
@@ -32,11 +33,22 @@ int guarded(cpsj_ctx *ctx, F &&f) {
     }
 }
 
+// every parameter struct starts with the caller's sizeof: a caller built
+// against another header is rejected instead of read past its end
+template <typename T>
+void require_abi(const T *p, const char *name) {
+    if (p != nullptr && p->struct_size != (int64_t)sizeof(T))
+        throw cpsj::Error{CPSJ_E_ABI, std::string(name) + ".struct_size is " + std::to_string(p->struct_size) +
+                                          ", this library expects " + std::to_string(sizeof(T)) +
+                                          " (ABI version " + std::to_string(CPSJ_ABI_MAJOR) + "." +
+                                          std::to_string(CPSJ_ABI_MINOR) + ")"};
+}
+
 }  // namespace
 
 extern "C" {
 
-int cpsj_version(void) { return (1 << 16) | 0; }
+int cpsj_version(void) { return CPSJ_ABI_VERSION; }
 
 int cpsj_ctx_create(int device, cpsj_ctx **out) {
     if (out == nullptr) return CPSJ_E_ARG;
@@ -156,6 +168,7 @@ int cpsj_minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint3
     if (!ctx) return CPSJ_E_ARG;
     return guarded(ctx, [&] {
         cpsj::require(dsts != nullptr, "null destinations");
+        require_abi(dsts, "cpsj_k1_dsts");
         cpsj::require(n_sets == 0 || (d_tokens && d_offsets), "null CSR pointers");
         cpsj::require(dsts->n_dsts >= 1 && dsts->n_dsts <= CPSJ_MAX_DSTS, "1 to 8 destinations");
         cpsj::K1Out out{};
@@ -209,11 +222,23 @@ int cpsj_xbuf_close(cpsj_ctx *ctx, void *d_ptr, int32_t opened) {
     });
 }
 
+int cpsj_copy_async(cpsj_ctx *ctx, void *dst, const void *src, int64_t bytes, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(bytes >= 0 && (bytes == 0 || (dst && src)), "bad copy arguments");
+        if (bytes == 0) return;
+        CPSJ_CUDA(cudaSetDevice(ctx->device));
+        CPSJ_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+    });
+}
+
 int cpsj_self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
                    void *stream) {
     if (!ctx) return CPSJ_E_ARG;
     return guarded(ctx, [&] {
         cpsj::require(in && plan && stats, "null argument");
+        require_abi(in, "cpsj_inputs");
+        require_abi(plan, "cpsj_plan");
         cpsj::require(in->n < (int64_t)1 << 31, "at most 2^31 - 1 sets");
         cpsj::require(in->n < 2 || (in->d_tokens && in->d_offsets && in->d_sizes && in->d_values && in->d_sketch),
                       "null input pointers");
@@ -253,6 +278,8 @@ int cpsj_lsh_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_lsh_plan *pla
     if (!ctx) return CPSJ_E_ARG;
     return guarded(ctx, [&] {
         cpsj::require(in && plan && stats, "null argument");
+        require_abi(in, "cpsj_inputs");
+        require_abi(plan, "cpsj_lsh_plan");
         cpsj::require(in->n < (int64_t)1 << 31, "at most 2^31 - 1 sets");
         cpsj::require(in->n < 2 || (in->d_tokens && in->d_offsets && in->d_sizes && in->d_values &&
                                     (in->d_sketch || plan->cost_only)),

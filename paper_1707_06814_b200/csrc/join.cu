@@ -60,7 +60,19 @@ struct DevCounters {
     unsigned long long def_m;    // their members
     unsigned long long def_slot; // allocation cursors of k_defer_copy
     unsigned long long def_mtop;
+    int verr;                    // a MinHash value >= 2^value_bits reached a
+                                 // split key (the plan's value_bits is wrong)
 };
+
+// a split/count key packs (segment << vbits) | value: a value that does not
+// fit vbits would corrupt the segment bits, so it is reported, not packed
+__device__ __forceinline__ uint32_t checked_value(uint32_t v, int vbits, int *verr) {
+    if (vbits < 32 && (v >> vbits) != 0u) {
+        atomicExch(verr, 1);
+        v &= (1u << vbits) - 1u;
+    }
+    return v;
+}
 
 inline unsigned blocks_for(int64_t n, int tpb = TPB) {
     return (unsigned)std::max<int64_t>(1, (n + tpb - 1) / tpb);
@@ -728,7 +740,7 @@ __global__ void k_build_keys(int64_t E, const int64_t *__restrict__ e_off, int64
                              const int64_t *__restrict__ im_off, const int64_t *__restrict__ fscan,
                              const int16_t *__restrict__ sel_pos, int t, const int32_t *__restrict__ surv,
                              const uint32_t *__restrict__ values, int vbits, KT *__restrict__ keys,
-                             int32_t *__restrict__ vals) {
+                             int32_t *__restrict__ vals, int *__restrict__ verr) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t k = warp_segment(e_off, n_int + 1, e);
     if (e >= E) return;
@@ -737,7 +749,7 @@ __global__ void k_build_keys(int64_t E, const int64_t *__restrict__ e_off, int64
     const int64_t r = local / s, p = local - r * s;
     const int pos = sel_pos[k * t + r];
     const int32_t x = surv[(im_off[k] - fscan[im_off[k]]) + p];
-    keys[e] = (KT)(((uint64_t)(seg_off[k] + r) << vbits) | values[(size_t)x * t + pos]);
+    keys[e] = (KT)(((uint64_t)(seg_off[k] + r) << vbits) | checked_value(values[(size_t)x * t + pos], vbits, verr));
     vals[e] = x;
 }
 
@@ -861,15 +873,15 @@ __global__ void k_verify(int64_t nc, const int2 *__restrict__ cand, const uint32
     }
 }
 
-// frontier cut: keep nodes rank, rank + ranks, ... of the level (node
-// records only; members stay where they are)
-__global__ void k_frontier_keep(int64_t Nk, int32_t rank, int32_t ranks, const int64_t *__restrict__ off,
+// frontier cut: keep the level's nodes listed in `idx` (node records only;
+// members stay where they are)
+__global__ void k_frontier_keep(int64_t Nk, const int64_t *__restrict__ idx, const int64_t *__restrict__ off,
                                 const int32_t *__restrict__ cnt, const uint64_t *__restrict__ seed,
                                 const int64_t *__restrict__ S, int64_t *__restrict__ off2, int32_t *__restrict__ cnt2,
                                 uint64_t *__restrict__ seed2, int64_t *__restrict__ S2) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= Nk) return;
-    const int64_t i = j * ranks + rank;
+    const int64_t i = idx[j];
     off2[j] = off[i];
     cnt2[j] = cnt[i];
     seed2[j] = seed[i];
@@ -1240,7 +1252,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) k_subtree(const SubtreeArgs a) 
             // by value; the index order of equal values is kept
 #pragma unroll 4
             for (int e = tid; e < s; e += ST_THREADS) {
-                sval[e] = __ldg(a.values + (size_t)surv[e] * t + pos);
+                sval[e] = checked_value(__ldg(a.values + (size_t)surv[e] * t + pos), a.vbits, &ctr->verr);
                 sidx[e] = (uint16_t)e;
             }
             __syncthreads();
@@ -1613,13 +1625,13 @@ void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level
 __global__ void k_ct_keys(int64_t EN, int t, const int64_t *__restrict__ im_off, int64_t n_int,
                           const int64_t *__restrict__ ilist, const int64_t *__restrict__ nd_off,
                           const int32_t *__restrict__ members, const uint32_t *__restrict__ values, int vbits,
-                          uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+                          uint64_t *__restrict__ keys, int32_t *__restrict__ vals, int *__restrict__ verr) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= EN) return;
     const int64_t q = e / t, i = e - q * t;
     const int64_t k = upper_bound_i64(im_off, n_int + 1, q) - 1;
     const int32_t x = members[nd_off[ilist[k]] + (q - im_off[k])];
-    keys[e] = ((uint64_t)(k * t + i) << vbits) | values[(size_t)x * t + i];
+    keys[e] = ((uint64_t)(k * t + i) << vbits) | checked_value(values[(size_t)x * t + i], vbits, verr);
     vals[e] = (int32_t)q;
 }
 
@@ -1649,13 +1661,13 @@ __global__ void k_ct_flags(int64_t Mi, int t, const int64_t *__restrict__ im_off
 
 void count_table_flags(cpsj_ctx *ctx, Driver &drv, const cpsj_inputs *in, const cpsj_plan *plan, int vbits,
                        int64_t n_int, int64_t Mi, const int64_t *ilist, const int64_t *im_off, const Level &lv,
-                       int64_t *flags, cudaStream_t st) {
+                       int64_t *flags, int *verr, cudaStream_t st) {
     const int t = in->t;
     const int64_t EN = Mi * t;
     DevBuf<uint64_t> keys(EN, st), keys2(EN, st);
     DevBuf<int32_t> vals(EN, st), vals2(EN, st);
     k_ct_keys<<<blocks_for(EN), TPB, 0, st>>>(EN, t, im_off, n_int, ilist, lv.off.p, lv.members.p, in->d_values,
-                                              vbits, keys.p, vals.p);
+                                              vbits, keys.p, vals.p, verr);
     CPSJ_LAUNCH_CHECK();
     int end_bit = vbits;
     while (end_bit < 64 && ((uint64_t)(n_int * t) >> (end_bit - vbits)) > 0) ++end_bit;
@@ -1961,6 +1973,31 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
                 (long long)NL, (long long)hc.leaf_m, hc.max_depth);
 }
 
+// the frontier cut of cpsj_plan: node i of the cut level belongs to rank
+// floor(ranks (2 C_i + c_i) / (2 C_N)), c = m + m (m - 1) / 64 for a leaf
+// (m <= limit) and m * bit_length(m) for an internal node
+std::vector<int64_t> frontier_share(const std::vector<int32_t> &cnt, int32_t limit, int32_t rank, int32_t ranks) {
+    auto cost = [&](int64_t m) -> int64_t {
+        if (m <= limit) return m + m * (m - 1) / 64;
+        int64_t b = 0;
+        while ((m >> b) != 0) ++b;
+        return m * b;
+    };
+    int64_t total = 0;
+    for (int32_t m : cnt) total += cost(m);
+    std::vector<int64_t> kept;
+    int64_t before = 0;
+    for (size_t i = 0; i < cnt.size(); ++i) {
+        const int64_t c = cost(cnt[i]);
+        // 128-bit product: total may exceed 2^63 / ranks on huge levels
+        const __int128 num = (__int128)ranks * (__int128)(2 * before + c);
+        const int64_t owner = total > 0 ? (int64_t)(num / (__int128)(2 * total)) : (int64_t)i % ranks;
+        if (owner == rank) kept.push_back((int64_t)i);
+        before += c;
+    }
+    return kept;
+}
+
 }  // namespace
 
 void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
@@ -2073,19 +2110,26 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             snap_cand = em.total_cand;
             snap_caps = (int64_t)ctx->cap_events.size();
             cut_done = true;
-            const int64_t Nk = lv.N > plan->frontier_rank
-                                   ? (lv.N - plan->frontier_rank + plan->frontier_ranks - 1) / plan->frontier_ranks
-                                   : 0;
+            // size-balanced contiguous cut (cpsj_plan): every rank derives
+            // the same owner for every node from the level's node sizes
+            std::vector<int32_t> hcnt((size_t)lv.N);
+            CPSJ_CUDA(cudaMemcpyAsync(hcnt.data(), lv.cnt.p, (size_t)lv.N * 4, cudaMemcpyDeviceToHost, st));
+            CPSJ_CUDA(cudaStreamSynchronize(st));
+            const std::vector<int64_t> kept =
+                frontier_share(hcnt, plan->limit, plan->frontier_rank, plan->frontier_ranks);
+            const int64_t Nk = (int64_t)kept.size();
             nx.off.ensure(std::max<int64_t>(Nk, 1), st);
             nx.cnt.ensure(std::max<int64_t>(Nk, 1), st);
             nx.seed.ensure(std::max<int64_t>(Nk, 1), st);
             nx.S.ensure(std::max<int64_t>(Nk, 1), st);
             if (Nk > 0) {
-                k_frontier_keep<<<blocks_for(Nk), TPB, 0, st>>>(Nk, plan->frontier_rank, plan->frontier_ranks,
-                                                               lv.off.p, lv.cnt.p, lv.seed.p, lv.S.p, nx.off.p,
-                                                               nx.cnt.p, nx.seed.p, nx.S.p);
+                DevBuf<int64_t> didx(Nk, st);
+                CPSJ_CUDA(cudaMemcpyAsync(didx.p, kept.data(), Nk * 8, cudaMemcpyHostToDevice, st));
+                k_frontier_keep<<<blocks_for(Nk), TPB, 0, st>>>(Nk, didx.p, lv.off.p, lv.cnt.p, lv.seed.p, lv.S.p,
+                                                               nx.off.p, nx.cnt.p, nx.seed.p, nx.S.p);
                 CPSJ_LAUNCH_CHECK();
                 ctx->launches++;
+                CPSJ_CUDA(cudaStreamSynchronize(st));  // `kept` goes out of scope
             }
             std::swap(lv.off, nx.off);
             std::swap(lv.cnt, nx.cnt);
@@ -2217,7 +2261,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             flags.ensure(Mi + 1, st);
             fscan.ensure(Mi + 1, st);
             if (plan->use_count_table)
-                count_table_flags(ctx, drv, in, plan, vbits, n_int, Mi, ilist.p, im_off_c.p, lv, flags.p, st);
+                count_table_flags(ctx, drv, in, plan, vbits, n_int, Mi, ilist.p, im_off_c.p, lv, flags.p,
+                                  &ctr.p->verr, st);
             else
                 k_flags<<<blocks_for(Mi + 1), TPB, 0, st>>>(Mi, im_off_c.p, n_int, ilist.p, lv.off.p,
                                                             lv.members.p, in->d_sketch, ell, nsk.p, plan->flag_dist,
@@ -2300,11 +2345,13 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             if (keys32)
                 k_build_keys<uint32_t><<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p,
                                                                       im_off_c.p, fscan.p, sel_pos.p, t, surv.p,
-                                                                      in->d_values, vbits, k32, vals.p);
+                                                                      in->d_values, vbits, k32, vals.p,
+                                                                      &ctr.p->verr);
             else
                 k_build_keys<uint64_t><<<blocks_for(E), TPB, 0, st>>>(E, e_off.p, n_int, seg_off.p, nsel.p,
                                                                       im_off_c.p, fscan.p, sel_pos.p, t, surv.p,
-                                                                      in->d_values, vbits, keys.p, vals.p);
+                                                                      in->d_values, vbits, keys.p, vals.p,
+                                                                      &ctr.p->verr);
             CPSJ_LAUNCH_CHECK();
             size_t bytes = 0;
             if (keys32)
@@ -2383,6 +2430,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     const DevCounters hc = em.finish(drv);
     const int64_t nres = (int64_t)hc.res_n;
     if (hc.err) throw Error{CPSJ_E_PICK, "node-sketch pick index out of range (uniform draw == 1.0)"};
+    if (hc.verr) throw Error{CPSJ_E_ARG, "a MinHash value is >= 2^value_bits (cpsj_plan.value_bits too small)"};
     stats->n_pairs = ctx->n_pairs;
     stats->pre_candidates = (int64_t)hc.pre;
     stats->candidates = em.total_cand;

@@ -128,7 +128,7 @@ class PeerArrays:
     (cpsj_minhash_sketch_multi), so the all-gather of the set-sharded
     embedding happens inside the kernel's epilogue."""
 
-    def __init__(self, ctx, n: int, t: int, ell: int, rank: int, world: int, group=None):
+    def __init__(self, ctx, n: int, t: int, ell: int, rank: int, world: int, group=None, nnz: int | None = None):
         import ctypes
 
         import torch
@@ -138,9 +138,15 @@ class PeerArrays:
         if world > 8:
             raise ValueError("peer exchange supports up to 8 ranks per node")
         self.ctx, self.n, self.t, self.ell, self.rank, self.world = ctx, n, t, ell, rank, world
+        self.nnz = nnz
         self._own, self._opened = [], []
         handles = []
-        for nbytes in (max(1, n * t * 4), max(1, n * ell * 8)):
+        sizes = [max(1, n * t * 4), max(1, n * ell * 8)]
+        if nnz is not None:
+            # the CSR too (tokens, offsets): each rank uploads only its slice
+            # and pushes it to the peers (csr_from_host_sharded)
+            sizes += [max(1, nnz * 4), (n + 1) * 8]
+        for nbytes in sizes:
             p = P()
             h = (ctypes.c_uint8 * IPC_HANDLE_BYTES)()
             ctx.check(ctx.lib.cpsj_xbuf_create(ctx.handle, nbytes, ctypes.byref(p), h))
@@ -148,24 +154,29 @@ class PeerArrays:
             handles.append(bytes(h))
         gathered = [None] * world
         dist.all_gather_object(gathered, handles, group=group)
-        self.values_ptrs, self.sketch_ptrs = [], []
+        self.values_ptrs, self.sketch_ptrs, self.tokens_ptrs, self.offsets_ptrs = [], [], [], []
         for r in range(world):
             if r == rank:
-                self.values_ptrs.append(self._own[0])
-                self.sketch_ptrs.append(self._own[1])
-                continue
-            ptrs = []
-            for hb in gathered[r]:
-                p = P()
-                buf = (ctypes.c_uint8 * IPC_HANDLE_BYTES).from_buffer_copy(hb)
-                ctx.check(ctx.lib.cpsj_xbuf_open(ctx.handle, buf, ctypes.byref(p)))
-                self._opened.append(int(p.value))
-                ptrs.append(int(p.value))
+                ptrs = list(self._own)
+            else:
+                ptrs = []
+                for hb in gathered[r]:
+                    p = P()
+                    buf = (ctypes.c_uint8 * IPC_HANDLE_BYTES).from_buffer_copy(hb)
+                    ctx.check(ctx.lib.cpsj_xbuf_open(ctx.handle, buf, ctypes.byref(p)))
+                    self._opened.append(int(p.value))
+                    ptrs.append(int(p.value))
             self.values_ptrs.append(ptrs[0])
             self.sketch_ptrs.append(ptrs[1])
+            if nnz is not None:
+                self.tokens_ptrs.append(ptrs[2])
+                self.offsets_ptrs.append(ptrs[3])
         dev = torch.device("cuda", ctx.device)
         self.values = torch.as_tensor(_DeviceArray(self._own[0], (n, t), "<i4", self), device=dev)
         self.sketch = torch.as_tensor(_DeviceArray(self._own[1], (n, ell), "<i8", self), device=dev)
+        if nnz is not None:
+            self.tokens = torch.as_tensor(_DeviceArray(self._own[2], (nnz,), "<i4", self), device=dev)
+            self.offsets = torch.as_tensor(_DeviceArray(self._own[3], (n + 1,), "<i8", self), device=dev)
 
     def close(self):
         for p in self._opened:
@@ -235,6 +246,95 @@ def embed_sharded_p2p(eparams, d_tok, d_off, d: int, sketch, rank: int, world: i
     return (peers.values if eparams is not None else None), (peers.sketch if sketch is not None else None)
 
 
+def _stream_barrier(device, group=None):
+    """All ranks reach this point in stream order (a 1-element NCCL
+    all-reduce: no host synchronisation); gloo falls back to a host barrier
+    after draining the device (functional runs)."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        flag = torch.zeros(1, dtype=torch.int32, device=device)
+        dist.all_reduce(flag, group=group)
+    else:
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+
+
+def csr_from_host_sharded(tok_host, off_host, rank: int, world: int, peers: PeerArrays, group=None,
+                          side_stream=None):
+    """End-to-end input staging for the set-sharded path: rank r copies only
+    ITS slice of the CSR (sets shard_range(n, r, W): tokens
+    off[lo]..off[hi] and offsets lo..hi) from pinned host memory into its own
+    full-size CSR buffer, then pushes that slice to every peer's buffer
+    (cpsj_copy_async over NVLink) on `side_stream`, so the push overlaps the
+    K1 launches that only need the local slice.  The caller joins the side
+    stream and runs a barrier (embed_sharded_p2p's closing all-reduce) before
+    any rank reads the full CSR.  Host->device bytes per rank = the slice
+    (about 1/W of the CSR) instead of the whole CSR.
+    Returns (tokens, offsets) = this rank's full-size device buffers and the
+    host->device byte count."""
+    import torch
+    ctx = peers.ctx
+    n = peers.n
+    lo, hi, _ = shard_range(n, rank, world)
+    main = torch.cuda.current_stream()
+    t0, t1 = int(off_host[lo]), int(off_host[hi])
+    h2d = 0
+    # own slice first (the K1 launches read it), on the main stream
+    if t1 > t0:
+        ctx.check(ctx.lib.cpsj_copy_async(ctx.handle, peers.tokens_ptrs[rank] + 4 * t0,
+                                          tok_host.data_ptr() + 4 * t0, 4 * (t1 - t0), main.cuda_stream))
+        h2d += 4 * (t1 - t0)
+    if hi >= lo:
+        ctx.check(ctx.lib.cpsj_copy_async(ctx.handle, peers.offsets_ptrs[rank] + 8 * lo,
+                                          off_host.data_ptr() + 8 * lo, 8 * (hi - lo + 1), main.cuda_stream))
+        h2d += 8 * (hi - lo + 1)
+    if world > 1:
+        ss = side_stream if side_stream is not None else main
+        if ss is not main:
+            ss.wait_stream(main)
+        for r in range(world):
+            if r == rank:
+                continue
+            if t1 > t0:
+                ctx.check(ctx.lib.cpsj_copy_async(ctx.handle, peers.tokens_ptrs[r] + 4 * t0,
+                                                  peers.tokens_ptrs[rank] + 4 * t0, 4 * (t1 - t0), ss.cuda_stream))
+            ctx.check(ctx.lib.cpsj_copy_async(ctx.handle, peers.offsets_ptrs[r] + 8 * lo,
+                                              peers.offsets_ptrs[rank] + 8 * lo, 8 * (hi - lo + 1), ss.cuda_stream))
+    return peers.tokens, peers.offsets, h2d
+
+
+def embed_sharded_p2p_from_host(eparams, tok_host, off_host, d: int, sketch, rank: int, world: int,
+                                peers: PeerArrays, group=None, side_stream=None):
+    """The whole set-sharded embedding from pinned host buffers: one barrier
+    (write-after-read guard), this rank's CSR slice host->device and pushed
+    to the peers (csr_from_host_sharded, overlapping K1), K1 values and
+    sketches of the slice stored to every rank (cpsj_minhash_sketch_multi),
+    and one closing barrier.  Returns (tokens, offsets, values, sketches,
+    h2d_bytes); every rank then holds the full CSR and full arrays."""
+    import torch
+
+    from ._native import Context
+    from .hashing import sketch_family
+    ctx = Context.get()
+    dev = torch.device("cuda", ctx.device)
+    n = peers.n
+    lo, hi, _ = shard_range(n, rank, world)
+    if world > 1:
+        _stream_barrier(dev, group)
+    d_tok, d_off, h2d = csr_from_host_sharded(tok_host, off_host, rank, world, peers, group, side_stream)
+    if eparams is not None:
+        _k1_to_peers(ctx, eparams.device(ctx), d_tok, d_off, d, lo, hi, peers.values_ptrs, False)
+    if sketch is not None:
+        _k1_to_peers(ctx, sketch_family(*sketch).device(ctx), d_tok, d_off, d, lo, hi, peers.sketch_ptrs, True)
+    if side_stream is not None:
+        torch.cuda.current_stream().wait_stream(side_stream)
+    if world > 1:
+        _stream_barrier(dev, group)      # every rank's slices and K1 rows precede the readers
+    return d_tok, d_off, (peers.values if eparams is not None else None), \
+        (peers.sketch if sketch is not None else None), h2d
+
+
 def embedded_from_parts(eparams, d_tok, d_off, d: int, values, sketches, sketch_key=None, host_csr=None):
     """EmbeddedDataset over device tensors produced by embed_sharded."""
     import torch
@@ -277,8 +377,9 @@ def shard_frontier(emb, params: CPSJoinParams, rank: int, world: int, depth: int
                    local_join=None) -> JoinArrays:
     """cpsjoin_self over `world` ranks, sharding the tree frontier: every
     rank builds every repetition's levels above `depth` (the root split is
-    cheap and identical everywhere), then keeps the nodes of level `depth`
-    with index % world == rank and everything below them (SURVEY.md 8(e):
+    cheap and identical everywhere), then keeps its size-balanced contiguous
+    share of the nodes of level `depth` (cost-weighted cut, see cpsj_plan in
+    include/cpsjoin_b200.h) and everything below them (SURVEY.md 8(e):
     scales past R GPUs, where repetition sharding stops).  Ranks != 0 count
     only what they found below the cut, so the counter sums and the pair
     union equal the unsharded join."""

@@ -187,3 +187,99 @@ def test_write_pairs_format(tmp_path):
     p = tmp_path / "out.txt"
     write_pairs(str(p), [0, 3], [5, 9], [0.5, 2.0 / 3.0])
     assert p.read_text() == "0 5 0.500000\n3 9 0.666667\n"
+
+
+# ------------------------------------------------------------ ABI guard
+
+ABI_STRUCTS = {"cpsj_inputs": "Inputs", "cpsj_plan": "Plan", "cpsj_lsh_plan": "LshPlan", "cpsj_k1_dsts": "K1Dsts",
+               "cpsj_join_stats": "JoinStats", "cpsj_ingest_stats": "IngestStats"}
+
+
+def test_ctypes_structs_match_header_sizeof(tmp_path):
+    """The ctypes declarations have the header's sizeof and field offsets
+    (gcc on include/cpsjoin_b200.h), and every parameter struct starts with
+    its struct_size guard."""
+    import ctypes
+
+    from paper_1707_06814_b200 import _native
+    lines = ["#include <stddef.h>", "#include <stdio.h>", '#include "cpsjoin_b200.h"', "int main(void) {"]
+    for c_name, py_name in ABI_STRUCTS.items():
+        lines.append(f'printf("{py_name} size %zu\\n", sizeof({c_name}));')
+        for f, _ in getattr(_native, py_name)._fields_:
+            lines.append(f'printf("{py_name} {f} %zu\\n", offsetof({c_name}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        py_name, what, v = ln.split()
+        got[(py_name, what)] = int(v)
+    for py_name in ABI_STRUCTS.values():
+        cls = getattr(_native, py_name)
+        assert got[(py_name, "size")] == ctypes.sizeof(cls), py_name
+        for f, _ in cls._fields_:
+            assert got[(py_name, f)] == getattr(cls, f).offset, (py_name, f)
+    for py_name in ("Inputs", "Plan", "LshPlan", "K1Dsts"):
+        cls = getattr(_native, py_name)
+        assert cls._fields_[0][0] == "struct_size"
+        assert cls().struct_size == ctypes.sizeof(cls)
+    lib = _native.load()
+    assert lib.cpsj_version() == _native.ABI_VERSION
+
+
+def _integration_stub() -> str:
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = doc.split("<!-- integration-stub:begin -->")[1].split("<!-- integration-stub:end -->")[0]
+    return block.split("```python")[1].split("```")[0]
+
+
+def test_integration_stub_declares_the_header_structs():
+    """The INTEGRATION.md stub's ctypes structs have the header's field
+    lists (names and order), so it cannot fall behind cpsjoin_b200.h."""
+    import ctypes
+
+    from paper_1707_06814_b200 import _native
+    ns = {}
+    code = _integration_stub()
+    # declarations only: everything before the library is opened
+    decl = code.split("lib = ctypes.CDLL")[0]
+    rest = code.split("\n", 1)[1]
+    structs = rest[rest.index("class Inputs"):rest.index("lib.cpsj_ctx_create")]
+    exec(decl + "P, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double\n" + structs,
+         ns)
+    for stub_name, ours in (("Inputs", _native.Inputs), ("Plan", _native.Plan), ("Stats", _native.JoinStats)):
+        cls = ns[stub_name]
+        assert [f for f, _ in cls._fields_] == [f for f, _ in ours._fields_]
+        assert ctypes.sizeof(cls) == ctypes.sizeof(ours)
+
+
+def test_reference_shaped_embedded_dataset_matches_reference():
+    """tests/refshape.py (the stand-in the GPU integration test hands to the
+    INTEGRATION.md stub) carries exactly what the reference's own
+    embed_dataset returns in every attribute the stub reads."""
+    ref_src = "/root/reference/pkg/src"
+    if not os.path.isdir(ref_src):
+        pytest.skip("reference not present (GPU box)")
+    import sys
+    sys.path.insert(0, ref_src)
+    try:
+        from simjoin.core import Dataset
+        from simjoin.embed import EmbeddingParams, embed_dataset
+    finally:
+        sys.path.remove(ref_src)
+    from refshape import from_fixture
+    z = np.load(os.path.join(ROOT, "tests", "golden", "planted_small.npz"))
+    tok, off = z["tokens"], z["offsets"]
+    lists = [tok[off[i]:off[i + 1]].astype(np.int64) for i in range(len(off) - 1)]
+    ds = Dataset.from_token_lists(lists, d=int(z["d"]))
+    ref = embed_dataset(EmbeddingParams(t=int(z["t"]), seed=int(z["emb_seed"])), ds)
+    ours = from_fixture(z)
+    assert len(ours) == len(ref) and ours.t == ref.t
+    assert np.array_equal(ours.verify_csr.indices, ref.verify_csr.indices)
+    assert ours.verify_csr.indices.dtype == ref.verify_csr.indices.dtype
+    assert np.array_equal(ours.verify_csr.indptr, ref.verify_csr.indptr)
+    assert np.array_equal(ours.sizes, ref.sizes) and ours.sizes.dtype == ref.sizes.dtype
+    assert np.array_equal(ours.values, ref.values) and ours.values.dtype == ref.values.dtype
+    assert np.array_equal(ours.sketches(8, 5), ref.sketches(8, 5))

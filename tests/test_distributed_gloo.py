@@ -192,3 +192,65 @@ def test_merge_results_is_order_independent():
     k2, s2 = merge_results(keys[perm], sims[perm])
     assert np.array_equal(k1, k2) and np.array_equal(s1, s2)
     assert np.all(np.diff(k1.astype(np.int64)) > 0)
+
+
+def _frontier_main(rank, world, depth, port, q):
+    """One rank of shard_frontier (the bench's N > 1 default) with the C
+    oracle's frontier mode as the injected local join."""
+    import torch.distributed as dist
+
+    from paper_1707_06814_b200.core import Counters
+    from paper_1707_06814_b200.cpsjoin import CPSJoinParams, JoinArrays
+    from paper_1707_06814_b200.distributed import shard_frontier
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = _workload()
+        values = O.minhash(w.tokens, w.offsets, O.embedding_tables(128, 7), 1)
+        mh, bt = O.sketch_tables(8, 7)
+        sk = O.sketch(w.tokens, w.offsets, mh, bt, 1)
+        params = CPSJoinParams(lambda_=0.5, seed=7, repetitions=3, limit=40)
+
+        def local(emb, p, frontier):
+            out = O.self_join(w.tokens, w.offsets, w.sizes, values, sk, p.lambda_, epsilon=p.epsilon, limit=p.limit,
+                              delta=p.delta, repetitions=p.repetitions, seed=p.seed, depth_cap=p.depth_cap,
+                              threads=1, frontier=frontier)
+            return JoinArrays(out.a, out.b, out.sims, Counters(out.pre_candidates, out.candidates, out.results,
+                                                               out.max_depth, out.peak_live_members),
+                              out.cap_events, {})
+
+        res = shard_frontier(None, params, rank, world, depth=depth, local_join=local)
+        c = res.counters
+        q.put((rank, res.a.tolist(), res.b.tolist(), res.similarity.tolist(),
+               [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members],
+               len(res.depth_cap_sizes)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,depth", [(2, 1), (3, 2)])
+def test_frontier_sharding_over_ranks_equals_single_process(world, depth):
+    """shard_frontier across `world` gloo processes (frontier cut, variable
+    all-gather of pairs, sort + unique, counter sum/max) equals the
+    unsharded join on every rank."""
+    w = _workload()
+    values = O.minhash(w.tokens, w.offsets, O.embedding_tables(128, 7), 1)
+    mh, bt = O.sketch_tables(8, 7)
+    sk = O.sketch(w.tokens, w.offsets, mh, bt, 1)
+    ref = O.self_join(w.tokens, w.offsets, w.sizes, values, sk, 0.5, repetitions=3, seed=7, limit=40, threads=1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_frontier_main, args=(r, world, depth, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, a, b, s, c, ncap in outs:
+        assert a == ref.a.tolist() and b == ref.b.tolist()
+        assert s == ref.sims.tolist()
+        assert c == [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members]
+        assert ncap == len(ref.cap_events)

@@ -231,6 +231,35 @@ def test_frontier_sharding_equals_unsharded(name, ranks, depth, no_k7, monkeypat
     assert sum(len(x.depth_cap_sizes) for x in parts) == len(ref.depth_cap_sizes)
 
 
+@pytest.mark.parametrize("no_k7", [False, True])
+@pytest.mark.parametrize("ranks,depth", [(2, 1), (3, 2), (5, 1)])
+@pytest.mark.parametrize("name", ["c1_sample", "c4_sample", "dense_cluster"])
+def test_frontier_rank_share_matches_oracle_rank(name, ranks, depth, no_k7, monkeypatch):
+    """Every rank's share of a frontier-sharded join (the size-balanced cut
+    of cpsj_plan) equals the C oracle's frontier mode for that rank: same
+    pairs, f64 similarities and counters, rank by rank."""
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    if no_k7:
+        monkeypatch.setenv("CPSJ_NO_SUBTREE", "1")
+    z = load(name)
+    ds = Dataset.from_csr(z["tokens"], z["offsets"], int(z["d"]))
+    emb = embed_dataset(EmbeddingParams(t=int(z["t"]), seed=int(z["emb_seed"])), ds)
+    p = _params(z, 0)
+    sizes = np.diff(z["offsets"]).astype(np.int64)
+    for r in range(ranks):
+        got = cpsjoin_self_arrays(emb, p, frontier=(r, ranks, depth))
+        ref = O.self_join(z["tokens"], z["offsets"], sizes, emb.values, emb.sketches(p.ell, p.seed), p.lambda_,
+                          epsilon=p.epsilon, limit=p.limit, delta=p.delta, repetitions=p.repetitions, seed=p.seed,
+                          depth_cap=p.depth_cap, frontier=(r, ranks, depth))
+        assert np.array_equal(got.a, ref.a) and np.array_equal(got.b, ref.b), r
+        assert np.array_equal(got.similarity, ref.sims), r
+        c = got.counters
+        assert [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members] == \
+            [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members], r
+        assert sorted(got.depth_cap_sizes.tolist()) == sorted(ref.cap_events.tolist()), r
+
+
 def _synthetic_emb(z):
     from scipy.sparse import csr_matrix
 
