@@ -20,6 +20,7 @@ same workload; under torchrun only rank 0 runs it.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -533,9 +534,17 @@ def run_ours(args, rank: int, world: int):
             emb = k1_sharded(t_tok, t_off)
         return join_sharded(emb)
 
+    step_stats = {}
+
     def timed(fn, steps, probe=None):
         if world > 1:
             torch.distributed.barrier()
+        # the join is host-driven (a few synchronisations per level): a
+        # Python garbage-collection pause inside the timed region would idle
+        # the device, so collect first and keep the collector off until the
+        # region closes
+        gc.collect()
+        gc.disable()
         torch.cuda.synchronize()
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
@@ -554,8 +563,11 @@ def run_ours(args, rank: int, world: int):
             # the last step is queued, before the closing synchronize
             probe()
         torch.cuda.synchronize()
+        gc.enable()
         ms = start.elapsed_time(end)
         per = [a.elapsed_time(b) for a, b in zip([start] + marks[:-1], marks)]
+        step_stats[getattr(fn, '__name__', 'step')] = {"min": min(per), "median": statistics.median(per),
+                                                       "max": max(per)}
         log(f"[rank {rank}] {getattr(fn, '__name__', 'step')}: per-step ms min {min(per):.2f} "
             f"median {statistics.median(per):.2f} max {max(per):.2f} | " + " ".join(f"{x:.1f}" for x in per))
         if world > 1:
@@ -633,6 +645,32 @@ def run_ours(args, rank: int, world: int):
     pairs_per_s = pre / (k4_ms / 1e3) if k4_ms > 0 else None
     popc_rate, popc_basis = int_peak("POPC", 16.0)
     popc_peak = 148 * popc_rate * f_clk / (2 * cfg.ell)  # 2 POPC per u64 word
+
+    # ---- per-stage HBM rooflines from device-counted work:
+    # bytes per unit x units counted by the join / profiled class time
+    hbm = float(peaks["hbm_gbs"])
+    st = res.stats
+    visits, entries = int(st.get("internal_visits", 0)), int(st.get("split_entries", 0))
+    vtok, ncand, nres = int(st.get("verify_tokens", 0)), int(res.counters.candidates), int(res.counters.results)
+
+    def stage(bytes_, ms, unit_note, kernels):
+        gbs = bytes_ / (ms / 1e3) / 1e9 if ms > 0 else None
+        return {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": (gbs / hbm) if gbs else None,
+                "algorithmic_bytes": int(bytes_), "ms_per_step": ms, "work": unit_note, "kernels": kernels}
+
+    split_bytes = visits * (4 + 8 * cfg.ell + 4) + entries * (32 + 4 + 4)
+    rooflines_stage = {
+        "split": stage(split_bytes, prof["node"][0] + prof["split"][0],
+                       f"{visits} internal-node member visits x (4 B id + {8 * cfg.ell} B sketch + 4 B survivor) + "
+                       f"{entries} split entries x (32 B value-gather sector + 4 B survivor id + 4 B child member)",
+                       "K2 node sketch/flags/survivors + K3 select/keys/sort/group/children + K7 subtree"),
+        "verify": stage(4 * vtok + 16 * ncand + 16 * nres, prof["k5_verify"][0],
+                        f"{ncand} candidates: 4 B x {vtok} row tokens + 16 B pair/offsets; 16 B per kept result",
+                        "K5 k_verify"),
+        "dedup": stage(16 * nres + 16 * int(len(res.a)), prof["k6_dedup"][0],
+                       f"{nres} verified results read (u64 key + f64 sim) + {len(res.a)} unique written",
+                       "K6 sort + unique"),
+    }
 
     # ---- parity at benchmark scale: the timed device result, the e2e result
     # and the single-GPU join must agree bit for bit, and (one rank, N = 1,
@@ -713,8 +751,10 @@ def run_ours(args, rank: int, world: int):
                          "note": "naive bound (2 ell POPC per pair); the kernels count 32-bit words in triplets "
                                  "(popc(x^y^z) + 2 popc(maj)), 1.5 ell POPC per fully compared pair, and exit "
                                  "early after 5/8 of the words for most pairs, so they can exceed frac 1"},
+        "roofline_stages": rooflines_stage,
         "kernels_ms_per_step": {k: v[0] for k, v in prof.items()},
         "kernels_note": "device time per class from one extra profiled step (events around each class)",
+        "per_step_ms": step_stats,
         "join_counters": {"pre_candidates": pre, "candidates": res.counters.candidates,
                           "results": res.counters.results, "max_depth": res.counters.max_depth,
                           "pairs": int(len(res.a))},

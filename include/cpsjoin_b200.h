@@ -206,6 +206,12 @@ typedef struct {
     int64_t n_levels;         /* frontier levels processed                    */
     int64_t gpu_launches;     /* own kernels launched by this call            */
     int64_t lib_calls;        /* CUB device-wide scans/sorts issued           */
+    /* work actually done, counted on the device (the per-stage rooflines):  */
+    int64_t internal_visits;  /* members of every internal node processed
+                                 (node sketch + flag rule, K2)               */
+    int64_t split_entries;    /* (survivor, selected position) entries split
+                                 (value gather + group-by, K3)               */
+    int64_t verify_tokens;    /* sum of |x| + |y| over verified candidates (K5) */
 } cpsj_join_stats;
 
 /*

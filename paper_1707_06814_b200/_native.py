@@ -51,7 +51,8 @@ class IngestStats(ctypes.Structure):
 class JoinStats(ctypes.Structure):
     _fields_ = [("n_pairs", i64), ("pre_candidates", i64), ("candidates", i64), ("results", i64),
                 ("max_depth", i64), ("peak_live_members", i64), ("n_depth_cap_events", i64),
-                ("n_levels", i64), ("gpu_launches", i64), ("lib_calls", i64)]
+                ("n_levels", i64), ("gpu_launches", i64), ("lib_calls", i64), ("internal_visits", i64),
+                ("split_entries", i64), ("verify_tokens", i64)]
 
 
 EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_error",

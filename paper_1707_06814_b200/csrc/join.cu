@@ -62,6 +62,9 @@ struct DevCounters {
     unsigned long long def_mtop;
     int verr;                    // a MinHash value >= 2^value_bits reached a
                                  // split key (the plan's value_bits is wrong)
+    unsigned long long visits;   // K7: internal-node member visits
+    unsigned long long entries;  // K7: split entries (survivor x selected position)
+    unsigned long long vtok;     // K5: tokens of the verified candidates' rows
 };
 
 // a split/count key packs (segment << vbits) | value: a value that does not
@@ -862,6 +865,7 @@ __global__ void k_verify(int64_t nc, const int2 *__restrict__ cand, const uint32
     }
     inter = __reduce_add_sync(0xffffffffu, inter);
     if (lane == 0) {
+        atomicAdd(&ctr->vtok, (unsigned long long)((ae - ab) + (be - bb)));
         const long long uni = (long long)sizes[c.x] + sizes[c.y] - inter;
         const double sim = (double)inter / (double)uni;
         if (sim >= lam) {
@@ -1235,6 +1239,10 @@ __global__ void __launch_bounds__(ST_THREADS, 1) k_subtree(const SubtreeArgs a) 
         }
         const int s = m - nflag;
         bool split = s >= 2;
+        if (tid == 0) {
+            atomicAdd(&ctr->visits, (unsigned long long)m);
+            if (split && depth < a.depth_cap) atomicAdd(&ctr->entries, (unsigned long long)s * (unsigned long long)nsel);
+        }
         if (split && depth >= a.depth_cap) {
             split = false;
             if (tid == 0) {
@@ -2026,6 +2034,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     // candidate and result buffers grow on demand
     Emitter em(ctx, st, in, lam, ctr.p);
     int64_t max_depth = 0, levels = 0;
+    int64_t lvl_visits = 0, lvl_entries = 0;  // level-path work (K7 counts its own on the device)
 
     // level arrays: lv (current) and nx (next) swap each level; they and
     // every per-level scratch array below keep their allocation across
@@ -2198,6 +2207,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         work.tiles = sc[0];
         work.tile_off = tile_off.p;
         const int64_t n_int = sc[1], Mi = sc[2];
+        lvl_visits += Mi;
         prof_plan.reset();
         // K7 deferral: this level's internal nodes of <= 8192 members (not in
         // n_int) join the deferred root list that one k_subtree launch takes
@@ -2301,6 +2311,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         const int64_t n_leaf_cand = sc[0];
         const int64_t n_flag = by_levels ? sc[1] : 0, E = by_levels ? sc[2] : 0, n_seg = by_levels ? sc[3] : 0;
         const int64_t ncap = by_levels ? sc[4] : 0;
+        lvl_entries += E;
         if (ncap) {
             std::vector<int64_t> h(ncap);
             CPSJ_CUDA(cudaMemcpyAsync(h.data(), capsz.p, ncap * 8, cudaMemcpyDeviceToHost, st));
@@ -2453,6 +2464,9 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     }
     stats->n_depth_cap_events = (int64_t)ctx->cap_events.size();
     stats->n_levels = levels;
+    stats->internal_visits = lvl_visits + (int64_t)hc.visits;
+    stats->split_entries = lvl_entries + (int64_t)hc.entries;
+    stats->verify_tokens = (int64_t)hc.vtok;
     stats->gpu_launches = ctx->launches - launches0;
     stats->lib_calls = ctx->lib_calls - lib0;
 }
