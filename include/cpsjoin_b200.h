@@ -304,6 +304,18 @@ CPSJ_API int cpsj_ingest_copy(cpsj_ctx *ctx, uint32_t *h_tokens, int64_t *h_offs
                      void *stream);
 
 /*
+ * First-seen dense remap of an embedding:
+ * EmbeddedDataset.dense and .d of the reference (_first_seen_dense,
+ * embed.py:108-114, applied at embed.py:129-132).  d_values: (n, t) u32
+ * row-major MinHash values; d_dense_out: (n, t) u32, the dense id of
+ * (position i, values[r, i]) numbered in order of first appearance in
+ * row-major order; *h_d_out = the number of distinct (i, value) keys.
+ * n * t must be below 2^32.  Synchronises the stream before returning.
+ */
+CPSJ_API int cpsj_dense_remap(cpsj_ctx *ctx, const uint32_t *d_values, int64_t n, int32_t t,
+                              uint32_t *d_dense_out, int64_t *h_d_out, void *stream);
+
+/*
  * Exact joins (SPEC.md module `allpairs`; specified by the
  * reference but not shipped -- here the at-scale recall oracle).
  *

@@ -288,8 +288,40 @@ def ingest_main():
     ingest_fixture("ingest_all_short", [[1], [], [2, 2, 2], [7]], None)
 
 
+def dense_fixture(name: str, ds, t: int, seed: int, full: bool):
+    """EmbeddedDataset.dense / .d made by the reference (_first_seen_dense,
+    embed.py:108-114,129-132) -- pins the GPU remap (csrc/dense.cu)."""
+    emb = embed_dataset(EmbeddingParams(t=t, seed=seed), ds)
+    flat, off = ds.flat_tokens()
+    kw = dict(tokens=flat.astype(np.uint32), offsets=off.astype(np.int64), d_universe=np.int64(ds.d),
+              t=np.int64(t), emb_seed=np.int64(seed), values_sha=np.array(sha(emb.values)),
+              dense_sha=np.array(sha(emb.dense)), dense_head=emb.dense[:16].copy(), d=np.int64(emb.d))
+    if full:
+        kw["values"] = emb.values
+        kw["dense"] = emb.dense
+    save(name, **kw)
+
+
+def dense_main():
+    # tests/test_embed.py:84-88,112-124 shape (make_dataset(n=10), t=8, seed 4)
+    rng = np.random.default_rng(3)
+    lists = [rng.choice(200, size=rng.integers(2, 25), replace=False) for _ in range(10)]
+    dense_fixture("dense_small", Dataset.from_token_lists(lists), 8, 4, True)
+    # heavy value sharing (a near-duplicate cluster): first-seen order matters
+    rng = np.random.default_rng(5)
+    dense = [list(range(180)) + list(range(1000 + 10 * i, 1010 + 10 * i)) for i in range(300)]
+    dense += [rng.choice(np.arange(5000, 20000), size=30, replace=False) for _ in range(300)]
+    dense_fixture("dense_cluster_remap", Dataset.from_token_lists(dense), 128, 8, False)
+    w1 = generate(1, scale=0.05)
+    ds1 = Dataset.from_token_lists([w1.tokens[w1.offsets[i]:w1.offsets[i + 1]] for i in range(w1.n)], d=w1.d)
+    dense_fixture("dense_c1_sample", ds1, 128, 7, False)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--dense-only" in sys.argv:
+        dense_main()
+        return
     if "--ingest-only" in sys.argv:
         ingest_main()
         return
@@ -301,6 +333,7 @@ def main():
         return
     rs_main()
     ct_main()
+    dense_main()
     kat_minhash()
     # reference-fixture shapes (planted J = 0.7 pairs)
     emb_fixture("planted_small", Dataset.from_token_lists(planted_lists(60, 12, 31)), 128, 3,

@@ -309,3 +309,17 @@ def lsh_join(tokens, offsets, sizes, values, sketches, lam: float, accept: int, 
     keys = np.array(sorted(found), dtype=np.uint64)
     sims = np.array([found[int(k)] for k in keys], dtype=np.float64)
     return keys, sims, pre, cand, res
+
+
+def first_seen_dense(values: np.ndarray) -> tuple[np.ndarray, int]:
+    """EmbeddedDataset.dense / .d (embed.py:108-114, 129-132) restated in
+    numpy: keys (i << 32) | values[r, i] numbered by first appearance in
+    row-major order.  Test infrastructure (the GPU remap's checker)."""
+    n, t = values.shape
+    if n == 0:
+        return np.zeros((0, t), dtype=np.uint32), 0
+    keys = (np.arange(t, dtype=np.uint64)[None, :] << np.uint64(32)) | values.astype(np.uint64)
+    uniq, first, inverse = np.unique(keys.ravel(), return_index=True, return_inverse=True)
+    rank = np.empty(len(uniq), dtype=np.int64)
+    rank[np.argsort(first, kind="stable")] = np.arange(len(uniq))
+    return rank[inverse].reshape(n, t).astype(np.uint32), len(uniq)

@@ -61,7 +61,7 @@ EXPORTS = ["cpsj_version", "cpsj_ctx_create", "cpsj_ctx_destroy", "cpsj_last_err
            "cpsj_launch_counts", "cpsj_frequency_order", "cpsj_exact_join",
            "cpsj_lsh_join", "cpsj_ingest_lists", "cpsj_parse_text", "cpsj_ingest_result_device", "cpsj_ingest_copy",
            "cpsj_minhash_sketch_multi", "cpsj_xbuf_create", "cpsj_xbuf_open", "cpsj_xbuf_close",
-           "cpsj_minhash_embed", "cpsj_copy_async"]
+           "cpsj_minhash_embed", "cpsj_copy_async", "cpsj_dense_remap"]
 
 MAX_DSTS = 8
 IPC_HANDLE_BYTES = 64
@@ -87,7 +87,8 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        so = path or SO
+        # CPSJ_LIB: an alternative build of the same sources (A/B diagnostics)
+        so = path or os.environ.get("CPSJ_LIB") or SO
         if not os.path.exists(so):
             raise ImportError(f"CUDA library not built: {so} (run python -m paper_1707_06814_b200.build)")
         L = ctypes.CDLL(so)
@@ -121,6 +122,7 @@ def load(path: str | None = None):
         L.cpsj_xbuf_open.argtypes = [P, P, ctypes.POINTER(P)]
         L.cpsj_xbuf_close.argtypes = [P, P, i32]
         L.cpsj_copy_async.argtypes = [P, P, P, i64, P]
+        L.cpsj_dense_remap.argtypes = [P, P, i64, i32, P, ctypes.POINTER(i64), P]
         L.cpsj_exact_join.argtypes = [P, P, P, i64, i64, dbl, i32, ctypes.POINTER(JoinStats), P]
         _lib = L
         return L

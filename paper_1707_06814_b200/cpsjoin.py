@@ -167,10 +167,10 @@ def _value_bits(emb: EmbeddedDataset) -> int:
     if emb._width and "values" in emb._dev and not getattr(emb, "_values_host_set", False):
         vmax = int(emb._width) - 1          # values computed by K1 from this CSR
     elif emb._values is not None:
-        key = id(emb._values)
-        if getattr(emb, "_vmax_key", None) != key:
-            emb._vmax_key, emb._vmax = key, (int(emb._values.max()) if emb._values.size else 0)
-        vmax = emb._vmax
+        # host-provided values: recomputed every call (an in-place change of
+        # the array must not leave a stale bound; the split kernels also
+        # reject any value >= 2^value_bits on the device)
+        vmax = int(emb._values.max()) if emb._values.size else 0
     else:
         return 0
     return max(1, vmax.bit_length())

@@ -354,6 +354,16 @@ int cpsj_exact_join(cpsj_ctx *ctx, const uint32_t *d_tokens, const int64_t *d_of
     });
 }
 
+int cpsj_dense_remap(cpsj_ctx *ctx, const uint32_t *d_values, int64_t n, int32_t t, uint32_t *d_dense_out,
+                     int64_t *h_d_out, void *stream) {
+    if (!ctx) return CPSJ_E_ARG;
+    return guarded(ctx, [&] {
+        cpsj::require(h_d_out != nullptr, "null d output");
+        CPSJ_CUDA(cudaSetDevice(ctx->device));
+        cpsj::dense_remap(ctx, d_values, n, t, d_dense_out, h_d_out, (cudaStream_t)stream);
+    });
+}
+
 int cpsj_launch_counts(const cpsj_ctx *ctx, int64_t *own_kernels, int64_t *lib_calls) {
     if (!ctx) return CPSJ_E_ARG;
     if (own_kernels) *own_kernels = ctx->launches;

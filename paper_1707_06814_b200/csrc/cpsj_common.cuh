@@ -252,6 +252,8 @@ void parse_text(cpsj_ctx *ctx, const uint8_t *d_bytes, int64_t B, int64_t d, cps
                 cudaStream_t st);
 void frequency_order(cpsj_ctx *ctx, const uint32_t *d_tokens, int64_t nnz, int64_t d, uint32_t *d_rank,
                      uint32_t *d_order, cudaStream_t st);
+void dense_remap(cpsj_ctx *ctx, const uint32_t *d_values, int64_t n, int32_t t, uint32_t *d_dense, int64_t *h_d,
+                 cudaStream_t st);
 void exact_join(cpsj_ctx *ctx, const uint32_t *tok, const int64_t *off, int64_t n, int64_t d, double lam, int naive,
                 cpsj_join_stats *stats, cudaStream_t st);
 }  // namespace cpsj

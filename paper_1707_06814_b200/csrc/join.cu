@@ -36,6 +36,7 @@
 #include <memory>
 
 #include "cpsj_common.cuh"
+#include "radix.cuh"
 
 namespace cpsj {
 
@@ -1714,6 +1715,71 @@ void leaf_dispatch(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Lev
 
 // Candidate and result buffers of one join call (grow on demand), K5 on
 // each batch of candidates and K6 at the end.
+// ---- K6 (cpsjoin.py:308-319): sort + unique of the verified pairs with
+// the hand-written radix sort (radix.cuh) over the significant key bits:
+// key (min << 32 | max) is packed to (min << nb | max), nb = bit length of
+// n - 1, so the sort runs 2 nb bits (40 at n = 1M) instead of 64.
+__global__ void k_k6_pack(const uint64_t *__restrict__ keys, const double *__restrict__ sims, int64_t m, int nb,
+                          uint64_t *__restrict__ kp, uint64_t *__restrict__ vp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint64_t k = keys[i];
+    kp[i] = ((k >> 32) << nb) | (k & 0xFFFFFFFFull);
+    vp[i] = __double_as_longlong(sims[i]);
+}
+
+// per tile (RS_TILE sorted items, 8 consecutive per thread): the number of
+// first-of-a-run items; with `out` set, their compaction (unpacked keys)
+// at the tile's exclusive offset `cnt[tile]` (k_rs_colscan)
+constexpr int K6_PER = RS_TILE / RS_THREADS;
+__global__ void __launch_bounds__(RS_THREADS) k_k6_unique(const uint64_t *__restrict__ k, const uint64_t *__restrict__ v,
+                                                          int64_t m, int nb, uint32_t *__restrict__ cnt,
+                                                          uint64_t *__restrict__ okeys, double *__restrict__ osims) {
+    __shared__ uint32_t wsum[RS_WARPS];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * RS_TILE + (int64_t)threadIdx.x * K6_PER;
+    uint32_t heads = 0;
+    uint64_t prev = (i0 > 0 && i0 <= m) ? k[i0 - 1] : ~0ull;
+#pragma unroll
+    for (int j = 0; j < K6_PER; ++j) {
+        const int64_t i = i0 + j;
+        if (i < m) {
+            const uint64_t x = k[i];
+            heads |= (uint32_t)(i == 0 || x != prev) << j;
+            prev = x;
+        }
+    }
+    const uint32_t c = (uint32_t)__popc(heads);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (okeys == nullptr) {
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int q = 0; q < RS_WARPS; ++q) t += wsum[q];
+            cnt[blockIdx.x] = t;
+        }
+        return;
+    }
+    uint32_t pos = cnt[blockIdx.x] + incl - c;
+    for (int q = 0; q < w; ++q) pos += wsum[q];
+    const uint64_t mask = (1ull << nb) - 1ull;
+#pragma unroll
+    for (int j = 0; j < K6_PER; ++j) {
+        if ((heads >> j) & 1u) {
+            const uint64_t x = k[i0 + j];
+            okeys[pos] = ((x >> nb) << 32) | (x & mask);
+            osims[pos] = __longlong_as_double((long long)v[i0 + j]);
+            ++pos;
+        }
+    }
+}
+
 struct Emitter {
     cpsj_ctx *ctx;
     cudaStream_t st;
@@ -1776,28 +1842,29 @@ struct Emitter {
         ctx->res_sims.release();
         ctx->n_pairs = 0;
         if (nres > 0) {
-            DevBuf<uint64_t> k2(nres, st);
-            DevBuf<double> s2(nres, st);
-            size_t bytes = 0;
-            CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64, st));
-            if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
-            CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, rkeys.p, k2.p, rsims.p, s2.p, nres, 0, 64,
-                                                      st));
-            ctx->lib_calls++;
+            int nb = 1;
+            while (nb < 32 && ((uint64_t)(in->n - 1) >> nb) != 0) ++nb;
+            DevBuf<uint64_t> ka(nres, st), va(nres, st), kb(nres, st), vb(nres, st);
+            const int64_t T = (nres + RS_TILE - 1) / RS_TILE;
+            DevBuf<uint32_t> scratch((size_t)rs_scratch_words(nres), st);
+            k_k6_pack<<<blocks_for(nres), TPB, 0, st>>>(rkeys.p, rsims.p, nres, nb, ka.p, va.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            const bool flip = radix_sort_pairs<uint64_t>(ctx, ka.p, va.p, kb.p, vb.p, nres, 2 * nb, scratch.p, st);
+            const uint64_t *sk = flip ? kb.p : ka.p, *sv = flip ? vb.p : va.p;
             ctx->res_keys.alloc(nres, st);
             ctx->res_sims.alloc(nres, st);
-            DevBuf<int64_t> nsel(1, st);
-            bytes = 0;
-            CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(nullptr, bytes, k2.p, s2.p, ctx->res_keys.p, ctx->res_sims.p,
-                                                     nsel.p, nres, st));
-            if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
-            CPSJ_CUDA(cub::DeviceSelect::UniqueByKey(drv.cub_tmp.p, bytes, k2.p, s2.p, ctx->res_keys.p,
-                                                     ctx->res_sims.p, nsel.p, nres, st));
-            ctx->lib_calls++;
-            int64_t u = 0;
-            CPSJ_CUDA(cudaMemcpyAsync(&u, nsel.p, 8, cudaMemcpyDeviceToHost, st));
+            uint32_t *cnt = scratch.p, *total = scratch.p + T;
+            k_k6_unique<<<(unsigned)T, RS_THREADS, 0, st>>>(sk, sv, nres, nb, cnt, nullptr, nullptr);
+            k_rs_colscan<<<1, 1024, 0, st>>>(cnt, T, total);
+            k_k6_unique<<<(unsigned)T, RS_THREADS, 0, st>>>(sk, sv, nres, nb, cnt, ctx->res_keys.p,
+                                                            ctx->res_sims.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 3;
+            uint32_t u = 0;
+            CPSJ_CUDA(cudaMemcpyAsync(&u, total, 4, cudaMemcpyDeviceToHost, st));
             CPSJ_CUDA(cudaStreamSynchronize(st));
-            ctx->n_pairs = u;
+            ctx->n_pairs = (int64_t)u;
         }
         return hc;
     }

@@ -36,12 +36,23 @@ class EmbeddingParams:
         return fam
 
 
-def _first_seen_dense(keys: np.ndarray) -> tuple[np.ndarray, int]:
-    """Remap keys to 0..k-1 in order of first appearance (host)."""
-    uniq, first, inverse = np.unique(keys, return_index=True, return_inverse=True)
-    order = np.empty(len(uniq), dtype=np.int64)
-    order[np.argsort(first, kind="stable")] = np.arange(len(uniq))
-    return order[inverse], len(uniq)
+def dense_remap_device(d_values, t: int):
+    """The reference's first-seen dense remap of an embedding
+    (_first_seen_dense over keys (i << 32) | values[r, i], embed.py:108-114,
+    129-132) on the GPU (cpsj_dense_remap, csrc/dense.cu).  d_values: (n, t)
+    int32 device tensor (u32 bits).  Returns ((n, t) int32 device tensor of
+    dense ids, d)."""
+    import ctypes
+    torch = _torch()
+    from ._native import Context, i64
+    ctx = Context.get()
+    n = int(d_values.shape[0])
+    out = torch.empty((n, t), dtype=torch.int32, device=d_values.device)
+    d = i64()
+    stream = torch.cuda.current_stream(d_values.device).cuda_stream
+    ctx.check(ctx.lib.cpsj_dense_remap(ctx.handle, d_values.data_ptr(), n, int(t), out.data_ptr(), ctypes.byref(d),
+                                       stream))
+    return out, int(d.value)
 
 
 def _torch():
@@ -173,14 +184,21 @@ class EmbeddedDataset:
         self._d = v
 
     def _compute_dense(self):
-        vals = self.values
-        n, t = vals.shape
+        # GPU remap (csrc/dense.cu); read lazily -- only embedded_record and
+        # the reference-facing attributes use it, the join never does
+        n, t = len(self), self.t
         if n == 0:
             self._dense, self._d = np.zeros((0, t), dtype=np.uint32), 0
             return
-        keys = (np.arange(t, dtype=np.uint64)[None, :] << np.uint64(32)) | vals.astype(np.uint64)
-        flat, d = _first_seen_dense(keys.ravel())
-        self._dense, self._d = flat.reshape(n, t).astype(np.uint32), d
+        if "values" in self._dev:
+            dv = self._dev["values"]
+        else:
+            from ._native import Context
+            ctx = Context.get()
+            dv = _torch().from_numpy(np.ascontiguousarray(self.values, dtype=np.uint32).view(np.int32)).to(
+                _torch().device("cuda", ctx.device))
+        dense, d = dense_remap_device(dv, t)
+        self._dense, self._d = dense.cpu().numpy().view(np.uint32), d
 
     @property
     def verify_csr(self):

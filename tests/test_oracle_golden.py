@@ -141,3 +141,22 @@ def test_exact_join_c1_sample_contains_found_pairs():
     found = (z["j1_pair_a"].astype(np.uint64) << np.uint64(32)) | z["j1_pair_b"].astype(np.uint64)
     assert np.isin(found, keys).all()  # 100% precision of the reference output
     assert len(found) >= 0.9 * len(keys)
+
+
+@pytest.mark.parametrize("name", ["dense_small", "dense_cluster_remap", "dense_c1_sample"])
+def test_first_seen_dense_restatement_matches_reference(name):
+    """oracle.first_seen_dense (the GPU remap's checker) reproduces the
+    reference's EmbeddedDataset.dense / .d on its own fixtures."""
+    import hashlib
+
+    from oracle import oracle as O
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    if "values" in z.files:
+        values = z["values"]
+    else:
+        values = O.minhash(z["tokens"], z["offsets"], O.embedding_tables(int(z["t"]), int(z["emb_seed"])), 1)
+    assert hashlib.sha256(np.ascontiguousarray(values).tobytes()).hexdigest() == str(z["values_sha"])
+    dense, d = O.first_seen_dense(values)
+    assert d == int(z["d"])
+    assert hashlib.sha256(np.ascontiguousarray(dense).tobytes()).hexdigest() == str(z["dense_sha"])
+    assert np.array_equal(dense[:16], z["dense_head"])

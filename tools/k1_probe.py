@@ -47,6 +47,9 @@ for i in range(reps):
     tv = run(efam, vals.data_ptr(), None)
     ts = run(sfam, None, sk.data_ptr())
     print(f"iter {i}: values {tv:.3f} ms  sketch {ts:.3f} ms", flush=True)
+import hashlib  # noqa: E402
+print("sha values", hashlib.sha256(vals.cpu().numpy().tobytes()).hexdigest()[:16],
+      "sketch", hashlib.sha256(sk.cpu().numpy().tobytes()).hexdigest()[:16])
 evals_v = len(w.tokens) * 128
 evals_s = len(w.tokens) * 64 * cfg.ell
 print(f"evals/s values {evals_v / tv * 1e3:.3e} sketch {evals_s / ts * 1e3:.3e}")
