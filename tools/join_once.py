@@ -1,6 +1,6 @@
-"""One embed + one CPSJoin call on a BASELINE workload (for ncu launch lists).
+"""One embed + CPSJoin call(s) on a BASELINE workload (for ncu launch lists).
 
-    python tools/join_once.py CFG SCALE R
+    python tools/join_once.py CFG SCALE R [CALLS]  (CPSJ_JOIN_TRACE=1 traces the last call)
 """
 import os
 import sys
@@ -23,6 +23,17 @@ d_tok = torch.from_numpy(w.tokens.view(np.int32)).to(dev)
 d_off = torch.from_numpy(w.offsets).to(dev)
 emb = embed_device_csr(EmbeddingParams(128, cfg.emb_seed), d_tok, d_off, w.d)
 emb.sketches_device(cfg.ell, cfg.join_seed)
-res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=cfg.lambdas[0], ell=cfg.ell, seed=cfg.join_seed, repetitions=R))
-torch.cuda.synchronize()
+calls = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+trace = os.environ.pop("CPSJ_JOIN_TRACE", None)
+for i in range(calls):
+    if i == calls - 1 and trace is not None:
+        os.environ["CPSJ_JOIN_TRACE"] = trace  # trace only the last (warm) call
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=cfg.lambdas[0], ell=cfg.ell, seed=cfg.join_seed,
+                                                 repetitions=R))
+    t1.record()
+    torch.cuda.synchronize()
+    print(f"call {i}: {t0.elapsed_time(t1):.3f} ms", flush=True)
 print("pairs", len(res.a), res.stats)
