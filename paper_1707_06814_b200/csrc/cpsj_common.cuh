@@ -180,6 +180,9 @@ struct cpsj_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t launches = 0;
+    // candidate-buffer capacity of the self-join (grows when a call
+    // overflows it; that call is re-run once with the larger buffer)
+    uint64_t cand_cap_hint = 1ull << 22;
 };
 
 struct cpsj_family {

@@ -92,6 +92,10 @@ inline unsigned blocks_for(int64_t n, int tpb = TPB) {
 // also listed by size class c (segment width 4 << c lanes, k_leaf_small),
 // counts in scount[c].
 constexpr int SMALL_CLASSES = 4;
+// slists class SMALL_CLASSES: leaves of 33..LB_MAX_PLAN members for the
+// CTA-per-leaf BruteForce (k_leaf_block) when the limit allows it
+constexpr int LEAF_CLASSES = SMALL_CLASSES + 1;
+constexpr int LB_MAX_PLAN = 256;
 __device__ __host__ __forceinline__ int small_class(int64_t m) {
     return m <= 4 ? 0 : m <= 8 ? 1 : m <= 16 ? 2 : 3;
 }
@@ -102,14 +106,18 @@ __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit
                        unsigned long long *__restrict__ scount = nullptr, int32_t defer_max = 0) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long pre = 0;
+    // with class lists, leaves of 33..LB_MAX_PLAN members go to the block
+    // kernel instead of the tile kernel (needs limit <= LB_MAX_PLAN)
+    const bool block_leaves = slists != nullptr && limit <= LB_MAX_PLAN;
     if (slists != nullptr) {
         // small leaves straight into their class lists (warp-aggregated
         // appends; the order inside a class does not matter)
         const int64_t m = i < N ? cnt[i] : 0;
-        const int c = (i < N && m <= limit && m >= 2 && m <= 32) ? small_class(m) : -1;
+        int c = (i < N && m <= limit && m >= 2 && m <= 32) ? small_class(m) : -1;
+        if (block_leaves && i < N && m > 32 && m <= limit) c = SMALL_CLASSES;
         const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int k = 0; k < SMALL_CLASSES; ++k) {
+        for (int k = 0; k < LEAF_CLASSES; ++k) {
             const unsigned mask = __ballot_sync(0xffffffffu, c == k);
             if (mask == 0) continue;
             unsigned long long base = 0;
@@ -123,7 +131,7 @@ __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit
         const bool leaf = m <= limit;
         const int64_t T = (m + 31) / 32;
         const int64_t pairs = m * (m - 1) / 2;
-        tiles[i] = (leaf && m > 32) ? T * (T + 1) / 2 : 0;
+        tiles[i] = (leaf && m > 32 && !block_leaves) ? T * (T + 1) / 2 : 0;
         spairs[i] = (leaf && m <= 32) ? pairs : 0;
         const bool defer = !leaf && m <= defer_max;
         internal[i] = (leaf || defer) ? 0 : 1;
@@ -225,13 +233,10 @@ __device__ __forceinline__ void emit_pair(bool pass, int32_t a, int32_t b, int2 
 // shuffle, words in order, with warp-wide early exits (the distance only
 // grows).  `kmax` is the warp-uniform round count.
 template <int ELL>
-__device__ __forceinline__ void cyclic_block(int32_t x, int32_t xsize, const uint64_t *__restrict__ sketch, int lane,
-                                             int mb, int W, bool valid, int kmax, const int8_t *__restrict__ side,
-                                             int32_t accept, double lam, int2 *cand, unsigned long long cap,
-                                             DevCounters *ctr) {
-    uint64_t w[ELL];
-#pragma unroll
-    for (int k = 0; k < ELL; ++k) w[k] = valid ? __ldg(sketch + (size_t)x * ELL + k) : 0ull;
+__device__ __forceinline__ void cyclic_block_w(const uint64_t (&w)[ELL], int32_t x, int32_t xsize, int lane, int mb,
+                                               int W, bool valid, int kmax, const int8_t *__restrict__ side,
+                                               int32_t accept, double lam, int2 *cand, unsigned long long cap,
+                                               DevCounters *ctr) {
     const int sl = lane & (W - 1), seg0 = lane - sl;
     for (int k = 1; k <= kmax; ++k) {
         int ps = sl + k;
@@ -263,6 +268,17 @@ __device__ __forceinline__ void cyclic_block(int32_t x, int32_t xsize, const uin
         if (pass) pass = size_filter(xsize, ysize, lam) && (side == nullptr || side[x] != side[y]);
         emit_pair(pass, x, y, cand, cap, ctr);
     }
+}
+
+template <int ELL>
+__device__ __forceinline__ void cyclic_block(int32_t x, int32_t xsize, const uint64_t *__restrict__ sketch, int lane,
+                                             int mb, int W, bool valid, int kmax, const int8_t *__restrict__ side,
+                                             int32_t accept, double lam, int2 *cand, unsigned long long cap,
+                                             DevCounters *ctr) {
+    uint64_t w[ELL];
+#pragma unroll
+    for (int k = 0; k < ELL; ++k) w[k] = valid ? __ldg(sketch + (size_t)x * ELL + k) : 0ull;
+    cyclic_block_w<ELL>(w, x, xsize, lane, mb, W, valid, kmax, side, accept, lam, cand, cap, ctr);
 }
 
 // BruteForce of leaves of 2..32 members (cps:139-157): leaves of size class
@@ -489,6 +505,122 @@ __global__ void k_tile_nodes(int64_t N, const int64_t *__restrict__ tile_off, in
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     for (int64_t t = tile_off[i]; t < tile_off[i + 1]; ++t) tile_node[t] = (int32_t)i;
+}
+
+// BruteForce of leaves of 33..LB_MAX members, a CTA per leaf (grid-stride
+// over the level's list of such leaves, k_plan class SMALL_CLASSES): the
+// leaf's member ids, sizes and sketches are staged in shared memory ONCE
+// (every load of the leaf independent of the others, so the member ->
+// sketch latency is paid once per leaf instead of once per 32x32 tile), then
+// the CTA's warps walk the leaf's tile triangle from shared memory:
+// diagonal tiles by the cyclic schedule, off-diagonal tiles with the column
+// member's words in registers and the row words as shared broadcasts.
+// Sketch rows are stored as 2 ELL + 1 u32 words (odd stride: a warp's
+// column loads hit 32 distinct banks).
+constexpr int LB_THREADS = 128;
+constexpr int LB_WARPS = LB_THREADS / 32;
+constexpr int LB_MAX = LB_MAX_PLAN;
+
+template <int ELL>
+__global__ void __launch_bounds__(LB_THREADS) k_leaf_block(const int64_t *__restrict__ list, int64_t cnt,
+                                                           const int64_t *__restrict__ nd_off,
+                                                           const int32_t *__restrict__ nd_cnt,
+                                                           const int32_t *__restrict__ members,
+                                                           const uint64_t *__restrict__ sketch,
+                                                           const int32_t *__restrict__ sizes,
+                                                           const int8_t *__restrict__ side, int32_t accept, double lam,
+                                                           int2 *__restrict__ cand, unsigned long long cap,
+                                                           DevCounters *ctr) {
+    constexpr int RW = 2 * ELL + 1;
+    __shared__ uint32_t skw[LB_MAX * RW];
+    __shared__ int32_t sid[LB_MAX], ssz[LB_MAX];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int64_t li = blockIdx.x; li < cnt; li += gridDim.x) {
+        const int64_t node = list[li];
+        const int m = nd_cnt[node];
+        const int32_t *mem = members + nd_off[node];
+        __syncthreads();  // the previous leaf's tiles are done with the buffers
+        for (int i = tid; i < m; i += LB_THREADS) {
+            const int32_t x = mem[i];
+            sid[i] = x;
+            ssz[i] = sizes[x];
+        }
+        __syncthreads();
+        // consecutive threads read consecutive u64 words of a member: the
+        // whole leaf's sketches arrive in ~m * ELL / 128 independent loads
+        for (int e = tid; e < m * ELL; e += LB_THREADS) {
+            const int i = e / ELL, k = e - i * ELL;
+            const uint64_t v = __ldg(sketch + (size_t)sid[i] * ELL + k);
+            skw[i * RW + 2 * k] = (uint32_t)v;
+            skw[i * RW + 2 * k + 1] = (uint32_t)(v >> 32);
+        }
+        __syncthreads();
+        const int T = (m + 31) >> 5;
+        const int ntiles = T * (T + 1) / 2;
+        for (int tl = wid; tl < ntiles; tl += LB_WARPS) {
+            int bi = 0, local = tl;
+            while (local >= T - bi) { local -= T - bi; ++bi; }
+            const int bj = bi + local;
+            if (bi == bj) {
+                const int mb = min(32, m - (bi << 5));
+                const int i = (bi << 5) + lane;
+                uint64_t w[ELL];
+#pragma unroll
+                for (int k = 0; k < ELL; ++k)
+                    w[k] = lane < mb ? ((uint64_t)skw[i * RW + 2 * k + 1] << 32) | skw[i * RW + 2 * k] : 0ull;
+                cyclic_block_w<ELL>(w, lane < mb ? sid[i] : 0, lane < mb ? ssz[i] : 0, lane, mb, 32, lane < mb,
+                                    mb >> 1, side, accept, lam, cand, cap, ctr);
+                continue;
+            }
+            // off-diagonal: block bi is full; a partial block bj (the leaf's
+            // last) becomes the row side so every lane has a column
+            const int nb = min(32, m - (bj << 5));
+            const bool swp = nb < 32;
+            const int cbk = swp ? bi : bj, rbk = swp ? bj : bi, nrows = swp ? nb : 32;
+            const int ci = (cbk << 5) + lane;
+            uint64_t cw[ELL];
+#pragma unroll
+            for (int k = 0; k < ELL; ++k) cw[k] = ((uint64_t)skw[ci * RW + 2 * k + 1] << 32) | skw[ci * RW + 2 * k];
+            const int32_t colx = sid[ci], colsz = ssz[ci];
+            for (int r = 0; r < nrows; r += 2) {
+                const bool two = r + 1 < nrows;
+                const int ia = (rbk << 5) + r, ib = two ? ia + 1 : ia;
+                uint64_t ra[ELL], rb[ELL];
+#pragma unroll
+                for (int k = 0; k < ELL; ++k) {
+                    ra[k] = ((uint64_t)skw[ia * RW + 2 * k + 1] << 32) | skw[ia * RW + 2 * k];
+                    rb[k] = ((uint64_t)skw[ib * RW + 2 * k + 1] << 32) | skw[ib * RW + 2 * k];
+                }
+                int da = 0, db = 0;
+                if (ELL >= 8) {
+                    constexpr int C1 = ELL * 5 / 8, C2 = ELL * 6 / 8;
+                    da = xdist<0, C1>(ra, cw);
+                    db = xdist<0, C1>(rb, cw);
+                    if (!__any_sync(0xffffffffu, da <= accept || (two && db <= accept))) continue;
+                    da += xdist<C1, C2>(ra, cw);
+                    db += xdist<C1, C2>(rb, cw);
+                    if (!__any_sync(0xffffffffu, da <= accept || (two && db <= accept))) continue;
+                    da += xdist<C2, ELL>(ra, cw);
+                    db += xdist<C2, ELL>(rb, cw);
+                } else {
+                    da = xdist<0, ELL>(ra, cw);
+                    db = xdist<0, ELL>(rb, cw);
+                }
+                {
+                    const int32_t row = sid[ia];
+                    bool pass = da <= accept;
+                    if (pass) pass = size_filter(ssz[ia], colsz, lam) && (side == nullptr || side[row] != side[colx]);
+                    emit_pair(pass, row, colx, cand, cap, ctr);
+                }
+                if (two) {
+                    const int32_t row = sid[ib];
+                    bool pass = db <= accept;
+                    if (pass) pass = size_filter(ssz[ib], colsz, lam) && (side == nullptr || side[row] != side[colx]);
+                    emit_pair(pass, row, colx, cand, cap, ctr);
+                }
+            }
+        }
+    }
 }
 
 // Pair-packed BruteForce for leaves of <= 32 members: thread per pair
@@ -1576,6 +1708,8 @@ struct Driver {
 };
 
 struct LeafWork {
+    const int64_t *blist = nullptr;  // leaves of 33..LB_MAX members (k_leaf_block)
+    int64_t bcnt = 0;
     int64_t tiles = 0;            // 32x32 tiles of leaves with m > 32
     const int64_t *tile_off = nullptr;
     int64_t pairs = 0;            // pairs of leaves with m <= 32 (pair-packed)
@@ -1588,6 +1722,16 @@ template <int ELL>
 void launch_leaf(cpsj_ctx *ctx, cudaStream_t st, const LeafWork &wk, const Level &lv, const cpsj_inputs *in,
                  int32_t accept, double lam, int2 *cand, unsigned long long cap, DevCounters *ctr) {
     ProfScope prof(ctx, PROF_LEAF, st);
+    if (wk.bcnt > 0) {
+        if constexpr (ELL > 0) {
+            const int grid = (int)std::min<int64_t>(wk.bcnt, (int64_t)ctx->sm_count * 16);
+            k_leaf_block<ELL><<<grid, LB_THREADS, 0, st>>>(wk.blist, wk.bcnt, lv.off.p, lv.cnt.p, lv.members.p,
+                                                           in->d_sketch, in->d_sizes, in->d_side, accept, lam, cand,
+                                                           cap, ctr);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+        }
+    }
     if (wk.tiles > 0) {
         DevBuf<int32_t> tile_node;
         if (lv.N < INT32_MAX) {
@@ -1793,18 +1937,41 @@ struct Emitter {
     DevBuf<double> rsims;
     unsigned long long res_bound = 0;  // host upper bound of result slots used
     int64_t total_cand = 0;
+    // deferred: candidates of every level, point phase and K7 accumulate in
+    // one buffer (ctr->cand_n is the cursor) and K5 runs once at the end
+    // (verify_deferred) -- no per-level wait for a candidate count
+    bool defer = false;
 
-    Emitter(cpsj_ctx *c, cudaStream_t s, const cpsj_inputs *i, double l, DevCounters *k)
-        : ctx(c), st(s), in(i), lam(l), ctr(k) {
+    Emitter(cpsj_ctx *c, cudaStream_t s, const cpsj_inputs *i, double l, DevCounters *k, bool deferred = false)
+        : ctx(c), st(s), in(i), lam(l), ctr(k), defer(deferred) {
+        if (defer) cand_cap = std::max<unsigned long long>(1, ctx->cand_cap_hint);
         cand.alloc(cand_cap, st);
         rkeys.alloc(res_cap, st);
         rsims.alloc(res_cap, st);
     }
 
+    void launch_verify(int64_t nc, int64_t first) {
+        if (res_bound + (unsigned long long)nc > res_cap) {
+            const unsigned long long want = std::max(res_bound + (unsigned long long)nc, 2 * res_cap);
+            rkeys.grow(want, res_cap, st);
+            rsims.grow(want, res_cap, st);
+            res_cap = want;
+        }
+        ProfScope prof(ctx, PROF_VERIFY, st);
+        k_verify<<<blocks_for(nc * 32), TPB, 0, st>>>(nc, cand.p + first, in->d_tokens, in->d_offsets, in->d_sizes,
+                                                      lam, rkeys.p, rsims.p, ctr);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+        total_cand += nc;
+        res_bound += (unsigned long long)nc;
+    }
+
     // K5 on the `nc` candidates emitted since the last reset; `regen`
     // re-emits them into a larger buffer when the first pass overflowed
+    // (immediate mode only; deferred mode verifies in verify_deferred)
     template <typename Regen>
     void verify(int64_t nc_in, Regen &&regen) {
+        if (defer) return;
         unsigned long long nc = (unsigned long long)nc_in;
         if (nc > cand_cap) {
             cand_cap = nc + nc / 4 + 1024;
@@ -1812,22 +1979,23 @@ struct Emitter {
             CPSJ_CUDA(cudaMemsetAsync(&ctr->cand_n, 0, sizeof(unsigned long long), st));
             regen();
         }
-        if (nc > 0) {
-            if (res_bound + nc > res_cap) {
-                const unsigned long long want = std::max(res_bound + nc, 2 * res_cap);
-                rkeys.grow(want, res_cap, st);
-                rsims.grow(want, res_cap, st);
-                res_cap = want;
-            }
-            ProfScope prof(ctx, PROF_VERIFY, st);
-            k_verify<<<blocks_for((int64_t)nc * 32), TPB, 0, st>>>((int64_t)nc, cand.p, in->d_tokens, in->d_offsets,
-                                                                   in->d_sizes, lam, rkeys.p, rsims.p, ctr);
-            CPSJ_LAUNCH_CHECK();
-            ctx->launches++;
-            total_cand += (int64_t)nc;
-            res_bound += nc;
-        }
+        if (nc > 0) launch_verify((int64_t)nc, 0);
         CPSJ_CUDA(cudaMemsetAsync(&ctr->cand_n, 0, sizeof(unsigned long long), st));
+    }
+
+    // deferred mode: K5 over every candidate of the call.  Returns false
+    // (nothing verified) when the buffer overflowed; the caller re-runs the
+    // join with ctx->cand_cap_hint raised to fit.
+    bool verify_deferred() {
+        unsigned long long nc = 0;
+        CPSJ_CUDA(cudaMemcpyAsync(&nc, &ctr->cand_n, sizeof(nc), cudaMemcpyDeviceToHost, st));
+        CPSJ_CUDA(cudaStreamSynchronize(st));
+        if (nc > cand_cap) {
+            ctx->cand_cap_hint = nc + nc / 4 + 1024;
+            return false;
+        }
+        if (nc > 0) launch_verify((int64_t)nc, 0);
+        return true;
     }
 
     // K6: sort + unique of the verified pairs into the context arena;
@@ -2003,9 +2171,9 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
         ll.members = std::move(leaf_mem);
         std::unique_ptr<ProfScope> prof_plan(new ProfScope(ctx, PROF_PLAN, st));
         DevBuf<int64_t> tiles(NL + 1, st), spairs(NL + 1, st), internal2(NL + 1, st), imem(NL + 1, st);
-        DevBuf<int64_t> tile_off(NL + 1, st), pair_off(NL + 1, st), slists((size_t)SMALL_CLASSES * NL, st);
-        DevBuf<unsigned long long> scount(SMALL_CLASSES, st);
-        CPSJ_CUDA(cudaMemsetAsync(scount.p, 0, SMALL_CLASSES * sizeof(unsigned long long), st));
+        DevBuf<int64_t> tile_off(NL + 1, st), pair_off(NL + 1, st), slists((size_t)LEAF_CLASSES * NL, st);
+        DevBuf<unsigned long long> scount(LEAF_CLASSES, st);
+        CPSJ_CUDA(cudaMemsetAsync(scount.p, 0, LEAF_CLASSES * sizeof(unsigned long long), st));
         const bool small_kernel = ell == 1 || ell == 2 || ell == 4 || ell == 8 || ell == 16;
         k_plan<<<blocks_for(NL + 1), TPB, 0, st>>>(NL, ll.cnt.p, plan->limit, tiles.p, spairs.p, internal2.p, imem.p,
                                                    ctr, small_kernel ? slists.p : nullptr, scount.p);
@@ -2015,8 +2183,10 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
         if (small_kernel) {
             drv.scan_multi({tiles.p}, {tile_off.p}, NL + 1);
             const int64_t *c64 = reinterpret_cast<const int64_t *>(scount.p);
-            drv.gather({{tile_off.p + NL, c64, c64 + 1, c64 + 2, c64 + 3}}, 5, dscal, sc);
+            drv.gather({{tile_off.p + NL, c64, c64 + 1, c64 + 2, c64 + 3, c64 + 4}}, 6, dscal, sc);
             work2.small = true;
+            work2.blist = slists.p + (size_t)SMALL_CLASSES * NL;
+            work2.bcnt = sc[5];
             work2.sl.wcum[0] = 0;
             for (int k = 0; k < SMALL_CLASSES; ++k) {
                 work2.sl.list[k] = slists.p + (size_t)k * NL;
@@ -2033,12 +2203,15 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
         work2.tile_off = tile_off.p;
         prof_plan.reset();
         auto gen = [&]() {
-            if (work2.tiles > 0 || work2.pairs > 0 || (work2.small && work2.sl.wcum[SMALL_CLASSES] > 0))
+            if (work2.tiles > 0 || work2.pairs > 0 || work2.bcnt > 0 ||
+                (work2.small && work2.sl.wcum[SMALL_CLASSES] > 0))
                 leaf_dispatch(ctx, st, work2, ll, in, plan->accept_dist, plan->lambda_, em.cand.p, em.cand_cap, ctr);
         };
         gen();
-        drv.gather({{reinterpret_cast<const int64_t *>(&ctr->cand_n)}}, 1, dscal, sc);
-        em.verify(sc[0], gen);
+        if (!em.defer) {
+            drv.gather({{reinterpret_cast<const int64_t *>(&ctr->cand_n)}}, 1, dscal, sc);
+            em.verify(sc[0], gen);
+        }
     }
     if (trace)
         fprintf(stderr, "[join] K7 (roots from depth %s%d): %lld roots (max %lld members, %d CTAs x %d KB smem) -> "
@@ -2075,8 +2248,10 @@ std::vector<int64_t> frontier_share(const std::vector<int32_t> &cnt, int32_t lim
 
 }  // namespace
 
-void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
-               cudaStream_t st) {
+// one self-join pass; returns false (and nothing else is valid) when the
+// deferred candidate buffer overflowed -- self_join re-runs with it grown
+bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
+                    cudaStream_t st) {
     require(in && plan && stats, "null argument");
     require(in->n >= 0 && in->t >= 1 && in->t <= 32767 && in->ell >= 1, "bad input shape");
     require(plan->n_reps >= 0 && plan->limit >= 1, "bad plan");
@@ -2099,7 +2274,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         CPSJ_CUDA(cudaMemcpyAsync(ctr.p, &init, sizeof(init), cudaMemcpyHostToDevice, st));
     }
     // candidate and result buffers grow on demand
-    Emitter em(ctx, st, in, lam, ctr.p);
+    Emitter em(ctx, st, in, lam, ctr.p, /*deferred=*/true);
     int64_t max_depth = 0, levels = 0;
     int64_t lvl_visits = 0, lvl_entries = 0;  // level-path work (K7 counts its own on the device)
 
@@ -2132,7 +2307,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     const int vbits = plan->value_bits > 0 && plan->value_bits < 32 ? plan->value_bits : 32;
     // per-level scratch (see above)
     DevBuf<int64_t> tiles, spairs, internal, imem, tile_off, pair_off, iscan, im_off, slists;
-    DevBuf<unsigned long long> scount(SMALL_CLASSES, st);
+    DevBuf<unsigned long long> scount(LEAF_CLASSES, st);
     // leaves of <= 32 members by size class (k_leaf_small) for compile-time ell
     // K7 deferral state (see the level loop)
     Level defl;
@@ -2183,7 +2358,7 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             // above it, then keep this rank's share of the level's nodes
             CPSJ_CUDA(cudaMemcpyAsync(&snap_ctr, ctr.p, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
             CPSJ_CUDA(cudaStreamSynchronize(st));
-            snap_cand = em.total_cand;
+            snap_cand = (int64_t)snap_ctr.cand_n;  // candidates emitted so far (verified at the end)
             snap_caps = (int64_t)ctx->cap_events.size();
             cut_done = true;
             // size-balanced contiguous cut (cpsj_plan): every rank derives
@@ -2225,8 +2400,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         for (DevBuf<int64_t> *b : {&tiles, &spairs, &internal, &imem, &tile_off, &pair_off, &iscan, &im_off})
             b->ensure(N + 1, st);
         if (small_kernel) {
-            slists.ensure((size_t)SMALL_CLASSES * N, st);
-            CPSJ_CUDA(cudaMemsetAsync(scount.p, 0, SMALL_CLASSES * sizeof(unsigned long long), st));
+            slists.ensure((size_t)LEAF_CLASSES * N, st);
+            CPSJ_CUDA(cudaMemsetAsync(scount.p, 0, LEAF_CLASSES * sizeof(unsigned long long), st));
         }
         CPSJ_CUDA(cudaMemsetAsync(&ctr.p->lvl_max_int, 0, sizeof(long long), st));
         const int64_t *maxint_p = reinterpret_cast<const int64_t *>(&ctr.p->lvl_max_int);
@@ -2247,12 +2422,14 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
             drv.scan_multi({tiles.p, internal.p, imem.p}, {tile_off.p, iscan.p, im_off.p}, N + 1);
             const int64_t *c64 = reinterpret_cast<const int64_t *>(scount.p);
             drv.gather({{tile_off.p + N, iscan.p + N, im_off.p + N, c64, c64 + 1, c64 + 2, c64 + 3, maxint_p,
-                         defn_p, defm_p}},
-                       10, dscal.p, sc);
+                         defn_p, defm_p, c64 + 4}},
+                       11, dscal.p, sc);
             max_int = sc[7];
             def_n = sc[8];
             def_m = sc[9];
             work.small = true;
+            work.blist = slists.p + (size_t)SMALL_CLASSES * N;
+            work.bcnt = sc[10];
             work.sl.wcum[0] = 0;
             for (int k = 0; k < SMALL_CLASSES; ++k) {
                 const int W = 4 << k;
@@ -2304,7 +2481,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
         // the leaves run on the side stream, overlapping the internal-node
         // kernels below; the main stream joins them before sync (B).  A
         // regeneration (candidate buffer grown) runs on the main stream.
-        const bool any_leaf = work.tiles > 0 || work.pairs > 0 || (work.small && work.sl.wcum[SMALL_CLASSES] > 0);
+        const bool any_leaf = work.tiles > 0 || work.pairs > 0 || work.bcnt > 0 ||
+                              (work.small && work.sl.wcum[SMALL_CLASSES] > 0);
         const bool leaf_forked = any_leaf && overlap_leaves && ctx->side != nullptr;
         cudaStream_t leaf_st = leaf_forked ? ctx->side : st;
         auto gen_leaf = [&]() {
@@ -2491,6 +2669,28 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                     (long long)(work.small ? work.sl.cnt[0] + work.sl.cnt[1] + work.sl.cnt[2] + work.sl.cnt[3]
                                            : work.pairs), (long long)n_leaf_cand, (long long)n_flag, (long long)E,
                     (long long)nx.N, us, drv.sync_us, (long long)max_int);
+            if (E > 0) {
+                // split segment sizes (survivors of a node, one segment per
+                // selected position): entries by size class
+                std::vector<int64_t> h_eoff(n_int + 1), h_nsel(n_int + 1);
+                CPSJ_CUDA(cudaMemcpy(h_eoff.data(), e_off.p, (n_int + 1) * 8, cudaMemcpyDeviceToHost));
+                CPSJ_CUDA(cudaMemcpy(h_nsel.data(), nsel.p, n_int * 8, cudaMemcpyDeviceToHost));
+                const int64_t lim[6] = {256, 1024, 4096, 16384, 65536, INT64_MAX};
+                int64_t segs[6] = {}, ents[6] = {};
+                for (int64_t k = 0; k < n_int; ++k) {
+                    if (h_nsel[k] == 0) continue;
+                    const int64_t sz = (h_eoff[k + 1] - h_eoff[k]) / h_nsel[k];
+                    int b = 0;
+                    while (sz > lim[b]) ++b;
+                    segs[b] += h_nsel[k];
+                    ents[b] += sz * h_nsel[k];
+                }
+                fprintf(stderr, "[join]   segments (count/entries) <=256 %lld/%lld <=1K %lld/%lld <=4K %lld/%lld "
+                        "<=16K %lld/%lld <=64K %lld/%lld >64K %lld/%lld\n",
+                        (long long)segs[0], (long long)ents[0], (long long)segs[1], (long long)ents[1],
+                        (long long)segs[2], (long long)ents[2], (long long)segs[3], (long long)ents[3],
+                        (long long)segs[4], (long long)ents[4], (long long)segs[5], (long long)ents[5]);
+            }
         }
         std::swap(lv, nx);  // the old level's arrays become the next level's storage
         nx.N = nx.M = 0;
@@ -2504,7 +2704,8 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
                     dscal.p, trace, def_depth.p);
     }
 
-    // ---- K6: sort + unique of the verified pairs
+    // ---- K5 over every candidate of the call, then K6
+    if (!em.verify_deferred()) return false;
     const DevCounters hc = em.finish(drv);
     const int64_t nres = (int64_t)hc.res_n;
     if (hc.err) throw Error{CPSJ_E_PICK, "node-sketch pick index out of range (uniform draw == 1.0)"};
@@ -2536,6 +2737,18 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     stats->verify_tokens = (int64_t)hc.vtok;
     stats->gpu_launches = ctx->launches - launches0;
     stats->lib_calls = ctx->lib_calls - lib0;
+    return true;
+}
+
+void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
+               cudaStream_t st) {
+    // a call whose candidates overflow the deferred buffer raises
+    // ctx->cand_cap_hint and runs again (later calls start large enough)
+    if (getenv("CPSJ_TINY_CAND_CAP") != nullptr) ctx->cand_cap_hint = 16;  // test hook: force the re-run
+    for (int attempt = 0;; ++attempt) {
+        if (self_join_once(ctx, in, plan, stats, st)) return;
+        require(attempt < 8, "candidate buffer keeps overflowing");
+    }
 }
 
 // ------------------------------------------------- MinHash LSH join (Alg. 3)

@@ -186,12 +186,14 @@ def test_join_matches_reference_golden(name):
 
 
 @pytest.mark.parametrize("env", [{"CPSJ_NO_SUBTREE": "1"}, {"CPSJ_K7_TINY_SCRATCH": "1"},
-                                 {"CPSJ_NO_SMALL_LEAF": "1", "CPSJ_NO_LEAF_OVERLAP": "1"}])
+                                 {"CPSJ_NO_SMALL_LEAF": "1", "CPSJ_NO_LEAF_OVERLAP": "1"},
+                                 {"CPSJ_TINY_CAND_CAP": "1"}])
 @pytest.mark.parametrize("name", ["planted_880", "dense_cluster", "c1_sample"])
 def test_join_alternate_paths_match_reference_golden(name, env, monkeypatch):
     """The same trees through the level kernels only (no K7 handoff), through
-    K7 with scratch small enough to overflow and retry, and through the
-    pair-packed small-leaf kernel on the main stream: identical results."""
+    K7 with scratch small enough to overflow and retry, through the
+    pair-packed small-leaf kernel on the main stream, and with a candidate
+    buffer small enough that the call re-runs: identical results."""
     from paper_1707_06814_b200 import Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -524,6 +526,30 @@ def test_pipelined_embed_with_sketch_hint_matches_oracle(chunks):
     assert np.array_equal(emb.sketches(8, 7), sk)
     res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=0.5, seed=7, repetitions=2))
     assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)
+
+
+@pytest.mark.parametrize("cfg,scale", [(2, 0.07), (3, 0.1)])
+def test_default_pipelined_embed_matches_oracle(cfg, scale):
+    """The DEFAULT chunk schedule (chunks=None: first chunk 1/32 growing by
+    1.8, used by embed_dataset for n >= 65,536 and by the bench's e2e leg)
+    gives the oracle's values, sketches and join bit for bit."""
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
+    from paper_1707_06814_b200.embed import _PIPELINE_MIN_SETS, _chunk_bounds
+    from paper_1707_06814_b200.workloads import generate
+    w = generate(cfg, scale=scale)
+    assert w.n >= _PIPELINE_MIN_SETS and len(_chunk_bounds(w.n, None)) > 3
+    ds = Dataset.from_csr(w.tokens, w.offsets, w.d)
+    emb = embed_dataset(EmbeddingParams(t=128, seed=7), ds, sketch=(8, 7))
+    values, sk, ref = O.full_pipeline(w.tokens, w.offsets, w.sizes, lam=0.5, emb_seed=7, seed=7, repetitions=2)
+    assert np.array_equal(emb.values, values)
+    assert np.array_equal(emb.sketches(8, 7), sk)
+    res = cpsjoin_self_arrays(emb, CPSJoinParams(lambda_=0.5, seed=7, repetitions=2))
+    assert np.array_equal(res.a, ref.a) and np.array_equal(res.b, ref.b)
+    assert np.array_equal(res.similarity, ref.sims)
+    c = res.counters
+    assert [c.pre_candidates, c.candidates, c.results, c.max_depth, c.peak_live_members] == \
+        [ref.pre_candidates, ref.candidates, ref.results, ref.max_depth, ref.peak_live_members]
 
 
 # ---- R x S join (SURVEY.md 8(f) rank 1), against reference-made fixtures
