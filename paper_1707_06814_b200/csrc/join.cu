@@ -103,12 +103,14 @@ __device__ __host__ __forceinline__ int small_class(int64_t m) {
 __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit,
                        int64_t *__restrict__ tiles, int64_t *__restrict__ spairs, int64_t *__restrict__ internal,
                        int64_t *__restrict__ imem, DevCounters *ctr, int64_t *__restrict__ slists = nullptr,
-                       unsigned long long *__restrict__ scount = nullptr, int32_t defer_max = 0) {
+                       unsigned long long *__restrict__ scount = nullptr, int32_t defer_max = 0,
+                       int32_t block_max = LB_MAX_PLAN) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long pre = 0;
     // with class lists, leaves of 33..LB_MAX_PLAN members go to the block
-    // kernel instead of the tile kernel (needs limit <= LB_MAX_PLAN)
-    const bool block_leaves = slists != nullptr && limit <= LB_MAX_PLAN;
+    // kernel instead of the tile kernel (needs limit <= LB_MAX_PLAN;
+    // block_max = 0 turns it off: CPSJ_NO_BLOCK_LEAF, A/B)
+    const bool block_leaves = slists != nullptr && limit <= block_max;
     if (slists != nullptr) {
         // small leaves straight into their class lists (warp-aggregated
         // appends; the order inside a class does not matter)
@@ -1707,6 +1709,12 @@ struct Driver {
     }
 };
 
+// A/B switch: CPSJ_NO_BLOCK_LEAF=1 sends every leaf > 32 members to the tile kernel
+inline int32_t block_leaf_max() {
+    const char *e = getenv("CPSJ_NO_BLOCK_LEAF");
+    return (e != nullptr && e[0] == '1') ? 0 : LB_MAX_PLAN;
+}
+
 struct LeafWork {
     const int64_t *blist = nullptr;  // leaves of 33..LB_MAX members (k_leaf_block)
     int64_t bcnt = 0;
@@ -2176,7 +2184,8 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
         CPSJ_CUDA(cudaMemsetAsync(scount.p, 0, LEAF_CLASSES * sizeof(unsigned long long), st));
         const bool small_kernel = ell == 1 || ell == 2 || ell == 4 || ell == 8 || ell == 16;
         k_plan<<<blocks_for(NL + 1), TPB, 0, st>>>(NL, ll.cnt.p, plan->limit, tiles.p, spairs.p, internal2.p, imem.p,
-                                                   ctr, small_kernel ? slists.p : nullptr, scount.p);
+                                                   ctr, small_kernel ? slists.p : nullptr, scount.p, 0,
+                                                   block_leaf_max());
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
         LeafWork work2;
@@ -2412,7 +2421,8 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
         defer_active = defer_active || (depth >= defer_depth && (defer_forced || lv.M <= DEFER_LEVEL_MEMBERS));
         const int32_t defer_max = (subtree_on && defer_active) ? ST_MAX_SUBM : 0;
         k_plan<<<blocks_for(N + 1), TPB, 0, st>>>(N, lv.cnt.p, plan->limit, tiles.p, spairs.p, internal.p, imem.p,
-                                                  ctr.p, small_kernel ? slists.p : nullptr, scount.p, defer_max);
+                                                  ctr.p, small_kernel ? slists.p : nullptr, scount.p, defer_max,
+                                                  block_leaf_max());
         CPSJ_LAUNCH_CHECK();
         ctx->launches++;
         int64_t sc[12];
