@@ -541,9 +541,9 @@ int orc_self_join_ct(const uint32_t *tok, const int64_t *off, const int64_t *siz
  * (m <= limit), m * bit_length(m) otherwise, C_i the cost of nodes before i
  * -- and runs the kept subtrees depth first with their reference stack
  * base S (S(child_j) = S(parent) + sizes of children before j).  Rank 0
- * reports the counters of the part above the cut; every rank reports its
- * pairs (ranks != 0 none from above the cut when no node reaches it), the
- * cut depth as reached, and the stack peak of what it expanded. */
+ * reports the counters and pairs of the part above the cut; every rank
+ * reports the pairs and counters of its kept subtrees, the cut depth as
+ * reached, and the stack peak of what it expanded. */
 typedef struct { const Ctx *c; Acc *accs; Node *nodes; const int64_t *kept; Scratch *w; } KeptArgs;
 static void kept_body(void *p, int64_t lo, int64_t hi, int tid) {
     KeptArgs *a = p;
@@ -618,9 +618,8 @@ int orc_self_join_frontier(const uint32_t *tok, const int64_t *off, const int64_
             for (int i = 0; i < nt; i++) scratch_free(&ws[i]);
             free(ws);
             free(kept);
-        } else if (rank != 0) {
-            top->len = 0;  /* the trees ended above the cut: rank 0 reports all of them */
         }
+        if (rank != 0) top->len = 0;  /* pairs above the cut: rank 0 reports them */
         free(level.v);
     }
     int err = merge_accs(accs, counted, nt + 1, out_keys, out_sims, out_n, counters, cap_events, n_cap_events);

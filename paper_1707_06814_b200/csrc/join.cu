@@ -1994,7 +1994,9 @@ struct Emitter {
     // deferred mode: K5 over every candidate of the call.  Returns false
     // (nothing verified) when the buffer overflowed; the caller re-runs the
     // join with ctx->cand_cap_hint raised to fit.
-    bool verify_deferred() {
+    // Candidates before `first` are skipped (a frontier rank != 0 leaves
+    // the part above the cut to rank 0).
+    bool verify_deferred(int64_t first = 0) {
         unsigned long long nc = 0;
         CPSJ_CUDA(cudaMemcpyAsync(&nc, &ctr->cand_n, sizeof(nc), cudaMemcpyDeviceToHost, st));
         CPSJ_CUDA(cudaStreamSynchronize(st));
@@ -2002,7 +2004,7 @@ struct Emitter {
             ctx->cand_cap_hint = nc + nc / 4 + 1024;
             return false;
         }
-        if (nc > 0) launch_verify((int64_t)nc, 0);
+        if ((int64_t)nc > first) launch_verify((int64_t)nc - first, first);
         return true;
     }
 
@@ -2714,8 +2716,10 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
                     dscal.p, trace, def_depth.p);
     }
 
-    // ---- K5 over every candidate of the call, then K6
-    if (!em.verify_deferred()) return false;
+    // ---- K5 over every candidate of the call (a frontier rank != 0: only
+    // those found below the cut), then K6
+    const int64_t first_cand = (frontier && plan->frontier_rank != 0) ? (cut_done ? snap_cand : INT64_MAX) : 0;
+    if (!em.verify_deferred(first_cand)) return false;
     const DevCounters hc = em.finish(drv);
     const int64_t nres = (int64_t)hc.res_n;
     if (hc.err) throw Error{CPSJ_E_PICK, "node-sketch pick index out of range (uniform draw == 1.0)"};
@@ -2727,11 +2731,11 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
     stats->max_depth = std::max<int64_t>(max_depth, hc.max_depth);
     stats->peak_live_members = (n >= 2 && R > 0) ? hc.peak : 0;
     if (frontier && plan->frontier_rank != 0) {
-        // counted by every rank above the cut: rank 0 reports it
+        // counted by every rank above the cut: rank 0 reports it (its
+        // candidates were never verified here, so results and pairs are
+        // this rank's share already)
         if (cut_done) {
             stats->pre_candidates -= (int64_t)snap_ctr.pre;
-            stats->candidates -= snap_cand;
-            stats->results -= (int64_t)snap_ctr.res_n;
             ctx->cap_events.erase(ctx->cap_events.begin(), ctx->cap_events.begin() + snap_caps);
         } else {
             // the tree ended above the cut: rank 0 has all of it
