@@ -65,6 +65,7 @@ int cpsj_ctx_create(int device, cpsj_ctx **out) {
         uint64_t thr = UINT64_MAX;
         CPSJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
         CPSJ_CUDA(cudaMallocHost(&ctx->h_scalars, 16 * sizeof(int64_t)));
+        CPSJ_CUDA(cudaMallocHost(&ctx->h_levels, 128 * sizeof(int64_t)));
         CPSJ_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         CPSJ_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         CPSJ_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
@@ -89,6 +90,10 @@ int cpsj_ctx_destroy(cpsj_ctx *ctx) {
         ctx->ing_src.release();
         if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
         ctx->h_scalars = nullptr;
+        if (ctx->h_levels) cudaFreeHost(ctx->h_levels);
+        ctx->h_levels = nullptr;
+        ctx->dle_arena.release();
+        ctx->dle_part.release();
         if (ctx->side) cudaStreamDestroy(ctx->side);
         if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
         if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);

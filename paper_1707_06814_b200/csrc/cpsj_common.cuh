@@ -183,6 +183,13 @@ struct cpsj_ctx {
     // candidate-buffer capacity of the self-join (grows when a call
     // overflows it; that call is re-run once with the larger buffer)
     uint64_t cand_cap_hint = 1ull << 22;
+    // device-driven level engine (join.cu, dle.cuh): join-wide arena,
+    // scan partials, deferred-root capacity, pinned per-level readbacks
+    cpsj::DevBuf<uint8_t> dle_arena;
+    uint64_t dle_arena_cap = 0;
+    cpsj::DevBuf<int64_t> dle_part;
+    int64_t dle_roots_cap = 0;
+    int64_t *h_levels = nullptr;  // pinned, DLE_MAX_LEVELS entries
 };
 
 struct cpsj_family {

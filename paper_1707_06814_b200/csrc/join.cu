@@ -28,6 +28,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -524,15 +526,12 @@ constexpr int LB_WARPS = LB_THREADS / 32;
 constexpr int LB_MAX = LB_MAX_PLAN;
 
 template <int ELL>
-__global__ void __launch_bounds__(LB_THREADS) k_leaf_block(const int64_t *__restrict__ list, int64_t cnt,
-                                                           const int64_t *__restrict__ nd_off,
-                                                           const int32_t *__restrict__ nd_cnt,
-                                                           const int32_t *__restrict__ members,
-                                                           const uint64_t *__restrict__ sketch,
-                                                           const int32_t *__restrict__ sizes,
-                                                           const int8_t *__restrict__ side, int32_t accept, double lam,
-                                                           int2 *__restrict__ cand, unsigned long long cap,
-                                                           DevCounters *ctr) {
+__device__ __forceinline__ void leaf_block_body(const int64_t *__restrict__ list, int64_t cnt,
+                                                const int64_t *__restrict__ nd_off, const int32_t *__restrict__ nd_cnt,
+                                                const int32_t *__restrict__ members,
+                                                const uint64_t *__restrict__ sketch, const int32_t *__restrict__ sizes,
+                                                const int8_t *__restrict__ side, int32_t accept, double lam,
+                                                int2 *__restrict__ cand, unsigned long long cap, DevCounters *ctr) {
     constexpr int RW = 2 * ELL + 1;
     __shared__ uint32_t skw[LB_MAX * RW];
     __shared__ int32_t sid[LB_MAX], ssz[LB_MAX];
@@ -623,6 +622,19 @@ __global__ void __launch_bounds__(LB_THREADS) k_leaf_block(const int64_t *__rest
             }
         }
     }
+}
+
+template <int ELL>
+__global__ void __launch_bounds__(LB_THREADS) k_leaf_block(const int64_t *__restrict__ list, int64_t cnt,
+                                                           const int64_t *__restrict__ nd_off,
+                                                           const int32_t *__restrict__ nd_cnt,
+                                                           const int32_t *__restrict__ members,
+                                                           const uint64_t *__restrict__ sketch,
+                                                           const int32_t *__restrict__ sizes,
+                                                           const int8_t *__restrict__ side, int32_t accept, double lam,
+                                                           int2 *__restrict__ cand, unsigned long long cap,
+                                                           DevCounters *ctr) {
+    leaf_block_body<ELL>(list, cnt, nd_off, nd_cnt, members, sketch, sizes, side, accept, lam, cand, cap, ctr);
 }
 
 // Pair-packed BruteForce for leaves of <= 32 members: thread per pair
@@ -2052,8 +2064,22 @@ struct Emitter {
 // `small`, exclusive scan `sscan`) and their subtrees by k_subtree, then the
 // K4 leaf kernels on the leaves it emitted.  Scratch exhaustion restores
 // the device counters and relaunches with twice the scratch.
+// the roots K7 starts from: node records of a level (or a deferred-root list)
+// whose member offsets index `members`
+struct RootView {
+    int64_t N;
+    const int32_t *members;
+    const int64_t *off;
+    const int32_t *cnt;
+    const uint64_t *seed;
+    const int64_t *S;
+};
+inline RootView root_view(const Level &lv) {
+    return RootView{lv.N, lv.members.p, lv.off.p, lv.cnt.p, lv.seed.p, lv.S.p};
+}
+
 void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in, const cpsj_plan *plan,
-                 const Level &lv, const int64_t *small, const int64_t *sscan, int64_t n_small, int64_t max_small,
+                 const RootView &lv, const int64_t *small, const int64_t *sscan, int64_t n_small, int64_t max_small,
                  int depth, DevCounters *ctr, int64_t *dscal, bool trace, const int32_t *root_depth = nullptr) {
     cudaStream_t st = drv.st;
     const int t = in->t, ell = in->ell;
@@ -2097,7 +2123,7 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
     DevBuf<int64_t> leaf_off, cap_sizes(cap_cap, st);
     DevBuf<StQueue> qs(1, st);
     SubtreeArgs a{};
-    a.members = lv.members.p;
+    a.members = lv.members;
     a.sketch = in->d_sketch;
     a.ell = ell;
     a.t = t;
@@ -2119,8 +2145,8 @@ void run_subtree(cpsj_ctx *ctx, Driver &drv, Emitter &em, const cpsj_inputs *in,
     a.subm = subm;
     auto launch = [&]() {
         CPSJ_CUDA(cudaMemsetAsync(q.p, 0, q_cap * sizeof(StNode), st));
-        k_subtree_init<<<blocks_for(n_small), TPB, 0, st>>>(n_small, slist.p, lv.off.p, lv.cnt.p, lv.seed.p,
-                                                            lv.S.p, depth, q.p, qs.p, root_depth);
+        k_subtree_init<<<blocks_for(n_small), TPB, 0, st>>>(n_small, slist.p, lv.off, lv.cnt, lv.seed, lv.S, depth,
+                                                            q.p, qs.p, root_depth);
         CPSJ_LAUNCH_CHECK();
         a.cand = em.cand.p;
         a.cand_cap = em.cand_cap;
@@ -2257,7 +2283,284 @@ std::vector<int64_t> frontier_share(const std::vector<int32_t> &cnt, int32_t lim
     return kept;
 }
 
+#include "dle.cuh"
+
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// Device-driven level engine (dle.cuh): the same join with no host read-back
+// inside a level.  Returns 1 = done, 0 = re-run (arena / root list / cap
+// list / candidate buffer grew), -1 = not applicable (the host-driven loop
+// handles it: count-table rule, frontier sharding, ell outside
+// {1,2,4,8,16}, limit > 256, or CPSJ_HOST_LEVELS=1).
+constexpr int DLE_MAX_LEVELS = 128;
+
+int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
+                  cudaStream_t st) {
+    const int ell = in->ell, t = in->t;
+    const char *host_env = getenv("CPSJ_HOST_LEVELS");
+    const bool frontier = plan->frontier_ranks > 1;
+    if ((host_env != nullptr && host_env[0] == '1') || plan->use_count_table || frontier ||
+        !(ell == 1 || ell == 2 || ell == 4 || ell == 8 || ell == 16) || plan->limit > LB_MAX_PLAN ||
+        plan->depth_cap + 2 > DLE_MAX_LEVELS || t > ST_MAX_SEL)
+        return -1;
+    std::memset(stats, 0, sizeof(*stats));
+    const int64_t launches0 = ctx->launches, lib0 = ctx->lib_calls;
+    const int64_t n = in->n;
+    const int32_t R = plan->n_reps;
+    const double lam = plan->lambda_;
+    ctx->n_pairs = 0;
+    ctx->cap_events.clear();
+    Driver drv{ctx, st};
+    DevBuf<DevCounters> ctr(1, st);
+    DevBuf<int64_t> dscal(16, st);
+    {
+        DevCounters init{};
+        init.peak = n;
+        CPSJ_CUDA(cudaMemcpyAsync(ctr.p, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+    }
+    Emitter em(ctx, st, in, lam, ctr.p, /*deferred=*/true);
+    const char *trace_env = getenv("CPSJ_JOIN_TRACE");
+    const bool trace = trace_env != nullptr && trace_env[0] == '1';
+    const int vbits = plan->value_bits > 0 && plan->value_bits < 32 ? plan->value_bits : 32;
+    const uint64_t child_off = (uint64_t)t + 64ull * (uint64_t)ell;
+    const char *sub_env = getenv("CPSJ_NO_SUBTREE");
+    const bool subtree_on = !(sub_env != nullptr && sub_env[0] == '1') && ell <= 32;
+    const char *dd_env = getenv("CPSJ_DEFER_DEPTH");
+    const int defer_depth = dd_env != nullptr ? atoi(dd_env) : 0;
+    const long long defer_level_m = dd_env != nullptr ? LLONG_MAX : (long long)DEFER_LEVEL_MEMBERS;
+    const char *ovl_env = getenv("CPSJ_NO_LEAF_OVERLAP");
+    const bool overlap_leaves = !(ovl_env != nullptr && ovl_env[0] == '1') && ctx->side != nullptr;
+
+    // join-wide arena: grows (and the call re-runs) when a call exhausts it
+    if (ctx->dle_arena_cap == 0) ctx->dle_arena_cap = std::max<uint64_t>(256ull << 20, (uint64_t)n * R * 200ull);
+    if (ctx->dle_arena.n < ctx->dle_arena_cap) ctx->dle_arena.alloc(ctx->dle_arena_cap, st);
+    if (ctx->dle_part.n < (size_t)(4 * dle::DLE_MAX_TILES)) ctx->dle_part.alloc(4 * dle::DLE_MAX_TILES, st);
+    if (ctx->dle_roots_cap == 0) ctx->dle_roots_cap = std::max<int64_t>(1 << 16, 4 * (int64_t)R * n / plan->limit);
+    const int64_t cap_cap = 1 << 16;
+    DevBuf<int64_t> cap_sizes(cap_cap, st);
+    DevBuf<int64_t> r_off(ctx->dle_roots_cap, st), r_S(ctx->dle_roots_cap, st);
+    DevBuf<int32_t> r_cnt(ctx->dle_roots_cap, st), r_depth(ctx->dle_roots_cap, st);
+    DevBuf<uint64_t> r_seed(ctx->dle_roots_cap, st), seeds(std::max(R, 1), st);
+    DevBuf<dle::DArena> ar(1, st);
+    DevBuf<dle::DLevel> lvs(DLE_MAX_LEVELS, st);
+    DevBuf<int> sticky(1, st);
+    {
+        dle::DArena h{ctx->dle_arena.p, 0ull, (unsigned long long)ctx->dle_arena_cap, 0};
+        CPSJ_CUDA(cudaMemcpyAsync(ar.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    }
+    CPSJ_CUDA(cudaMemsetAsync(lvs.p, 0, sizeof(dle::DLevel) * DLE_MAX_LEVELS, st));
+    CPSJ_CUDA(cudaMemsetAsync(sticky.p, 0, sizeof(int), st));
+    CPSJ_CUDA(cudaMemcpyAsync(seeds.p, plan->h_rep_seeds, (size_t)R * 8, cudaMemcpyHostToDevice, st));
+    dle::DRoots roots{r_off.p, r_cnt.p, r_seed.p, r_S.p, r_depth.p, ctx->dle_roots_cap};
+
+    const int sms = ctx->sm_count;
+    const unsigned G = (unsigned)(sms * 8), GB = (unsigned)(sms * 4), GS = (unsigned)(sms * 2);
+    auto L = [&](int d) { return lvs.p + d; };
+    auto dscan = [&](int d, int k, std::initializer_list<int> ins, std::initializer_list<int> outs, int n_off,
+                     int n_plus, int mkeys) {
+        dle::DScan a{};
+        a.L = L(d);
+        int i = 0;
+        for (int o : ins) a.in_off[i++] = o;
+        i = 0;
+        for (int o : outs) a.out_off[i++] = o;
+        a.n_off = n_off;
+        a.n_plus = n_plus;
+        a.mkeys = mkeys;
+        a.part = ctx->dle_part.p;
+        auto run = [&](auto kk) {
+            constexpr int KK = decltype(kk)::value;
+            dle::k_dscan_reduce<KK><<<GS, SCAN_THREADS, 0, st>>>(a);
+            dle::k_dscan_partials<KK><<<1, SCAN_THREADS, 0, st>>>(a);
+            dle::k_dscan_apply<KK><<<GS, SCAN_THREADS, 0, st>>>(a);
+        };
+        if (k == 1) run(std::integral_constant<int, 1>{});
+        else run(std::integral_constant<int, 2>{});
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches += 3;
+    };
+    using dle::DLevel;
+    // worst-case split-sort passes: value bits + bits of the largest segment count
+    int max_pass = (vbits + 31 + 7) / 8;
+    max_pass = std::min(max_pass, 8);
+
+    dle::k_dle_alloc_roots<<<1, 1, 0, st>>>(ar.p, L(0), n, R);
+    dle::k_dle_roots<<<G, TPB, 0, st>>>(L(0), n, R, seeds.p);
+    CPSJ_LAUNCH_CHECK();
+    ctx->launches += 2;
+    std::vector<cudaEvent_t> evs;
+    int last = -1;         // deepest enqueued level
+    int known_empty = -1;  // first level observed empty (lagged)
+    int checked = 0;       // levels whose count was read
+    for (int depth = 0; depth + 1 < DLE_MAX_LEVELS && depth <= plan->depth_cap + 1; ++depth) {
+        DLevel *Lp = L(depth), *Nx = L(depth + 1);
+        std::unique_ptr<ProfScope> prof(new ProfScope(ctx, PROF_PLAN, st));
+        dle::k_dle_plan<<<G, TPB, 0, st>>>(Lp, plan->limit, block_leaf_max(), subtree_on ? ST_MAX_SUBM : 0, depth,
+                                          defer_depth, defer_level_m, sticky.p, ctr.p);
+        dscan(depth, 2, {DL_OFF(internal), DL_OFF(imem)}, {DL_OFF(iscan), DL_OFF(im_off)}, DL_OFF(N), 1, 0);
+        if (subtree_on) {
+            dle::k_dle_defer<<<G, TPB, 0, st>>>(Lp, plan->limit, depth,
+                                               reinterpret_cast<const int32_t *>(ctx->dle_arena.p), roots, ctr.p,
+                                               ar.p);
+        }
+        dle::k_dle_alloc_internal<<<1, 1, 0, st>>>(ar.p, Lp, ell, t, &ctr.p->visits);
+        dle::k_dle_compact_internal<<<G, TPB, 0, st>>>(Lp);
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches += 4;
+        prof.reset();
+        // leaves of the level: K4 on the side stream (overlaps the rest)
+        cudaStream_t lst = st;
+        if (overlap_leaves) {
+            CPSJ_CUDA(cudaEventRecord(ctx->ev_fork, st));
+            CPSJ_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            lst = ctx->side;
+        }
+        {
+            ProfScope pl(ctx, PROF_LEAF, lst);
+            auto leafk = [&](auto ek) {
+                constexpr int EK = decltype(ek)::value;
+                dle::k_dle_leaf_small<EK><<<G, TPB, 0, lst>>>(Lp, in->d_sketch, in->d_sizes, in->d_side,
+                                                             plan->accept_dist, lam, em.cand.p, em.cand_cap, ctr.p);
+                dle::k_dle_leaf_block<EK><<<(unsigned)(sms * 16), LB_THREADS, 0, lst>>>(
+                    Lp, in->d_sketch, in->d_sizes, in->d_side, plan->accept_dist, lam, em.cand.p, em.cand_cap, ctr.p);
+            };
+            switch (ell) {
+                case 1: leafk(std::integral_constant<int, 1>{}); break;
+                case 2: leafk(std::integral_constant<int, 2>{}); break;
+                case 4: leafk(std::integral_constant<int, 4>{}); break;
+                case 8: leafk(std::integral_constant<int, 8>{}); break;
+                default: leafk(std::integral_constant<int, 16>{}); break;
+            }
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 2;
+        }
+        if (overlap_leaves) CPSJ_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
+        // node phase (K2)
+        {
+            ProfScope pn(ctx, PROF_NODE, st);
+            dle::k_dle_node_sketch<<<GB, TPB, 0, st>>>(Lp, in->d_sketch, ell, t, ctr.p);
+            dle::k_dle_flags<<<G, TPB, 0, st>>>(Lp, in->d_sketch, ell, plan->flag_dist);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 2;
+            dscan(depth, 1, {DL_OFF(flags)}, {DL_OFF(fscan)}, DL_OFF(Mi), 1, 0);
+            dle::k_dle_survivors<<<G, TPB, 0, st>>>(Lp);
+            dle::k_dle_flag_list<<<G, TPB, 0, st>>>(Lp);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 2;
+        }
+        {
+            ProfScope pp(ctx, PROF_POINT, st);
+            dle::k_dle_point<<<G, TPB, 0, st>>>(Lp, in->d_sketch, ell, in->d_sizes, in->d_side, plan->accept_dist,
+                                               lam, em.cand.p, em.cand_cap, ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+        }
+        // split (K3)
+        {
+            ProfScope ps(ctx, PROF_SPLIT, st);
+            dle::k_dle_select<<<G, TPB, 0, st>>>(Lp, depth, plan->depth_cap, t, plan->split_p, cap_sizes.p, cap_cap,
+                                                ctr.p, ar.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+            dscan(depth, 2, {DL_OFF(nsel), DL_OFF(nent)}, {DL_OFF(seg_off), DL_OFF(e_off)}, DL_OFF(n_int), 1, 0);
+            dle::k_dle_alloc_split<<<1, 1, 0, st>>>(ar.p, Lp, vbits, &ctr.p->entries);
+            dle::k_dle_build_keys<<<G, TPB, 0, st>>>(Lp, t, in->d_values, vbits, &ctr.p->verr);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 2;
+            for (int p = 0; p < max_pass; ++p) {
+                dle::k_dle_rs_hist<<<GB, RS_THREADS, 0, st>>>(Lp, p);
+                dle::k_dle_rs_colscan<<<256, 1024, 0, st>>>(Lp, p);
+                dle::k_dle_rs_scatter<<<GB, RS_THREADS, 0, st>>>(Lp, p);
+                ctx->launches += 3;
+            }
+            CPSJ_LAUNCH_CHECK();
+            dscan(depth, 2, {}, {DL_OFF(kscan), DL_OFF(mscan)}, DL_OFF(E), 1, 1);
+            dle::k_dle_alloc_children<<<1, 1, 0, st>>>(ar.p, Lp, Nx, 0);
+            dle::k_dle_children<<<G, TPB, 0, st>>>(Lp, Nx, child_off);
+            dle::k_dle_child_sizes<<<G, TPB, 0, st>>>(Nx, ctr.p);
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches += 3;
+        }
+        // lagged termination: the next level's liveness, read without a sync
+        CPSJ_CUDA(cudaMemcpyAsync(ctx->h_levels + depth, &Nx->live, sizeof(int), cudaMemcpyDeviceToHost, st));
+        cudaEvent_t ev;
+        CPSJ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CPSJ_CUDA(cudaEventRecord(ev, st));
+        evs.push_back(ev);
+        last = depth;
+        // at most two levels enqueued ahead of the last one read
+        if (depth - checked >= 2) CPSJ_CUDA(cudaEventSynchronize(evs[checked]));
+        while (checked <= depth && cudaEventQuery(evs[checked]) == cudaSuccess) {
+            if (*reinterpret_cast<volatile int *>(ctx->h_levels + checked) == 0 && known_empty < 0)
+                known_empty = checked + 1;
+            ++checked;
+        }
+        if (known_empty >= 0) break;
+    }
+    if (overlap_leaves) CPSJ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    CPSJ_CUDA(cudaStreamSynchronize(st));
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    // read back the levels, the arena state and the counters
+    std::vector<DLevel> hl(last + 2);
+    CPSJ_CUDA(cudaMemcpy(hl.data(), lvs.p, sizeof(DLevel) * (last + 2), cudaMemcpyDeviceToHost));
+    dle::DArena har{};
+    CPSJ_CUDA(cudaMemcpy(&har, ar.p, sizeof(har), cudaMemcpyDeviceToHost));
+    DevCounters hc0{};
+    CPSJ_CUDA(cudaMemcpy(&hc0, ctr.p, sizeof(hc0), cudaMemcpyDeviceToHost));
+    if (har.overflow) {
+        // a larger arena / root list next time (both are cheap to over-size)
+        ctx->dle_arena_cap *= 2;
+        if ((int64_t)hc0.def_slot >= ctx->dle_roots_cap) ctx->dle_roots_cap *= 2;
+        if (trace) fprintf(stderr, "[join] device level engine: arena / list overflow, re-run with x2\n");
+        return 0;
+    }
+    int64_t max_depth = 0, levels = 0;
+    for (int d = 0; d <= last + 1 && d < (int)hl.size(); ++d) {
+        if (hl[d].N > 0) {
+            max_depth = d;
+            ++levels;
+        }
+        if (trace && hl[d].N > 0)
+            fprintf(stderr, "[join] (device levels) depth %d nodes %lld members %lld internal %lld (members %lld) "
+                            "segments %lld entries %lld children %lld | sort passes %d\n",
+                    d, hl[d].N, hl[d].M, hl[d].n_int, hl[d].Mi, hl[d].n_seg, hl[d].E, hl[d].Nn, hl[d].npass);
+    }
+    if (hc0.cap_n) {
+        std::vector<int64_t> h(hc0.cap_n);
+        CPSJ_CUDA(cudaMemcpy(h.data(), cap_sizes.p, hc0.cap_n * 8, cudaMemcpyDeviceToHost));
+        ctx->cap_events.insert(ctx->cap_events.end(), h.begin(), h.end());
+    }
+    // K7 on every deferred root (members in the arena)
+    const int64_t def_n = (int64_t)hc0.def_slot;
+    if (def_n > 0) {
+        RootView rv{def_n, reinterpret_cast<const int32_t *>(ctx->dle_arena.p), r_off.p, r_cnt.p, r_seed.p, r_S.p};
+        int first_depth = 0;
+        for (int d = 0; d <= last; ++d)
+            if (hl[d].defer_max > 0) { first_depth = d; break; }
+        run_subtree(ctx, drv, em, in, plan, rv, nullptr, nullptr, def_n, ST_MAX_SUBM, first_depth, ctr.p, dscal.p,
+                    trace, r_depth.p);
+    }
+    if (!em.verify_deferred(0)) return 0;
+    const DevCounters hc = em.finish(drv);
+    const int64_t nres = (int64_t)hc.res_n;
+    if (hc.err) throw Error{CPSJ_E_PICK, "node-sketch pick index out of range (uniform draw == 1.0)"};
+    if (hc.verr) throw Error{CPSJ_E_ARG, "a MinHash value is >= 2^value_bits (cpsj_plan.value_bits too small)"};
+    stats->n_pairs = ctx->n_pairs;
+    stats->pre_candidates = (int64_t)hc.pre;
+    stats->candidates = em.total_cand;
+    stats->results = nres;
+    stats->max_depth = std::max<int64_t>(max_depth, hc.max_depth);
+    stats->peak_live_members = hc.peak;
+    stats->n_depth_cap_events = (int64_t)ctx->cap_events.size();
+    stats->n_levels = levels;
+    stats->internal_visits = (int64_t)hc.visits;
+    stats->split_entries = (int64_t)hc.entries;
+    stats->verify_tokens = (int64_t)hc.vtok;
+    stats->gpu_launches = ctx->launches - launches0;
+    stats->lib_calls = ctx->lib_calls - lib0;
+    return 1;
+}
 
 // one self-join pass; returns false (and nothing else is valid) when the
 // deferred candidate buffer overflowed -- self_join re-runs with it grown
@@ -2712,8 +3015,8 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
     if (def_done > 0) {
         defl.N = def_done;
         defl.M = def_m_done;
-        run_subtree(ctx, drv, em, in, plan, defl, nullptr, nullptr, def_done, ST_MAX_SUBM, first_defer_depth, ctr.p,
-                    dscal.p, trace, def_depth.p);
+        run_subtree(ctx, drv, em, in, plan, root_view(defl), nullptr, nullptr, def_done, ST_MAX_SUBM,
+                    first_defer_depth, ctr.p, dscal.p, trace, def_depth.p);
     }
 
     // ---- K5 over every candidate of the call (a frontier rank != 0: only
@@ -2759,7 +3062,17 @@ void self_join(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj
     // a call whose candidates overflow the deferred buffer raises
     // ctx->cand_cap_hint and runs again (later calls start large enough)
     if (getenv("CPSJ_TINY_CAND_CAP") != nullptr) ctx->cand_cap_hint = 16;  // test hook: force the re-run
+    if (getenv("CPSJ_TINY_ARENA") != nullptr) ctx->dle_arena_cap = 1 << 16;  // test hook: arena re-run
+    const bool dle_ok = in->n >= 2 && plan->n_reps > 0;
     for (int attempt = 0;; ++attempt) {
+        if (dle_ok) {
+            const int r = self_join_dle(ctx, in, plan, stats, st);
+            if (r == 1) return;
+            if (r == 0) {
+                require(attempt < 16, "device level engine keeps overflowing");
+                continue;
+            }
+        }
         if (self_join_once(ctx, in, plan, stats, st)) return;
         require(attempt < 8, "candidate buffer keeps overflowing");
     }
