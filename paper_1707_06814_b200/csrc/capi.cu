@@ -94,6 +94,7 @@ int cpsj_ctx_destroy(cpsj_ctx *ctx) {
         ctx->h_levels = nullptr;
         ctx->dle_arena.release();
         ctx->dle_part.release();
+        ctx->dle_status.release();
         if (ctx->side) cudaStreamDestroy(ctx->side);
         if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
         if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);

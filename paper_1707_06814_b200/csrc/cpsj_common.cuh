@@ -190,6 +190,8 @@ struct cpsj_ctx {
     cpsj::DevBuf<int64_t> dle_part;
     int64_t dle_roots_cap = 0;
     int64_t *h_levels = nullptr;  // pinned, DLE_MAX_LEVELS entries
+    cpsj::DevBuf<unsigned long long> dle_status;  // single-pass scan status words
+    unsigned long long dle_epoch = 0;             // last scan epoch used (< 2^20)
 };
 
 struct cpsj_family {

@@ -216,7 +216,7 @@ __device__ __forceinline__ void kill_level(DLevel *L) {
 }
 
 // after the plan scan: arrays of the level's internal nodes
-__global__ void k_dle_alloc_internal(DArena *ar, DLevel *L, int ell, int t, unsigned long long *visits) {
+__device__ void alloc_internal(DArena *ar, DLevel *L, int ell, int t, unsigned long long *visits) {
     if (!L->live) return;
     const long long N = L->N;
     const long long n_int = L->iscan[N], Mi = L->im_off[N];
@@ -239,7 +239,7 @@ __global__ void k_dle_alloc_internal(DArena *ar, DLevel *L, int ell, int t, unsi
 }
 
 // after the selection scan: the split's arrays (64-bit keys, radix scratch)
-__global__ void k_dle_alloc_split(DArena *ar, DLevel *L, int vbits, unsigned long long *entries) {
+__device__ void alloc_split(DArena *ar, DLevel *L, int vbits, unsigned long long *entries) {
     if (!L->live) return;
     const long long n_int = L->n_int;
     const long long n_seg = n_int > 0 ? L->seg_off[n_int] : 0, E = n_int > 0 ? L->e_off[n_int] : 0;
@@ -262,7 +262,7 @@ __global__ void k_dle_alloc_split(DArena *ar, DLevel *L, int vbits, unsigned lon
 }
 
 // after the group-mark scan: the next level's node arrays + plan scratch
-__global__ void k_dle_alloc_children(DArena *ar, DLevel *L, DLevel *Nx, int nx_defer_max) {
+__device__ void alloc_children(DArena *ar, DLevel *L, DLevel *Nx, int nx_defer_max) {
     Nx->live = 0;
     if (!L->live) return;
     const long long E = L->E;
@@ -285,6 +285,134 @@ __global__ void k_dle_alloc_children(DArena *ar, DLevel *L, DLevel *Nx, int nx_d
         return;
     }
     Nx->live = 1;
+}
+
+__global__ void k_dle_alloc_internal(DArena *ar, DLevel *L, int ell, int t, unsigned long long *visits) {
+    alloc_internal(ar, L, ell, t, visits);
+}
+__global__ void k_dle_alloc_split(DArena *ar, DLevel *L, int vbits, unsigned long long *entries) {
+    alloc_split(ar, L, vbits, entries);
+}
+__global__ void k_dle_alloc_children(DArena *ar, DLevel *L, DLevel *Nx, int nx_defer_max) {
+    alloc_children(ar, L, Nx, nx_defer_max);
+}
+
+// -------------------------------------------------- single-pass scans
+//
+// One launch per scan (instead of reduce / partials / apply): tiles are
+// taken in order from a ticket counter, each tile publishes its aggregate
+// and then its inclusive prefix in a status word, and the next tiles look
+// back over those words (decoupled look-back).  A status word packs
+// (epoch : 20 | flag : 2 | value : 42); the epoch (unique per scan call of
+// the context) makes stale words from earlier scans invisible, so the array
+// is never cleared.  The block that scans the last tile then runs the
+// level's allocation step (hook), which only needs the totals.
+struct DScan1 {
+    const DLevel *L;
+    int in_off[2], out_off[2];
+    int n_off, n_plus, mkeys;
+    unsigned long long *status;   // [2][DLE_MAX_TILES]
+    unsigned long long *ticket;
+    unsigned long long epoch;     // < 2^20
+    int hook;                     // 0 none, 1 alloc_internal, 2 alloc_split, 3 alloc_children
+    DArena *ar;
+    DLevel *Lw, *Nx;
+    int ell, t, vbits;
+    unsigned long long *acc;      // visits / entries accumulator of the hook
+};
+constexpr unsigned long long ST_VAL_MASK = (1ull << 42) - 1ull;
+
+__device__ __forceinline__ unsigned long long st_pack(unsigned long long epoch, unsigned flag, long long v) {
+    return (epoch << 44) | ((unsigned long long)flag << 42) | ((unsigned long long)v & ST_VAL_MASK);
+}
+
+template <int K>
+__global__ void __launch_bounds__(SCAN_THREADS) k_dscan1(DScan1 a) {
+    __shared__ int64_t wsum[32];
+    __shared__ long long s_tile, s_excl[K];
+    if (!a.L->live) return;
+    const int64_t n = dsize(a.L, a.n_off) + a.n_plus;
+    const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    DScan as{};
+    as.L = a.L;
+    for (int k = 0; k < K; ++k) as.in_off[k] = a.in_off[k];
+    as.mkeys = a.mkeys;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = (long long)atomicAdd(a.ticket, 1ull);
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (tile >= tiles) break;
+        const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * 4;
+        int64_t v[K][4];
+        dscan_load<K>(as, n, base, v);
+        int64_t local[K], agg[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) local[k] = scan_block(v[k][0] + v[k][1] + v[k][2] + v[k][3], wsum, agg[k]);
+        // publish, then look back (warp k for array k)
+        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (w < K) {
+            unsigned long long *stat = a.status + (size_t)w * DLE_MAX_TILES;
+            const long long my = agg[w];
+            if (tile == 0) {
+                if (lane == 0) {
+                    s_excl[w] = 0;
+                    atomicExch(stat + tile, st_pack(a.epoch, 2u, my));
+                }
+            } else {
+                if (lane == 0) atomicExch(stat + tile, st_pack(a.epoch, 1u, my));
+                long long excl = 0;
+                int64_t j = tile - 1;
+                // the warp reads 32 predecessors at a time
+                for (;;) {
+                    const int64_t q = j - lane;
+                    unsigned long long word = 0;
+                    unsigned flag = 3;  // lanes before tile 0 act as a zero prefix
+                    if (q >= 0) {
+                        do {
+                            word = *(volatile unsigned long long *)(stat + q);
+                            flag = (word >> 44) == a.epoch ? (unsigned)((word >> 42) & 3u) : 0u;
+                        } while (flag == 0);
+                    }
+                    const long long val = q >= 0 ? (long long)(word & ST_VAL_MASK) : 0;
+                    // the nearest lane with an inclusive prefix ends the walk
+                    const unsigned incl = __ballot_sync(0xffffffffu, flag >= 2);
+                    const int stop = incl ? __ffs(incl) - 1 : 32;
+                    long long sum = lane <= stop && lane < 32 ? val : 0;
+                    if (lane > stop) sum = 0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+                    excl += __shfl_sync(0xffffffffu, sum, 0);
+                    if (incl) break;
+                    j -= 32;
+                }
+                if (lane == 0) {
+                    s_excl[w] = excl;
+                    atomicExch(stat + tile, st_pack(a.epoch, 2u, excl + my));
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            int64_t *out = dptr<int64_t>(a.L, a.out_off[k]);
+            int64_t run = s_excl[k] + local[k];
+#pragma unroll
+            for (int j2 = 0; j2 < 4; ++j2) {
+                if (base + j2 < n) out[base + j2] = run;
+                run += v[k][j2];
+            }
+        }
+        if (tile == tiles - 1 && a.hook != 0) {
+            __syncthreads();
+            __threadfence();
+            if (threadIdx.x == 0) {
+                if (a.hook == 1) alloc_internal(a.ar, a.Lw, a.ell, a.t, a.acc);
+                else if (a.hook == 2) alloc_split(a.ar, a.Lw, a.vbits, a.acc);
+                else alloc_children(a.ar, a.Lw, a.Nx, 0);
+            }
+        }
+        __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------- level
@@ -439,8 +567,10 @@ __global__ void k_dle_survivors(DLevel *L) {
     DLE_FOR_WARPS(base, Mi) {
         const int64_t e = base + (threadIdx.x & 31);
         const int64_t k = warp_segment(L->im_off_c, n_int + 1, e);
-        if (e >= Mi || L->flags[e]) continue;
-        L->surv[e - L->fscan[e]] = L->members[L->off[L->ilist[k]] + (e - L->im_off_c[k])];
+        if (e >= Mi) continue;
+        // survivors in member order; flagged members listed for k_dle_point
+        if (L->flags[e]) L->flist[L->fscan[e]] = e;
+        else L->surv[e - L->fscan[e]] = L->members[L->off[L->ilist[k]] + (e - L->im_off_c[k])];
     }
 }
 

@@ -2355,11 +2355,30 @@ int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, c
     dle::DRoots roots{r_off.p, r_cnt.p, r_seed.p, r_S.p, r_depth.p, ctx->dle_roots_cap};
 
     const int sms = ctx->sm_count;
-    const unsigned G = (unsigned)(sms * 8), GB = (unsigned)(sms * 4), GS = (unsigned)(sms * 2);
+    // grid-stride kernels: enough warps to cover the gathers of a large
+    // level, few enough that an empty launch is cheap (CPSJ_DLE_GRID = CTAs
+    // per SM of the element-wise kernels, A/B)
+    const char *genv = getenv("CPSJ_DLE_GRID");
+    const int gmul = genv != nullptr ? std::max(1, atoi(genv)) : 4;
+    const unsigned G = (unsigned)(sms * gmul), GB = (unsigned)(sms * std::max(1, gmul / 2)),
+                   GS = (unsigned)(sms * std::max(1, gmul / 4));
     auto L = [&](int d) { return lvs.p + d; };
+    if (ctx->dle_status.n < (size_t)(2 * dle::DLE_MAX_TILES)) {
+        ctx->dle_status.alloc(2 * dle::DLE_MAX_TILES, st);
+        CPSJ_CUDA(cudaMemsetAsync(ctx->dle_status.p, 0, 2 * dle::DLE_MAX_TILES * 8, st));
+        ctx->dle_epoch = 0;
+    }
+    DevBuf<unsigned long long> tickets(4 * DLE_MAX_LEVELS + 8, st);
+    CPSJ_CUDA(cudaMemsetAsync(tickets.p, 0, (4 * DLE_MAX_LEVELS + 8) * 8, st));
+    int ticket_i = 0;
+    // one single-pass scan (k_dscan1) with an optional allocation hook
     auto dscan = [&](int d, int k, std::initializer_list<int> ins, std::initializer_list<int> outs, int n_off,
-                     int n_plus, int mkeys) {
-        dle::DScan a{};
+                     int n_plus, int mkeys, int hook = 0, unsigned long long *acc = nullptr) {
+        if (++ctx->dle_epoch >= (1ull << 20)) {
+            CPSJ_CUDA(cudaMemsetAsync(ctx->dle_status.p, 0, 2 * dle::DLE_MAX_TILES * 8, st));
+            ctx->dle_epoch = 1;
+        }
+        dle::DScan1 a{};
         a.L = L(d);
         int i = 0;
         for (int o : ins) a.in_off[i++] = o;
@@ -2368,22 +2387,31 @@ int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, c
         a.n_off = n_off;
         a.n_plus = n_plus;
         a.mkeys = mkeys;
-        a.part = ctx->dle_part.p;
-        auto run = [&](auto kk) {
-            constexpr int KK = decltype(kk)::value;
-            dle::k_dscan_reduce<KK><<<GS, SCAN_THREADS, 0, st>>>(a);
-            dle::k_dscan_partials<KK><<<1, SCAN_THREADS, 0, st>>>(a);
-            dle::k_dscan_apply<KK><<<GS, SCAN_THREADS, 0, st>>>(a);
-        };
-        if (k == 1) run(std::integral_constant<int, 1>{});
-        else run(std::integral_constant<int, 2>{});
+        a.status = ctx->dle_status.p;
+        a.ticket = tickets.p + (ticket_i++);
+        a.epoch = ctx->dle_epoch;
+        a.hook = hook;
+        a.ar = ar.p;
+        a.Lw = L(d);
+        a.Nx = L(d + 1);
+        a.ell = ell;
+        a.t = t;
+        a.vbits = vbits;
+        a.acc = acc;
+        require(ticket_i <= 4 * DLE_MAX_LEVELS + 8, "too many scans");
+        if (k == 1) dle::k_dscan1<1><<<GS, SCAN_THREADS, 0, st>>>(a);
+        else dle::k_dscan1<2><<<GS, SCAN_THREADS, 0, st>>>(a);
         CPSJ_LAUNCH_CHECK();
-        ctx->launches += 3;
+        ctx->launches += 1;
     };
     using dle::DLevel;
     // worst-case split-sort passes: value bits + bits of the largest segment count
-    int max_pass = (vbits + 31 + 7) / 8;
-    max_pass = std::min(max_pass, 8);
+    // a level's internal nodes have > limit members, so it has at most
+    // R n / (limit + 1) of them, each selecting at most t positions
+    int seg_bits = 1;
+    while (seg_bits < 40 && ((uint64_t)((int64_t)R * n / (plan->limit + 1) + 1) * (uint64_t)t >> seg_bits) != 0)
+        ++seg_bits;
+    const int max_pass = std::min(8, (vbits + seg_bits + 7) / 8);
 
     dle::k_dle_alloc_roots<<<1, 1, 0, st>>>(ar.p, L(0), n, R);
     dle::k_dle_roots<<<G, TPB, 0, st>>>(L(0), n, R, seeds.p);
@@ -2398,16 +2426,16 @@ int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, c
         std::unique_ptr<ProfScope> prof(new ProfScope(ctx, PROF_PLAN, st));
         dle::k_dle_plan<<<G, TPB, 0, st>>>(Lp, plan->limit, block_leaf_max(), subtree_on ? ST_MAX_SUBM : 0, depth,
                                           defer_depth, defer_level_m, sticky.p, ctr.p);
-        dscan(depth, 2, {DL_OFF(internal), DL_OFF(imem)}, {DL_OFF(iscan), DL_OFF(im_off)}, DL_OFF(N), 1, 0);
+        dscan(depth, 2, {DL_OFF(internal), DL_OFF(imem)}, {DL_OFF(iscan), DL_OFF(im_off)}, DL_OFF(N), 1, 0,
+              /*hook=alloc_internal*/ 1, &ctr.p->visits);
         if (subtree_on) {
             dle::k_dle_defer<<<G, TPB, 0, st>>>(Lp, plan->limit, depth,
                                                reinterpret_cast<const int32_t *>(ctx->dle_arena.p), roots, ctr.p,
                                                ar.p);
         }
-        dle::k_dle_alloc_internal<<<1, 1, 0, st>>>(ar.p, Lp, ell, t, &ctr.p->visits);
         dle::k_dle_compact_internal<<<G, TPB, 0, st>>>(Lp);
         CPSJ_LAUNCH_CHECK();
-        ctx->launches += 4;
+        ctx->launches += 3;
         prof.reset();
         // leaves of the level: K4 on the side stream (overlaps the rest)
         cudaStream_t lst = st;
@@ -2445,9 +2473,8 @@ int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, c
             ctx->launches += 2;
             dscan(depth, 1, {DL_OFF(flags)}, {DL_OFF(fscan)}, DL_OFF(Mi), 1, 0);
             dle::k_dle_survivors<<<G, TPB, 0, st>>>(Lp);
-            dle::k_dle_flag_list<<<G, TPB, 0, st>>>(Lp);
             CPSJ_LAUNCH_CHECK();
-            ctx->launches += 2;
+            ctx->launches += 1;
         }
         {
             ProfScope pp(ctx, PROF_POINT, st);
@@ -2463,11 +2490,11 @@ int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, c
                                                 ctr.p, ar.p);
             CPSJ_LAUNCH_CHECK();
             ctx->launches++;
-            dscan(depth, 2, {DL_OFF(nsel), DL_OFF(nent)}, {DL_OFF(seg_off), DL_OFF(e_off)}, DL_OFF(n_int), 1, 0);
-            dle::k_dle_alloc_split<<<1, 1, 0, st>>>(ar.p, Lp, vbits, &ctr.p->entries);
+            dscan(depth, 2, {DL_OFF(nsel), DL_OFF(nent)}, {DL_OFF(seg_off), DL_OFF(e_off)}, DL_OFF(n_int), 1, 0,
+                  /*hook=alloc_split*/ 2, &ctr.p->entries);
             dle::k_dle_build_keys<<<G, TPB, 0, st>>>(Lp, t, in->d_values, vbits, &ctr.p->verr);
             CPSJ_LAUNCH_CHECK();
-            ctx->launches += 2;
+            ctx->launches += 1;
             for (int p = 0; p < max_pass; ++p) {
                 dle::k_dle_rs_hist<<<GB, RS_THREADS, 0, st>>>(Lp, p);
                 dle::k_dle_rs_colscan<<<256, 1024, 0, st>>>(Lp, p);
@@ -2475,12 +2502,11 @@ int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, c
                 ctx->launches += 3;
             }
             CPSJ_LAUNCH_CHECK();
-            dscan(depth, 2, {}, {DL_OFF(kscan), DL_OFF(mscan)}, DL_OFF(E), 1, 1);
-            dle::k_dle_alloc_children<<<1, 1, 0, st>>>(ar.p, Lp, Nx, 0);
+            dscan(depth, 2, {}, {DL_OFF(kscan), DL_OFF(mscan)}, DL_OFF(E), 1, 1, /*hook=alloc_children*/ 3);
             dle::k_dle_children<<<G, TPB, 0, st>>>(Lp, Nx, child_off);
             dle::k_dle_child_sizes<<<G, TPB, 0, st>>>(Nx, ctr.p);
             CPSJ_LAUNCH_CHECK();
-            ctx->launches += 3;
+            ctx->launches += 2;
         }
         // lagged termination: the next level's liveness, read without a sync
         CPSJ_CUDA(cudaMemcpyAsync(ctx->h_levels + depth, &Nx->live, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -2490,7 +2516,7 @@ int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, c
         evs.push_back(ev);
         last = depth;
         // at most two levels enqueued ahead of the last one read
-        if (depth - checked >= 2) CPSJ_CUDA(cudaEventSynchronize(evs[checked]));
+        if (depth - checked >= 1) CPSJ_CUDA(cudaEventSynchronize(evs[checked]));
         while (checked <= depth && cudaEventQuery(evs[checked]) == cudaSuccess) {
             if (*reinterpret_cast<volatile int *>(ctx->h_levels + checked) == 0 && known_empty < 0)
                 known_empty = checked + 1;
