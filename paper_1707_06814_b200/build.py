@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 SO = os.path.join(OUT_DIR, "libcpsjoin_b200.so")
 SOURCES = ["minhash.cu", "join.cu", "exact.cu", "ingest.cu", "dense.cu", "capi.cu"]
-HEADERS = ["cpsj_common.cuh", "radix.cuh"]
+HEADERS = ["cpsj_common.cuh", "radix.cuh", "dle.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -17,9 +17,10 @@
 // SHFL so one token is hashed by every function of the chunk at once.
 // Production kernels (L <= 3; half-warp per set, 8 functions per lane, one
 // LDS.128 per key byte, sets visited in a length-bucketed order):
-//   k_sketch_s16<L>: sketches.  Entries carry (top 15 hash bits << 1 |
-//     sketch bit), the minimum key carries the argmin's sketch bit, two
-//     functions per register with VIMNMX3.U16x2; shared-memory bound.
+//   k_sketch_s16<L>: sketches.  Entries carry (sketch bit << 15 | top 15
+//     hash bits); unsigned and signed SIMD minima (VIMNMX3.U16x2 / .S16x2,
+//     two functions per register) give the argmin's sketch bit; upper-byte
+//     entries cached across sorted tokens (sketch_chunk_bits).
 //   k_values_h8<L>: values.  Position keys (hash16 << 16 | position),
 //     first/last tie detection, pairwise VIMNMX3; integer-ALU bound.
 //   k_embed_h8<L>: both in one launch (the pipelined embed's chunks).
@@ -529,9 +530,9 @@ __global__ void k_build_simg(const uint32_t *__restrict__ hi, const uint32_t *__
                     if (bitmask != nullptr) bit ^= bitmask[(size_t)fn * 32 + kk * 8];
                 }
         }
-        // sketch image: (top 15 hash bits << 1) | bit; values image (no bit
+        // sketch image: (bit << 15) | top 15 hash bits; values image (no bit
         // tables): the top 16 hash bits
-        v16[q] = bitmask != nullptr ? ((v >> 17) << 1) | (bit & 1u) : v >> 16;
+        v16[q] = bitmask != nullptr ? ((bit & 1u) << 15) | (v >> 17) : v >> 16;
     }
     img[e] = make_uint4((v16[0] << 16) | v16[1], (v16[2] << 16) | v16[3], (v16[4] << 16) | v16[5],
                         (v16[6] << 16) | v16[7]);
@@ -540,6 +541,11 @@ __global__ void k_build_simg(const uint32_t *__restrict__ hi, const uint32_t *__
 __device__ __forceinline__ uint32_t vmin16x2(uint32_t a, uint32_t b) {
     uint32_t r;
     asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t vmin16x2s(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
     return r;
 }
 __device__ __forceinline__ uint32_t vmax16x2(uint32_t a, uint32_t b) {
@@ -581,7 +587,7 @@ __device__ __noinline__ uint32_t half_resolve15(const uint32_t *__restrict__ hi,
         uint32_t e = lds32(col + __byte_perm(tk, 0u, 0x4404));
         if (L > 1) e ^= lds32(col + 65536u + (tk & 0xFF00u));
         if (L > 2) e ^= lds32(col + 131072u + __byte_perm(tk, 0u, 0x4424));
-        if (((e >> (sh + 1)) & 0x7FFFu) == m15) {
+        if (((e >> sh) & 0x7FFFu) == m15) {
             const uint32_t b0 = tk & 255, b1 = (tk >> 8) & 255, b2 = (tk >> 16) & 255, b3 = tk >> 24;
             const uint32_t h = __ldg(hi + base + b0) ^ __ldg(hi + base + 256 + b1) ^ __ldg(hi + base + 512 + b2) ^
                                __ldg(hi + base + 768 + b3);
@@ -605,7 +611,163 @@ __device__ __noinline__ uint32_t half_resolve15(const uint32_t *__restrict__ hi,
     return bt;
 }
 
-template <int L>
+// ---------------------------------------------------------------------
+// One set x one 128-function chunk of the sketch kernels (k_sketch_s16 and
+// the sketch jobs of k_embed_h8): returns this lane's 8 sketch bits (bit q =
+// function l + 16q of the chunk).
+//
+// Keys are (bit << 15) | h15.  mU = unsigned min, mS = SIGNED min of the
+// same keys (VIMNMX3.U16x2 / .S16x2, two tokens per instruction, no key
+// rewrite for the second track): keys with bit 1 are negative as s16, so
+//   mU = (0, min h15 over the bit-0 tokens)  if a bit-0 token exists,
+//   mS = (1, min h15 over the bit-1 tokens)  if a bit-1 token exists,
+// and mU == mS when every token carries the same bit.  The argmin's bit is
+// the bit of the smaller h15; equal h15 on both sides is exactly "tokens
+// tied on the 15 compared bits carry different bits" and is re-resolved on
+// the full 64-bit hash (hashing.py:124,197-211), so the result is exact.
+//
+// PFX: tokens are sorted, so neighbours share their upper key bytes; the
+// XOR of the upper-byte entries P = T1[b1] ^ T2[b2] stays in registers and is
+// reloaded only when tok >> 8 changes (T2 only when tok >> 16 changes).  On
+// Zipf-ranked tokens (c2: 55% / 11% of the tokens change byte 1 / byte 2)
+// this cuts the shared-memory lookups per evaluation from L to about 1.65.
+template <int L, bool PFX>
+__device__ __forceinline__ uint32_t sketch_chunk_bits(
+    const uint32_t *__restrict__ tokens, int64_t beg, int len, int c, int F, const uint32_t *__restrict__ hi,
+    const uint32_t *__restrict__ lo, const uint32_t *__restrict__ bitmask, uint32_t smem0, uint32_t lane_base,
+    int lane, int l, unsigned hmask) {
+    uint32_t mU[4], mS[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        mU[r] = 0xFFFFFFFFu;
+        mS[r] = 0x7FFF7FFFu;
+    }
+    if (PFX && L > 1) {
+        uint32_t P[4] = {0u, 0u, 0u, 0u}, P2[4] = {0u, 0u, 0u, 0u};
+        uint32_t cur = 0xFFFFFFFFu;  // tok >> 8 of the cached upper entries
+        auto refresh = [&](uint32_t tok) {
+            const uint32_t pre = tok >> 8;
+            if (pre != cur) {
+                if (L > 2 && ((pre ^ cur) >> 8) != 0u) {
+                    const uint4 v = lds128(lane_base + 131072u + __byte_perm(tok, 0u, 0x4424));
+                    P2[0] = v.x; P2[1] = v.y; P2[2] = v.z; P2[3] = v.w;
+                }
+                const uint4 v = lds128(lane_base + 65536u + (tok & 0xFF00u));
+                P[0] = v.x ^ P2[0]; P[1] = v.y ^ P2[1]; P[2] = v.z ^ P2[2]; P[3] = v.w ^ P2[3];
+                cur = pre;
+            }
+        };
+        for (int base = 0; base < len; base += 16) {
+            const int cnt = len - base < 16 ? len - base : 16;
+            const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
+            int j = 0;
+#pragma unroll 2
+            for (; j + 1 < cnt; j += 2) {
+                const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
+                const uint4 ea = lds128(lane_base + __byte_perm(ta, 0u, 0x4404));
+                const uint4 eb = lds128(lane_base + __byte_perm(tb, 0u, 0x4404));
+                refresh(ta);
+                const uint32_t ka[4] = {ea.x ^ P[0], ea.y ^ P[1], ea.z ^ P[2], ea.w ^ P[3]};
+                refresh(tb);
+                const uint32_t kb[4] = {eb.x ^ P[0], eb.y ^ P[1], eb.z ^ P[2], eb.w ^ P[3]};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    mU[r] = __vimin3_u16x2(mU[r], ka[r], kb[r]);
+                    mS[r] = __vimin3_s16x2(mS[r], ka[r], kb[r]);
+                }
+            }
+            if (j < cnt) {
+                const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                const uint4 ea = lds128(lane_base + __byte_perm(ta, 0u, 0x4404));
+                refresh(ta);
+                const uint32_t ka[4] = {ea.x ^ P[0], ea.y ^ P[1], ea.z ^ P[2], ea.w ^ P[3]};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    mU[r] = vmin16x2(mU[r], ka[r]);
+                    mS[r] = vmin16x2s(mS[r], ka[r]);
+                }
+            }
+        }
+    } else {
+        for (int base = 0; base < len; base += 16) {
+            const int cnt = len - base < 16 ? len - base : 16;
+            const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
+            int j = 0;
+#pragma unroll 2
+            for (; j + 1 < cnt; j += 2) {
+                const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
+                const uint4 ha = key_oct<L>(ta, lane_base);
+                const uint4 hb = key_oct<L>(tb, lane_base);
+                const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w}, xb[4] = {hb.x, hb.y, hb.z, hb.w};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    mU[r] = __vimin3_u16x2(mU[r], xa[r], xb[r]);
+                    mS[r] = __vimin3_s16x2(mS[r], xa[r], xb[r]);
+                }
+            }
+            if (j < cnt) {
+                const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
+                const uint4 ha = key_oct<L>(ta, lane_base);
+                const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    mU[r] = vmin16x2(mU[r], xa[r]);
+                    mS[r] = vmin16x2s(mS[r], xa[r]);
+                }
+            }
+        }
+    }
+    // register j: function l + 32j in the high half (bit 2j), l + 32j + 16 in
+    // the low half (bit 2j + 1)
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int hl = 0; hl < 2; ++hl) {
+            const int sh = hl == 0 ? 16 : 0, q = 2 * j + hl;
+            const uint32_t u = (mU[j] >> sh) & 0xFFFFu, sg = (mS[j] >> sh) & 0xFFFFu;
+            // u == sg: one bit value only; else u = (0, h0), sg = (1, h1)
+            const uint32_t h1 = sg & 0x7FFFu;
+            const uint32_t bit = u == sg ? u >> 15 : (h1 < u ? 1u : 0u);
+            bits |= bit << q;
+            const int f = (c << 7) + l + 32 * j + 16 * hl;
+            const bool tie = len > 1 && f < F && (u ^ sg) == 0x8000u;
+            unsigned tied = __ballot_sync(hmask, tie);
+            while (tied) {
+                const int src = __ffs(tied) - 1;
+                tied &= tied - 1;
+                const int fs = __shfl_sync(hmask, f, src);
+                const uint32_t m15 = __shfl_sync(hmask, u, src);
+                const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
+                const uint32_t tw = half_resolve15<L>(hi, lo, fs, m15, col, sh, tokens, beg, len, l, hmask);
+                if (lane == src) bits = (bits & ~(1u << q)) | (sketch_bit_g(bitmask, fs, tw) << q);
+            }
+        }
+    }
+    return len <= 0 ? 0u : bits;
+}
+
+// this lane's word of the sketch row of its half's set: ballots transpose
+// the per-lane bits (bit q = function l + 16q) into 4 words of 32 functions
+__device__ __forceinline__ void sketch_store_words(uint32_t bits, int h, int l, bool has, int c, int words32,
+                                                   int64_t row, const K1Out &out) {
+    uint32_t bq[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) bq[q] = __ballot_sync(0xffffffffu, (bits >> q) & 1u);
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        w[k] = h == 0 ? (bq[2 * k] & 0xFFFFu) | (bq[2 * k + 1] << 16) : (bq[2 * k] >> 16) | (bq[2 * k + 1] & 0xFFFF0000u);
+    if (has && l < 4 && (c << 2) + l < words32) {
+        const uint32_t mine_w = l == 0 ? w[0] : l == 1 ? w[1] : l == 2 ? w[2] : w[3];
+        for (int d = 0; d < out.n; ++d)
+            reinterpret_cast<uint32_t *>(out.sketch[d])[row * words32 + (c << 2) + l] = mine_w;
+    }
+}
+
+template <int L, bool PFX>
 __global__ void __launch_bounds__(K1H_THREADS, 1) k_sketch_s16(
     const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
     const int32_t *__restrict__ order, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
@@ -648,90 +810,10 @@ __global__ void __launch_bounds__(K1H_THREADS, 1) k_sketch_s16(
             }
             const int64_t len64 = end - beg;
             const int len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
-            // m1[r]: min of the (h15 << 1 | bit) keys of functions
-            // (l + 32r, l + 32r + 16) in the high / low halves; m1x[r]: min of
-            // the keys with the bit inverted.  Among the tokens of minimal
-            // h15, both bits occur iff m1 == m1x (both are (h15min, 0));
-            // otherwise they all carry m1's bit and any tie on h15 is harmless.
-            uint32_t m1[4], m1x[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) m1[r] = m1x[r] = 0xFFFFFFFFu;
-            for (int base = 0; base < len; base += 16) {
-                const int cnt = len - base < 16 ? len - base : 16;
-                const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
-                int j = 0;
-#pragma unroll 2
-                for (; j + 1 < cnt; j += 2) {
-                    const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
-                    const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
-                    const uint4 ha = key_oct<L>(ta, lane_base);
-                    const uint4 hb = key_oct<L>(tb, lane_base);
-                    const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w}, xb[4] = {hb.x, hb.y, hb.z, hb.w};
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        m1[r] = __vimin3_u16x2(m1[r], xa[r], xb[r]);
-                        m1x[r] = __vimin3_u16x2(m1x[r], xa[r] ^ 0x00010001u, xb[r] ^ 0x00010001u);
-                    }
-                }
-                if (j < cnt) {
-                    const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
-                    const uint4 ha = key_oct<L>(ta, lane_base);
-                    const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w};
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        m1[r] = vmin16x2(m1[r], xa[r]);
-                        m1x[r] = vmin16x2(m1x[r], xa[r] ^ 0x00010001u);
-                    }
-                }
-            }
-            // bits: q = 2j (high half) and 2j+1 (low half) of register j
-            uint32_t bits = 0;  // bit q = sketch bit of function l + 16q
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t a1 = m1[j] >> 16, ax = m1x[j] >> 16, b1 = m1[j] & 0xFFFFu, bx = m1x[j] & 0xFFFFu;
-                bits |= (a1 & 1u) << (2 * j);
-                bits |= (b1 & 1u) << (2 * j + 1);
-                const int fa = (c << 7) + l + 32 * j, fb = fa + 16;
-                const bool tie_a = len > 1 && fa < F && a1 == ax;
-                const bool tie_b = len > 1 && fb < F && b1 == bx;
-                unsigned tied = __ballot_sync(hmask, tie_a);
-                while (tied) {
-                    const int src = __ffs(tied) - 1;
-                    tied &= tied - 1;
-                    const int f = __shfl_sync(hmask, fa, src);
-                    const uint32_t m15 = __shfl_sync(hmask, a1 >> 1, src);
-                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
-                    const uint32_t tw = half_resolve15<L>(hi, lo, f, m15, col, 16, tokens, beg, len, l, hmask);
-                    if (lane == src) bits = (bits & ~(1u << (2 * j))) | (sketch_bit_g(bitmask, f, tw) << (2 * j));
-                }
-                tied = __ballot_sync(hmask, tie_b);
-                while (tied) {
-                    const int src = __ffs(tied) - 1;
-                    tied &= tied - 1;
-                    const int f = __shfl_sync(hmask, fb, src);
-                    const uint32_t m15 = __shfl_sync(hmask, b1 >> 1, src);
-                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
-                    const uint32_t tw = half_resolve15<L>(hi, lo, f, m15, col, 0, tokens, beg, len, l, hmask);
-                    if (lane == src)
-                        bits = (bits & ~(1u << (2 * j + 1))) | (sketch_bit_g(bitmask, f, tw) << (2 * j + 1));
-                }
-            }
-            if (len <= 0) bits = 0;
+            const uint32_t bits = sketch_chunk_bits<L, PFX>(tokens, beg, len, c, F, hi, lo, bitmask, smem0, lane_base,
+                                                            lane, l, hmask);
             __syncwarp();
-            uint32_t bq[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) bq[q] = __ballot_sync(0xffffffffu, (bits >> q) & 1u);
-            uint32_t w[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                w[k] = h == 0 ? (bq[2 * k] & 0xFFFFu) | (bq[2 * k + 1] << 16)
-                              : (bq[2 * k] >> 16) | (bq[2 * k + 1] & 0xFFFF0000u);
-            const int64_t row = out.row0 + s;
-            if (has && l < 4 && (c << 2) + l < words32) {
-                const uint32_t mine_w = l == 0 ? w[0] : l == 1 ? w[1] : l == 2 ? w[2] : w[3];
-                for (int d = 0; d < out.n; ++d)
-                    reinterpret_cast<uint32_t *>(out.sketch[d])[row * words32 + (c << 2) + l] = mine_w;
-            }
+            sketch_store_words(bits, h, l, has, c, words32, out.row0 + s, out);
         }
     }
     if (out.n > 1) __threadfence_system();
@@ -924,7 +1006,7 @@ __global__ void __launch_bounds__(K1H_THREADS, 1) k_values_h8(
 // sketch hint, and every pipelined chunk): job 0.. of the embedding family's
 // value chunks, then the sketch family's chunks, one length order and one
 // launch tail for both (k_values_h8 and k_sketch_s16 bodies).
-template <int L>
+template <int L, bool PFX>
 __global__ void __launch_bounds__(K1H_THREADS, 1) k_embed_h8(
     const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
     const int32_t *__restrict__ order, const uint32_t *__restrict__ ehi, const uint32_t *__restrict__ elo,
@@ -1072,90 +1154,10 @@ __global__ void __launch_bounds__(K1H_THREADS, 1) k_embed_h8(
             }
             const int64_t len64 = end - beg;
             const int len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
-            // m1[r]: min of the (h15 << 1 | bit) keys of functions
-            // (l + 32r, l + 32r + 16) in the high / low halves; m1x[r]: min of
-            // the keys with the bit inverted.  Among the tokens of minimal
-            // h15, both bits occur iff m1 == m1x (both are (h15min, 0));
-            // otherwise they all carry m1's bit and any tie on h15 is harmless.
-            uint32_t m1[4], m1x[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) m1[r] = m1x[r] = 0xFFFFFFFFu;
-            for (int base = 0; base < len; base += 16) {
-                const int cnt = len - base < 16 ? len - base : 16;
-                const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
-                int j = 0;
-#pragma unroll 2
-                for (; j + 1 < cnt; j += 2) {
-                    const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
-                    const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
-                    const uint4 ha = key_oct<L>(ta, lane_base);
-                    const uint4 hb = key_oct<L>(tb, lane_base);
-                    const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w}, xb[4] = {hb.x, hb.y, hb.z, hb.w};
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        m1[r] = __vimin3_u16x2(m1[r], xa[r], xb[r]);
-                        m1x[r] = __vimin3_u16x2(m1x[r], xa[r] ^ 0x00010001u, xb[r] ^ 0x00010001u);
-                    }
-                }
-                if (j < cnt) {
-                    const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
-                    const uint4 ha = key_oct<L>(ta, lane_base);
-                    const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w};
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        m1[r] = vmin16x2(m1[r], xa[r]);
-                        m1x[r] = vmin16x2(m1x[r], xa[r] ^ 0x00010001u);
-                    }
-                }
-            }
-            // bits: q = 2j (high half) and 2j+1 (low half) of register j
-            uint32_t bits = 0;  // bit q = sketch bit of function l + 16q
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t a1 = m1[j] >> 16, ax = m1x[j] >> 16, b1 = m1[j] & 0xFFFFu, bx = m1x[j] & 0xFFFFu;
-                bits |= (a1 & 1u) << (2 * j);
-                bits |= (b1 & 1u) << (2 * j + 1);
-                const int fa = (c << 7) + l + 32 * j, fb = fa + 16;
-                const bool tie_a = len > 1 && fa < F && a1 == ax;
-                const bool tie_b = len > 1 && fb < F && b1 == bx;
-                unsigned tied = __ballot_sync(hmask, tie_a);
-                while (tied) {
-                    const int src = __ffs(tied) - 1;
-                    tied &= tied - 1;
-                    const int f = __shfl_sync(hmask, fa, src);
-                    const uint32_t m15 = __shfl_sync(hmask, a1 >> 1, src);
-                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
-                    const uint32_t tw = half_resolve15<L>(hi, lo, f, m15, col, 16, tokens, beg, len, l, hmask);
-                    if (lane == src) bits = (bits & ~(1u << (2 * j))) | (sketch_bit_g(bitmask, f, tw) << (2 * j));
-                }
-                tied = __ballot_sync(hmask, tie_b);
-                while (tied) {
-                    const int src = __ffs(tied) - 1;
-                    tied &= tied - 1;
-                    const int f = __shfl_sync(hmask, fb, src);
-                    const uint32_t m15 = __shfl_sync(hmask, b1 >> 1, src);
-                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
-                    const uint32_t tw = half_resolve15<L>(hi, lo, f, m15, col, 0, tokens, beg, len, l, hmask);
-                    if (lane == src)
-                        bits = (bits & ~(1u << (2 * j + 1))) | (sketch_bit_g(bitmask, f, tw) << (2 * j + 1));
-                }
-            }
-            if (len <= 0) bits = 0;
+            const uint32_t bits = sketch_chunk_bits<L, PFX>(tokens, beg, len, c, F, hi, lo, bitmask, smem0, lane_base,
+                                                            lane, l, hmask);
             __syncwarp();
-            uint32_t bq[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) bq[q] = __ballot_sync(0xffffffffu, (bits >> q) & 1u);
-            uint32_t w[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                w[k] = h == 0 ? (bq[2 * k] & 0xFFFFu) | (bq[2 * k + 1] << 16)
-                              : (bq[2 * k] >> 16) | (bq[2 * k + 1] & 0xFFFF0000u);
-            const int64_t row = out.row0 + s;
-            if (has && l < 4 && (c << 2) + l < words32) {
-                const uint32_t mine_w = l == 0 ? w[0] : l == 1 ? w[1] : l == 2 ? w[2] : w[3];
-                for (int d = 0; d < out.n; ++d)
-                    reinterpret_cast<uint32_t *>(out.sketch[d])[row * words32 + (c << 2) + l] = mine_w;
-            }
+            sketch_store_words(bits, h, l, has, c, words32, out.row0 + s, out);
         }
         }
     }
@@ -1242,17 +1244,25 @@ static DevBuf<int32_t> length_order(cpsj_ctx *ctx, const int64_t *off, int64_t n
     return order;
 }
 
+// A/B switch: CPSJ_K1_NO_PFX=1 looks every key byte up for every token
+static bool k1_prefix_cache() {
+    const char *e = getenv("CPSJ_K1_NO_PFX");
+    return !(e && e[0] == '1');
+}
+
 template <int L>
 static void launch_embed_h8(cpsj_ctx *ctx, const cpsj_family *efam, const cpsj_family *sfam, const uint32_t *tok,
                             const int64_t *off, int64_t n, const K1Out &vout, const K1Out &sout,
                             cudaStream_t stream) {
     const int smem = L * 256 * 16 * 16 + 16;
-    CPSJ_CUDA(cudaFuncSetAttribute(k_embed_h8<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const bool pfx = k1_prefix_cache();
+    auto kern = pfx ? k_embed_h8<L, true> : k_embed_h8<L, false>;
+    CPSJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     ProfScope prof(ctx, PROF_K1, stream);
     DevBuf<int32_t> order = length_order(ctx, off, n, stream);
     const int64_t want = ((n + 1) / 2 + K1H_WARPS - 1) / K1H_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
-    k_embed_h8<L><<<grid, K1H_THREADS, smem, stream>>>(
+    kern<<<grid, K1H_THREADS, smem, stream>>>(
         tok, off, n, order.p, efam->d_hi, efam->d_lo, reinterpret_cast<const uint4 *>(efam->d_vimg[L - 1]), efam->F,
         sfam->d_hi, sfam->d_lo, sfam->d_bitmask, reinterpret_cast<const uint4 *>(sfam->d_simg[L - 1]), sfam->F, vout,
         sout);
@@ -1280,15 +1290,15 @@ template <int L>
 static void launch_sketch_s16(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
                               int64_t n, const K1Out &out, cudaStream_t stream) {
     const int smem = L * 256 * 16 * 16 + 16;
-    CPSJ_CUDA(cudaFuncSetAttribute(k_sketch_s16<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const bool pfx = k1_prefix_cache();
+    auto kern = pfx ? k_sketch_s16<L, true> : k_sketch_s16<L, false>;
+    CPSJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     ProfScope prof(ctx, PROF_K1, stream);
     DevBuf<int32_t> order = length_order(ctx, off, n, stream);
     const int64_t want = ((n + 1) / 2 + K1H_WARPS - 1) / K1H_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
-    k_sketch_s16<L><<<grid, K1H_THREADS, smem, stream>>>(tok, off, n, order.p, fam->d_hi, fam->d_lo,
-                                                         fam->d_bitmask,
-                                                         reinterpret_cast<const uint4 *>(fam->d_simg[L - 1]), fam->F,
-                                                         out);
+    kern<<<grid, K1H_THREADS, smem, stream>>>(tok, off, n, order.p, fam->d_hi, fam->d_lo, fam->d_bitmask,
+                                              reinterpret_cast<const uint4 *>(fam->d_simg[L - 1]), fam->F, out);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
 }
