@@ -1102,8 +1102,14 @@ __global__ void k_gather8(Gather8 g, int cnt, int64_t *__restrict__ out) {
 constexpr int ST_THREADS = 512;
 constexpr int ST_WARPS = ST_THREADS / 32;
 constexpr int ST_MAX_SEL = 256;  // selected positions of one node (t <= 256)
-constexpr int ST_MAX_SUBM = 8192;  // largest node a CTA holds
-constexpr int64_t DEFER_LEVEL_MEMBERS = 1 << 20;  // levels this small defer their nodes to K7
+#ifndef CPSJ_ST_MAX_SUBM
+#define CPSJ_ST_MAX_SUBM 8192
+#endif
+#ifndef CPSJ_DEFER_LEVEL_MEMBERS
+#define CPSJ_DEFER_LEVEL_MEMBERS (1 << 20)
+#endif
+constexpr int ST_MAX_SUBM = CPSJ_ST_MAX_SUBM;  // largest node a CTA holds
+constexpr int64_t DEFER_LEVEL_MEMBERS = CPSJ_DEFER_LEVEL_MEMBERS;  // levels this small defer their nodes to K7
 
 struct StNode {
     int64_t S;

@@ -489,6 +489,23 @@ __device__ __forceinline__ uint4 key_oct(uint32_t tok, uint32_t lane_base) {
 
 constexpr int K1H_WARPS = 24;
 constexpr int K1H_THREADS = K1H_WARPS * 32;
+// the sketch-only kernel fits 64 registers: a full 1024-thread CTA (more
+// warps to cover the shared-memory and shuffle latencies)
+#ifndef K1S_WARPS
+#define K1S_WARPS 32
+#endif
+constexpr int K1S_THREADS = K1S_WARPS * 32;
+// sketch_chunk_bits: a 16-token batch (both halves of the warp, 32 slots)
+// uses the cached upper entries when at most this many of its tokens change
+// key byte 1
+#ifndef K1_PFX_MAX_RELOADS
+#define K1_PFX_MAX_RELOADS 22
+#endif
+// ... and a warp stops testing for the rest of a chunk after this many
+// consecutive batches declined (uniform tokens: no test overhead)
+#ifndef K1_PFX_GIVE_UP
+#define K1_PFX_GIVE_UP 16
+#endif
 
 // ---------------------------------------------------------------------
 // Sketch-only kernel (the production sketch path for L <= 3).  A sketch
@@ -635,89 +652,95 @@ template <int L, bool PFX>
 __device__ __forceinline__ uint32_t sketch_chunk_bits(
     const uint32_t *__restrict__ tokens, int64_t beg, int len, int c, int F, const uint32_t *__restrict__ hi,
     const uint32_t *__restrict__ lo, const uint32_t *__restrict__ bitmask, uint32_t smem0, uint32_t lane_base,
-    int lane, int l, unsigned hmask) {
+    int lane, int l, unsigned hmask, uint32_t mine0, int &misses) {
     uint32_t mU[4], mS[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         mU[r] = 0xFFFFFFFFu;
         mS[r] = 0x7FFF7FFFu;
     }
-    if (PFX && L > 1) {
-        uint32_t P[4] = {0u, 0u, 0u, 0u}, P2[4] = {0u, 0u, 0u, 0u};
-        uint32_t cur = 0xFFFFFFFFu;  // tok >> 8 of the cached upper entries
-        auto refresh = [&](uint32_t tok) {
-            const uint32_t pre = tok >> 8;
-            if (pre != cur) {
-                if (L > 2 && ((pre ^ cur) >> 8) != 0u) {
-                    const uint4 v = lds128(lane_base + 131072u + __byte_perm(tok, 0u, 0x4424));
-                    P2[0] = v.x; P2[1] = v.y; P2[2] = v.z; P2[3] = v.w;
-                }
-                const uint4 v = lds128(lane_base + 65536u + (tok & 0xFF00u));
-                P[0] = v.x ^ P2[0]; P[1] = v.y ^ P2[1]; P[2] = v.z ^ P2[2]; P[3] = v.w ^ P2[3];
-                cur = pre;
+    // Warp-uniform trip count: both halves run max(len) token slots and a
+    // slot past a set's end re-reads its last token (min is idempotent), so
+    // every shuffle is a full-mask one with an immediate lane, the batch has
+    // no remainder code and the groups of four below are straight-line.
+    const int lenw = max(len, __shfl_xor_sync(0xffffffffu, len, 16));
+    const int lim = len > 0 ? len - 1 : 0;
+    uint32_t P[4] = {0u, 0u, 0u, 0u}, P2[4] = {0u, 0u, 0u, 0u};
+    uint32_t prev_last = 0xFFFFFFFFu;  // token before the batch (none: forces the first reload)
+    uint32_t mine = mine0;             // this lane's token of the batch (the caller loaded batch 0)
+    for (int base = 0; base < lenw; base += 16) {
+        // the next batch's tokens are requested before this batch is hashed
+        uint32_t mine_next = 0u;
+        if (base + 16 < lenw && len > 0) mine_next = __ldg(tokens + beg + min(base + 16 + l, lim));
+        unsigned c1 = 0u, c2 = 0u;  // bit j: token j of the batch changes key byte 1 / byte 2
+        bool cached = false;        // warp-uniform: this batch runs on the cached upper entries
+        if (PFX && L > 1 && misses < K1_PFX_GIVE_UP) {
+            uint32_t pred = __shfl_up_sync(0xffffffffu, mine, 1, 16);
+            if (l == 0) pred = prev_last;
+            const uint32_t x = mine ^ pred;
+            const unsigned b1 = __ballot_sync(0xffffffffu, x > 0xFFu);
+            // a batch whose tokens mostly change byte 1 (uniform tokens over a
+            // large universe) is cheaper with all L lookups and no branches
+            cached = __popc(b1) <= K1_PFX_MAX_RELOADS;
+            if (cached) {
+                c1 = b1 >> (lane & 16);
+                if (L > 2) c2 = __ballot_sync(0xffffffffu, x > 0xFFFFu) >> (lane & 16);
+                prev_last = __shfl_sync(0xffffffffu, mine, 15, 16);
+                misses = 0;
+            } else {
+                prev_last = 0xFFFFFFFFu;  // the cache is stale after this batch
+                ++misses;
             }
-        };
-        for (int base = 0; base < len; base += 16) {
-            const int cnt = len - base < 16 ? len - base : 16;
-            const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
-            int j = 0;
-#pragma unroll 2
-            for (; j + 1 < cnt; j += 2) {
-                const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
-                const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
-                const uint4 ea = lds128(lane_base + __byte_perm(ta, 0u, 0x4404));
-                const uint4 eb = lds128(lane_base + __byte_perm(tb, 0u, 0x4404));
-                refresh(ta);
-                const uint32_t ka[4] = {ea.x ^ P[0], ea.y ^ P[1], ea.z ^ P[2], ea.w ^ P[3]};
-                refresh(tb);
-                const uint32_t kb[4] = {eb.x ^ P[0], eb.y ^ P[1], eb.z ^ P[2], eb.w ^ P[3]};
+        }
+        const int cntw = lenw - base;  // warp-uniform; slots >= cntw rounded up to 4 are skipped
+        if (cached) {
+#pragma unroll 1
+            for (int g = 0; g < 4 && 4 * g < cntw; ++g) {
+                const unsigned c1g = c1 >> (4 * g), c2g = c2 >> (4 * g);
+                const uint32_t lane_g = (uint32_t)(4 * g);
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    mU[r] = __vimin3_u16x2(mU[r], ka[r], kb[r]);
-                    mS[r] = __vimin3_s16x2(mS[r], ka[r], kb[r]);
+                for (int pr2 = 0; pr2 < 2; ++pr2) {
+                    uint32_t k[2][4];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int jj = 2 * pr2 + u;
+                        const uint32_t tk = __shfl_sync(0xffffffffu, mine, lane_g + jj, 16);
+                        const uint4 e = lds128(lane_base + __byte_perm(tk, 0u, 0x4404));
+                        if ((c1g >> jj) & 1u) {
+                            if (L > 2 && ((c2g >> jj) & 1u)) {
+                                const uint4 v2 = lds128(lane_base + 131072u + __byte_perm(tk, 0u, 0x4424));
+                                P2[0] = v2.x; P2[1] = v2.y; P2[2] = v2.z; P2[3] = v2.w;
+                            }
+                            const uint4 v = lds128(lane_base + 65536u + (tk & 0xFF00u));
+                            P[0] = v.x ^ P2[0]; P[1] = v.y ^ P2[1]; P[2] = v.z ^ P2[2]; P[3] = v.w ^ P2[3];
+                        }
+                        k[u][0] = e.x ^ P[0]; k[u][1] = e.y ^ P[1]; k[u][2] = e.z ^ P[2]; k[u][3] = e.w ^ P[3];
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        mU[r] = __vimin3_u16x2(mU[r], k[0][r], k[1][r]);
+                        mS[r] = __vimin3_s16x2(mS[r], k[0][r], k[1][r]);
+                    }
                 }
             }
-            if (j < cnt) {
-                const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
-                const uint4 ea = lds128(lane_base + __byte_perm(ta, 0u, 0x4404));
-                refresh(ta);
-                const uint32_t ka[4] = {ea.x ^ P[0], ea.y ^ P[1], ea.z ^ P[2], ea.w ^ P[3]};
+        } else {
+#pragma unroll 1
+            for (int g = 0; g < 4 && 4 * g < cntw; ++g) {
+                const uint32_t lane_g = (uint32_t)(4 * g);
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    mU[r] = vmin16x2(mU[r], ka[r]);
-                    mS[r] = vmin16x2s(mS[r], ka[r]);
+                for (int pr2 = 0; pr2 < 2; ++pr2) {
+                    const uint4 ea = key_oct<L>(__shfl_sync(0xffffffffu, mine, lane_g + 2 * pr2, 16), lane_base);
+                    const uint4 eb = key_oct<L>(__shfl_sync(0xffffffffu, mine, lane_g + 2 * pr2 + 1, 16), lane_base);
+                    const uint32_t ka[4] = {ea.x, ea.y, ea.z, ea.w}, kb[4] = {eb.x, eb.y, eb.z, eb.w};
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        mU[r] = __vimin3_u16x2(mU[r], ka[r], kb[r]);
+                        mS[r] = __vimin3_s16x2(mS[r], ka[r], kb[r]);
+                    }
                 }
             }
         }
-    } else {
-        for (int base = 0; base < len; base += 16) {
-            const int cnt = len - base < 16 ? len - base : 16;
-            const uint32_t mine = l < cnt ? __ldg(tokens + beg + base + l) : 0u;
-            int j = 0;
-#pragma unroll 2
-            for (; j + 1 < cnt; j += 2) {
-                const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
-                const uint32_t tb = __shfl_sync(hmask, mine, j + 1, 16);
-                const uint4 ha = key_oct<L>(ta, lane_base);
-                const uint4 hb = key_oct<L>(tb, lane_base);
-                const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w}, xb[4] = {hb.x, hb.y, hb.z, hb.w};
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    mU[r] = __vimin3_u16x2(mU[r], xa[r], xb[r]);
-                    mS[r] = __vimin3_s16x2(mS[r], xa[r], xb[r]);
-                }
-            }
-            if (j < cnt) {
-                const uint32_t ta = __shfl_sync(hmask, mine, j, 16);
-                const uint4 ha = key_oct<L>(ta, lane_base);
-                const uint32_t xa[4] = {ha.x, ha.y, ha.z, ha.w};
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    mU[r] = vmin16x2(mU[r], xa[r]);
-                    mS[r] = vmin16x2s(mS[r], xa[r]);
-                }
-            }
-        }
+        mine = mine_next;
     }
     // register j: function l + 32j in the high half (bit 2j), l + 32j + 16 in
     // the low half (bit 2j + 1)
@@ -767,22 +790,73 @@ __device__ __forceinline__ void sketch_store_words(uint32_t bits, int h, int l, 
     }
 }
 
+// one set of a half-warp: CSR row, clamped length; `has` = the slot is a set
+struct K1Set {
+    int64_t s, beg;
+    int len;
+    bool has;
+};
+__device__ __forceinline__ K1Set k1_load_set(const int64_t *__restrict__ offsets, const int32_t *__restrict__ order,
+                                             int64_t n, int64_t idx) {
+    K1Set d{0, 0, 0, idx < n};
+    if (d.has) {
+        d.s = order != nullptr ? (int64_t)__ldg(order + idx) : idx;
+        const int64_t end = __ldg(offsets + d.s + 1);
+        d.beg = __ldg(offsets + d.s);
+        const int64_t len64 = end - d.beg;
+        d.len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
+    }
+    return d;
+}
+__device__ __forceinline__ uint32_t k1_first_tokens(const uint32_t *__restrict__ tokens, const K1Set &d, int l) {
+    return d.len > 0 ? __ldg(tokens + d.beg + min(l, d.len - 1)) : 0u;
+}
+
+// the sets of this warp for one 128-function sketch chunk (tables resident in
+// shared memory).  The next set's CSR row and first tokens are requested
+// while the current set is hashed, so no global-load latency is exposed
+// between sets.
 template <int L, bool PFX>
-__global__ void __launch_bounds__(K1H_THREADS, 1) k_sketch_s16(
+__device__ __forceinline__ void sketch_chunk_sets(
+    const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
+    const int32_t *__restrict__ order, int c, int F, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
+    const uint32_t *__restrict__ bitmask, uint32_t smem0, uint32_t lane_base, int lane, int64_t p_first,
+    int64_t p_step, const K1Out &out) {
+    const int h = lane >> 4, l = lane & 15;
+    const unsigned hmask = 0xFFFFu << (16 * h);
+    const int words32 = F >> 5;
+    const int64_t npairs = (n + 1) >> 1;
+    if (p_first >= npairs) return;
+    K1Set cur = k1_load_set(offsets, order, n, 2 * p_first + h);
+    uint32_t mine0 = k1_first_tokens(tokens, cur, l);
+    K1Set nxt = k1_load_set(offsets, order, n, p_first + p_step < npairs ? 2 * (p_first + p_step) + h : n);
+    int misses = 0;  // consecutive batches that declined the cached entries (sketch_chunk_bits)
+    for (int64_t pr = p_first; pr < npairs; pr += p_step) {
+        const uint32_t bits = sketch_chunk_bits<L, PFX>(tokens, cur.beg, cur.len, c, F, hi, lo, bitmask, smem0,
+                                                        lane_base, lane, l, hmask, mine0, misses);
+        // the next set's row has arrived by now: request its first tokens
+        // and the row after it, then finish this set
+        mine0 = k1_first_tokens(tokens, nxt, l);
+        const K1Set nn = k1_load_set(offsets, order, n, pr + 2 * p_step < npairs ? 2 * (pr + 2 * p_step) + h : n);
+        __syncwarp();
+        sketch_store_words(bits, h, l, cur.has, c, words32, out.row0 + cur.s, out);
+        cur = nxt;
+        nxt = nn;
+    }
+}
+
+template <int L, bool PFX>
+__global__ void __launch_bounds__(K1S_THREADS, 1) k_sketch_s16(
     const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
     const int32_t *__restrict__ order, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
     const uint32_t *__restrict__ bitmask, const uint4 *__restrict__ simg, int F, const K1Out out) {
     extern __shared__ __align__(128) uint4 tab4[];  // [L][256][16] x uint4, then the mbarrier
     uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + L * 256 * 16);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int h = lane >> 4, l = lane & 15;
-    const unsigned hmask = 0xFFFFu << (16 * h);
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tab4);
-    const uint32_t lane_base = smem0 + ((uint32_t)l << 4);
+    const uint32_t lane_base = smem0 + ((uint32_t)(lane & 15) << 4);
     const int nchunks = (F + 127) >> 7;
-    const int words32 = F >> 5;
-    const int64_t npairs = (n + 1) >> 1;
-    const int64_t p_first = (int64_t)blockIdx.x * K1H_WARPS + warp, p_step = (int64_t)gridDim.x * K1H_WARPS;
+    const int64_t p_first = (int64_t)blockIdx.x * K1S_WARPS + warp, p_step = (int64_t)gridDim.x * K1S_WARPS;
     const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(mbar);
     if (threadIdx.x == 0) mbar_init(mbar_a, 1);
     __syncthreads();
@@ -799,22 +873,8 @@ __global__ void __launch_bounds__(K1H_THREADS, 1) k_sketch_s16(
         }
         mbar_wait(mbar_a, phase);
         phase ^= 1u;
-        for (int64_t pr = p_first; pr < npairs; pr += p_step) {
-            const int64_t idx = 2 * pr + h;
-            const bool has = idx < n;
-            int64_t s = 0, beg = 0, end = 0;
-            if (has) {
-                s = order != nullptr ? (int64_t)order[idx] : idx;
-                beg = offsets[s];
-                end = offsets[s + 1];
-            }
-            const int64_t len64 = end - beg;
-            const int len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
-            const uint32_t bits = sketch_chunk_bits<L, PFX>(tokens, beg, len, c, F, hi, lo, bitmask, smem0, lane_base,
-                                                            lane, l, hmask);
-            __syncwarp();
-            sketch_store_words(bits, h, l, has, c, words32, out.row0 + s, out);
-        }
+        sketch_chunk_sets<L, PFX>(tokens, offsets, n, order, c, F, hi, lo, bitmask, smem0, lane_base, lane, p_first,
+                                  p_step, out);
     }
     if (out.n > 1) __threadfence_system();
 }
@@ -1141,24 +1201,9 @@ __global__ void __launch_bounds__(K1H_THREADS, 1) k_embed_h8(
         } else {
             const uint32_t *hi = shi, *lo = slo;
             const int F = FS;
-            const int words32 = FS >> 5;
             const K1Out &out = sout;
-        for (int64_t pr = p_first; pr < npairs; pr += p_step) {
-            const int64_t idx = 2 * pr + h;
-            const bool has = idx < n;
-            int64_t s = 0, beg = 0, end = 0;
-            if (has) {
-                s = order != nullptr ? (int64_t)order[idx] : idx;
-                beg = offsets[s];
-                end = offsets[s + 1];
-            }
-            const int64_t len64 = end - beg;
-            const int len = len64 < 0x7FFFFFFF ? (int)len64 : 0x7FFFFFFF;
-            const uint32_t bits = sketch_chunk_bits<L, PFX>(tokens, beg, len, c, F, hi, lo, bitmask, smem0, lane_base,
-                                                            lane, l, hmask);
-            __syncwarp();
-            sketch_store_words(bits, h, l, has, c, words32, out.row0 + s, out);
-        }
+        sketch_chunk_sets<L, PFX>(tokens, offsets, n, order, c, F, hi, lo, bitmask, smem0, lane_base, lane, p_first,
+                                  p_step, out);
         }
     }
     if (vout.n > 1) __threadfence_system();
@@ -1272,14 +1317,18 @@ static void launch_embed_h8(cpsj_ctx *ctx, const cpsj_family *efam, const cpsj_f
 
 template <int L>
 static void launch_values_h8(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
-                             int64_t n, const K1Out &out, cudaStream_t stream) {
+                             int64_t n, const K1Out &out, cudaStream_t stream, const int32_t *order = nullptr) {
     const int smem = L * 256 * 16 * 16 + 16;
     CPSJ_CUDA(cudaFuncSetAttribute(k_values_h8<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     ProfScope prof(ctx, PROF_K1, stream);
-    DevBuf<int32_t> order = length_order(ctx, off, n, stream);
+    DevBuf<int32_t> own;
+    if (order == nullptr) {
+        own = length_order(ctx, off, n, stream);
+        order = own.p;
+    }
     const int64_t want = ((n + 1) / 2 + K1H_WARPS - 1) / K1H_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
-    k_values_h8<L><<<grid, K1H_THREADS, smem, stream>>>(tok, off, n, order.p, fam->d_hi, fam->d_lo,
+    k_values_h8<L><<<grid, K1H_THREADS, smem, stream>>>(tok, off, n, order, fam->d_hi, fam->d_lo,
                                                         reinterpret_cast<const uint4 *>(fam->d_vimg[L - 1]), fam->F,
                                                         out);
     CPSJ_LAUNCH_CHECK();
@@ -1288,16 +1337,20 @@ static void launch_values_h8(cpsj_ctx *ctx, const cpsj_family *fam, const uint32
 
 template <int L>
 static void launch_sketch_s16(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
-                              int64_t n, const K1Out &out, cudaStream_t stream) {
+                              int64_t n, const K1Out &out, cudaStream_t stream, const int32_t *order = nullptr) {
     const int smem = L * 256 * 16 * 16 + 16;
     const bool pfx = k1_prefix_cache();
     auto kern = pfx ? k_sketch_s16<L, true> : k_sketch_s16<L, false>;
     CPSJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     ProfScope prof(ctx, PROF_K1, stream);
-    DevBuf<int32_t> order = length_order(ctx, off, n, stream);
-    const int64_t want = ((n + 1) / 2 + K1H_WARPS - 1) / K1H_WARPS;
+    DevBuf<int32_t> own;
+    if (order == nullptr) {
+        own = length_order(ctx, off, n, stream);
+        order = own.p;
+    }
+    const int64_t want = ((n + 1) / 2 + K1S_WARPS - 1) / K1S_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
-    kern<<<grid, K1H_THREADS, smem, stream>>>(tok, off, n, order.p, fam->d_hi, fam->d_lo, fam->d_bitmask,
+    kern<<<grid, K1S_THREADS, smem, stream>>>(tok, off, n, order, fam->d_hi, fam->d_lo, fam->d_bitmask,
                                               reinterpret_cast<const uint4 *>(fam->d_simg[L - 1]), fam->F, out);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
@@ -1420,13 +1473,35 @@ void minhash_embed(cpsj_ctx *ctx, const cpsj_family *efam, const cpsj_family *sf
     sout.n = 1;
     if (n == 0) return;
     const int L = max_token < (1u << 8) ? 1 : max_token < (1u << 16) ? 2 : max_token < (1u << 24) ? 3 : 4;
-    const char *nf = getenv("CPSJ_K1_NO_FUSE");  // A/B switch: two launches
+    // Both outputs by the half-warp kernels: one length order, then the
+    // values launch (24 warps, 80 registers) and the sketch launch (32
+    // warps, 64 registers).  CPSJ_K1_FUSE=1 (A/B) runs both in the single
+    // 24-warp launch k_embed_h8 instead.
+    const char *fu = getenv("CPSJ_K1_FUSE");
     if (L < 4 && efam->d_vimg[L - 1] != nullptr && sfam->d_simg[L - 1] != nullptr && d_values != nullptr &&
-        d_sketch != nullptr && !(nf && nf[0] == '1') && !getenv("CPSJ_K1_NO_H8") && !getenv("CPSJ_K1_NO_S16")) {
+        d_sketch != nullptr && !getenv("CPSJ_K1_NO_H8") && !getenv("CPSJ_K1_NO_S16")) {
+        if (fu != nullptr && fu[0] == '1') {
+            switch (L) {
+                case 1: launch_embed_h8<1>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
+                case 2: launch_embed_h8<2>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
+                default: launch_embed_h8<3>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
+            }
+            return;
+        }
+        DevBuf<int32_t> order = length_order(ctx, d_offsets, n, stream);
         switch (L) {
-            case 1: launch_embed_h8<1>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
-            case 2: launch_embed_h8<2>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
-            default: launch_embed_h8<3>(ctx, efam, sfam, d_tokens, d_offsets, n, vout, sout, stream); break;
+            case 1:
+                launch_values_h8<1>(ctx, efam, d_tokens, d_offsets, n, vout, stream, order.p);
+                launch_sketch_s16<1>(ctx, sfam, d_tokens, d_offsets, n, sout, stream, order.p);
+                break;
+            case 2:
+                launch_values_h8<2>(ctx, efam, d_tokens, d_offsets, n, vout, stream, order.p);
+                launch_sketch_s16<2>(ctx, sfam, d_tokens, d_offsets, n, sout, stream, order.p);
+                break;
+            default:
+                launch_values_h8<3>(ctx, efam, d_tokens, d_offsets, n, vout, stream, order.p);
+                launch_sketch_s16<3>(ctx, sfam, d_tokens, d_offsets, n, sout, stream, order.p);
+                break;
         }
         return;
     }
