@@ -50,6 +50,7 @@ struct DLevel {
     long long n_seg, E;     // split segments, split entries
     long long Nn, Mn;       // children (the next level's N, M)
     int key_bits, npass;    // split sort: significant key bits, passes run
+    int k32, pad0;          // split keys stored as u32 (they fit 32 bits: half the sort traffic)
     int defer_max, live;    // K7 deferral bound; 0 once the level is empty / aborted
     // node arrays
     int64_t *off;
@@ -74,6 +75,15 @@ struct DLevel {
 
 // the level's pointer / size fields by byte offset (kernels generic over
 // which array of the descriptor they scan)
+// split keys are u32 when (segment, value) fits 32 bits (DLevel::k32), else u64
+__device__ __forceinline__ uint64_t ld_key(const uint64_t *keys, int k32, int64_t i) {
+    return k32 ? (uint64_t) reinterpret_cast<const uint32_t *>(keys)[i] : keys[i];
+}
+__device__ __forceinline__ void st_key(uint64_t *keys, int k32, int64_t i, uint64_t v) {
+    if (k32) reinterpret_cast<uint32_t *>(keys)[i] = (uint32_t)v;
+    else keys[i] = v;
+}
+
 #define DL_OFF(f) ((int)offsetof(DLevel, f))
 template <typename T>
 __device__ __forceinline__ T *dptr(const DLevel *L, int off) {
@@ -116,7 +126,10 @@ __device__ __forceinline__ void dscan_load(const DScan &a, int64_t n, int64_t ba
             const uint64_t *keys = (L->npass & 1) ? L->keys2 : L->keys;
             const int64_t E = L->E;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) group_marks(keys, E, base + j, v[0][j], v[1][j]);
+            for (int j = 0; j < 4; ++j) {
+                if (L->k32) group_marks(reinterpret_cast<const uint32_t *>(keys), E, base + j, v[0][j], v[1][j]);
+                else group_marks(keys, E, base + j, v[0][j], v[1][j]);
+            }
             return;
         }
     }
@@ -248,6 +261,7 @@ __device__ void alloc_split(DArena *ar, DLevel *L, int vbits, unsigned long long
     int kb = vbits;
     while (kb < 64 && ((unsigned long long)n_seg >> (kb - vbits)) > 0) ++kb;
     L->key_bits = kb;
+    L->k32 = kb <= 32 ? 1 : 0;
     L->npass = E > 1 ? (kb + 7) / 8 : 0;
     L->keys = (uint64_t *)dalloc(ar, (E + 1) * 8);
     L->keys2 = (uint64_t *)dalloc(ar, (E + 1) * 8);
@@ -483,8 +497,10 @@ struct DRoots {
     int32_t *depth;
     int64_t cap;
 };
-__global__ void k_dle_defer(DLevel *L, int32_t limit, int32_t depth, const int32_t *arena_base, DRoots r,
+__global__ void k_dle_defer(DLevel *Lg, int32_t limit, int32_t depth, const int32_t *arena_base, DRoots r,
                             DevCounters *ctr, DArena *ar) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live || L->defer_max == 0) return;
     const int64_t N = L->N;
     DLE_FOR(i, N) {
@@ -503,7 +519,9 @@ __global__ void k_dle_defer(DLevel *L, int32_t limit, int32_t depth, const int32
     }
 }
 
-__global__ void k_dle_compact_internal(DLevel *L) {
+__global__ void k_dle_compact_internal(DLevel *Lg) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     const int64_t N = L->N;
     DLE_FOR(i, N + 1) {
@@ -516,7 +534,9 @@ __global__ void k_dle_compact_internal(DLevel *L) {
     }
 }
 
-__global__ void k_dle_node_sketch(DLevel *L, const uint64_t *__restrict__ sketch, int ell, int t, DevCounters *ctr) {
+__global__ void k_dle_node_sketch(DLevel *Lg, const uint64_t *__restrict__ sketch, int ell, int t, DevCounters *ctr) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     const int64_t n_int = L->n_int;
     const int mbits = 64 * ell;
@@ -542,7 +562,9 @@ __global__ void k_dle_node_sketch(DLevel *L, const uint64_t *__restrict__ sketch
     }
 }
 
-__global__ void k_dle_flags(DLevel *L, const uint64_t *__restrict__ sketch, int ell, int32_t flag_dist) {
+__global__ void k_dle_flags(DLevel *Lg, const uint64_t *__restrict__ sketch, int ell, int32_t flag_dist) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     const int64_t Mi = L->Mi, n_int = L->n_int;
     DLE_FOR_WARPS(base, Mi + 1) {
@@ -561,7 +583,9 @@ __global__ void k_dle_flags(DLevel *L, const uint64_t *__restrict__ sketch, int 
     }
 }
 
-__global__ void k_dle_survivors(DLevel *L) {
+__global__ void k_dle_survivors(DLevel *Lg) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     const int64_t Mi = L->Mi, n_int = L->n_int;
     DLE_FOR_WARPS(base, Mi) {
@@ -574,7 +598,9 @@ __global__ void k_dle_survivors(DLevel *L) {
     }
 }
 
-__global__ void k_dle_flag_list(DLevel *L) {
+__global__ void k_dle_flag_list(DLevel *Lg) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     const int64_t Mi = L->Mi;
     if (L->fscan[Mi] == 0) return;
@@ -582,9 +608,11 @@ __global__ void k_dle_flag_list(DLevel *L) {
 }
 
 // warp per flagged member (k_point's body)
-__global__ void k_dle_point(DLevel *L, const uint64_t *__restrict__ sketch, int ell, const int32_t *__restrict__ sizes,
+__global__ void k_dle_point(DLevel *Lg, const uint64_t *__restrict__ sketch, int ell, const int32_t *__restrict__ sizes,
                             const int8_t *__restrict__ side, int32_t accept, double lam, int2 *__restrict__ cand,
                             unsigned long long cap, DevCounters *ctr) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     const int64_t Mi = L->Mi, n_int = L->n_int;
     const int64_t n_flag = L->fscan[Mi];
@@ -624,8 +652,10 @@ __global__ void k_dle_point(DLevel *L, const uint64_t *__restrict__ sketch, int 
 }
 
 // warp per internal node (+ the sentinel): k_select's body
-__global__ void k_dle_select(DLevel *L, int32_t depth, int32_t depth_cap, int t, double split_p,
+__global__ void k_dle_select(DLevel *Lg, int32_t depth, int32_t depth_cap, int t, double split_p,
                              int64_t *__restrict__ cap_sizes, int64_t cap_cap, DevCounters *ctr, DArena *ar) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     const int64_t n_int = L->n_int;
     const int lane = threadIdx.x & 31;
@@ -665,7 +695,9 @@ __global__ void k_dle_select(DLevel *L, int32_t depth, int32_t depth_cap, int t,
     }
 }
 
-__global__ void k_dle_build_keys(DLevel *L, int t, const uint32_t *__restrict__ values, int vbits, int *verr) {
+__global__ void k_dle_build_keys(DLevel *Lg, int t, const uint32_t *__restrict__ values, int vbits, int *verr) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     const int64_t E = L->E, n_int = L->n_int;
     DLE_FOR_WARPS(base, E) {
@@ -677,7 +709,8 @@ __global__ void k_dle_build_keys(DLevel *L, int t, const uint32_t *__restrict__ 
         const int64_t r = local / s, p = local - r * s;
         const int pos = L->sel_pos[k * t + r];
         const int32_t x = L->surv[(L->im_off_c[k] - L->fscan[L->im_off_c[k]]) + p];
-        L->keys[e] = ((uint64_t)(L->seg_off[k] + r) << vbits) | checked_value(values[(size_t)x * t + pos], vbits, verr);
+        st_key(L->keys, L->k32, e,
+               ((uint64_t)(L->seg_off[k] + r) << vbits) | checked_value(values[(size_t)x * t + pos], vbits, verr));
         L->vals[e] = x;
     }
 }
@@ -686,7 +719,9 @@ __global__ void k_dle_build_keys(DLevel *L, int t, const uint32_t *__restrict__ 
 
 // pass p of the split sort (keys/vals <-> keys2/vals2 by p's parity); a
 // pass at or beyond npass is a no-op, so the host enqueues the worst case
-__global__ void __launch_bounds__(RS_THREADS) k_dle_rs_hist(DLevel *L, int p) {
+__global__ void __launch_bounds__(RS_THREADS) k_dle_rs_hist(DLevel *Lg, int p) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     __shared__ uint32_t h[256];
     if (!L->live || p >= L->npass) return;
     const int64_t n = L->E;
@@ -701,7 +736,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_dle_rs_hist(DLevel *L, int p) {
         for (int r = 0; r < RS_ROUNDS; ++r) {
             const int64_t i = rs_item(tile, w, r, lane);
             const bool valid = i < n;
-            const int d = valid ? (int)((keys[i] >> shift) & 255u) : 256 + lane;
+            const int d = valid ? (int)((ld_key(keys, L->k32, i) >> shift) & 255u) : 256 + lane;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             if (valid && (peers & ((1u << lane) - 1)) == 0) atomicAdd(&h[d], (uint32_t)__popc(peers));
         }
@@ -711,7 +746,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_dle_rs_hist(DLevel *L, int p) {
     }
 }
 
-__global__ void __launch_bounds__(1024) k_dle_rs_colscan(DLevel *L, int p) {
+__global__ void __launch_bounds__(1024) k_dle_rs_colscan(DLevel *Lg, int p) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t carry;
     if (!L->live || p >= L->npass) return;
@@ -752,7 +789,9 @@ __global__ void __launch_bounds__(1024) k_dle_rs_colscan(DLevel *L, int p) {
     if (threadIdx.x == 0) total[blockIdx.x] = carry;
 }
 
-__global__ void __launch_bounds__(RS_THREADS) k_dle_rs_scatter(DLevel *L, int p) {
+__global__ void __launch_bounds__(RS_THREADS) k_dle_rs_scatter(DLevel *Lg, int p) {
+    const DLevel Lc = *Lg;  // one read of the descriptor: its fields stay in registers
+    const DLevel *const L = &Lc;
     __shared__ uint32_t wc[RS_WARPS][256];
     __shared__ uint32_t base[256];
     __shared__ uint32_t wtot[8];
@@ -775,7 +814,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_dle_rs_scatter(DLevel *L, int p)
         for (int r = 0; r < RS_ROUNDS; ++r) {
             const int64_t i = rs_item(tile, w, r, lane);
             const bool valid = i < n;
-            k[r] = valid ? keys[i] : 0ull;
+            k[r] = valid ? ld_key(keys, L->k32, i) : 0ull;
             const int d = valid ? (int)((k[r] >> shift) & 255u) : 256 + lane;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             const uint32_t below = (uint32_t)__popc(peers & ((1u << lane) - 1));
@@ -819,7 +858,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_dle_rs_scatter(DLevel *L, int p)
             if (i < n) {
                 const int d = (int)((k[r] >> shift) & 255u);
                 const int64_t dst = (int64_t)base[d] + wc[w][d] + rk[r];
-                keys_out[dst] = k[r];
+                st_key(keys_out, L->k32, dst, k[r]);
                 vals_out[dst] = vals[i];
             }
         }
@@ -828,7 +867,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_dle_rs_scatter(DLevel *L, int p)
 }
 
 // children of the level (k_children_e + k_child_sizes over the sorted split)
-__global__ void k_dle_children(DLevel *L, DLevel *Nx, uint64_t child_off) {
+__global__ void k_dle_children(DLevel *Lg, DLevel *Nxg, uint64_t child_off) {
+    const DLevel Lc = *Lg, Nc = *Nxg;
+    const DLevel *const L = &Lc, *const Nx = &Nc;
     if (!L->live || !Nx->live) return;
     const int64_t E = L->E, n_int = L->n_int;
     const int32_t *vals = (L->npass & 1) ? L->vals2 : L->vals;
@@ -848,7 +889,9 @@ __global__ void k_dle_children(DLevel *L, DLevel *Nx, uint64_t child_off) {
     }
 }
 
-__global__ void k_dle_child_sizes(DLevel *Nx, DevCounters *ctr) {
+__global__ void k_dle_child_sizes(DLevel *Nxg, DevCounters *ctr) {
+    const DLevel Nc = *Nxg;
+    const DLevel *const Nx = &Nc;
     if (!Nx->live) return;
     const int64_t N = Nx->N, M = Nx->M;
     DLE_FOR_WARPS(base, N) {
@@ -869,11 +912,13 @@ __global__ void k_dle_child_sizes(DLevel *Nx, DevCounters *ctr) {
 // k_leaf_small over the level's class lists (warps of class c laid out by
 // the class counts, computed here from the descriptor)
 template <int ELL>
-__global__ void __launch_bounds__(TPB) k_dle_leaf_small(const DLevel *L, const uint64_t *__restrict__ sketch,
+__global__ void __launch_bounds__(TPB) k_dle_leaf_small(const DLevel *L_, const uint64_t *__restrict__ sketch,
                                                         const int32_t *__restrict__ sizes,
                                                         const int8_t *__restrict__ side, int32_t accept, double lam,
                                                         int2 *__restrict__ cand, unsigned long long cap,
                                                         DevCounters *ctr) {
+    const DLevel Lc = *L_;
+    const DLevel *const L = &Lc;
     if (!L->live) return;
     int64_t wcum[SMALL_CLASSES + 1];
     wcum[0] = 0;

@@ -2297,16 +2297,20 @@ std::vector<int64_t> frontier_share(const std::vector<int32_t> &cnt, int32_t lim
 // Device-driven level engine (dle.cuh): the same join with no host read-back
 // inside a level.  Returns 1 = done, 0 = re-run (arena / root list / cap
 // list / candidate buffer grew), -1 = not applicable (the host-driven loop
-// handles it: count-table rule, frontier sharding, ell outside
-// {1,2,4,8,16}, limit > 256, or CPSJ_HOST_LEVELS=1).
+// handles it: the default; also the count-table rule, frontier sharding,
+// ell outside {1,2,4,8,16}, limit > 256).  Enabled by CPSJ_DEVICE_LEVELS=1.
 constexpr int DLE_MAX_LEVELS = 128;
 
 int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, cpsj_join_stats *stats,
                   cudaStream_t st) {
     const int ell = in->ell, t = in->t;
-    const char *host_env = getenv("CPSJ_HOST_LEVELS");
+    // opt-in: measured slower than the host-driven loop on every BASELINE
+    // config (c2 R=2: 4.1 vs 3.7 ms, c5 x0.2 R=3: 9.4 vs 7.5 ms) -- its
+    // fixed-grid kernels and three-launch radix passes cost more than the
+    // three read-backs per level they remove
+    const char *dev_env = getenv("CPSJ_DEVICE_LEVELS");
     const bool frontier = plan->frontier_ranks > 1;
-    if ((host_env != nullptr && host_env[0] == '1') || plan->use_count_table || frontier ||
+    if (!(dev_env != nullptr && dev_env[0] == '1') || plan->use_count_table || frontier ||
         !(ell == 1 || ell == 2 || ell == 4 || ell == 8 || ell == 16) || plan->limit > LB_MAX_PLAN ||
         plan->depth_cap + 2 > DLE_MAX_LEVELS || t > ST_MAX_SEL)
         return -1;
@@ -2687,6 +2691,9 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
     DevBuf<uint64_t> keys, keys2;
     DevBuf<int32_t> vals, vals2;
     DevBuf<int64_t> head, hscan, gstart, keep, ksize, kscan, mscan;
+    DevBuf<uint32_t> rs_scratch;
+    const char *cub_env = getenv("CPSJ_SPLIT_CUB");  // A/B switch: CUB onesweep for the split's group-by
+    const bool split_cub = cub_env != nullptr && cub_env[0] == '1';
 
     // Three host synchronisations per level: (A) leaf/internal totals,
     // (B) candidate count + flag/entry totals, (C) child totals.  Every
@@ -2891,7 +2898,10 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
             drv.scan_multi({nsel.p, nent.p}, {seg_off.p, e_off.p}, n_int + 1);
         }
         // ---- (B) one read: leaf candidates, flags, split entries, depth caps
-        if (leaf_forked) CPSJ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+        // (deferred verification needs no candidate count here: the leaves
+        // keep running on the side stream until the level's arrays are
+        // recycled, see the end of the level)
+        if (leaf_forked && !em.defer) CPSJ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         {
             const int64_t *cand_n = reinterpret_cast<const int64_t *>(&ctr.p->cand_n);
             const int64_t *cap_n = reinterpret_cast<const int64_t *>(&ctr.p->cap_n);
@@ -2934,6 +2944,7 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
 
         // ---- split, part 2: stable group-by (K3)
         bool keys32 = false;
+        const int32_t *split_vals = nullptr;  // member ids in sorted split order
         if (E > 0) {
             ProfScope prof_split(ctx, PROF_SPLIT, st);
             keys.ensure(E, st);
@@ -2956,27 +2967,46 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
                                                                       in->d_values, vbits, keys.p, vals.p,
                                                                       &ctr.p->verr);
             CPSJ_LAUNCH_CHECK();
-            size_t bytes = 0;
-            if (keys32)
-                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k32, k32b, vals.p, vals2.p, E, 0, end_bit, st));
-            else
-                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0,
-                                                          end_bit, st));
-            if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
-            if (keys32)
-                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, k32, k32b, vals.p, vals2.p, E, 0,
-                                                          end_bit, st));
-            else
-                CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
-                                                          0, end_bit, st));
-            ctx->lib_calls++;
+            // stable sort by (segment, value): the hand-written LSD radix
+            // sort (radix.cuh); CPSJ_SPLIT_CUB=1 (A/B) uses CUB's onesweep
+            const void *sorted_keys = nullptr;
+            const int32_t *sorted_vals = nullptr;
+            if (!split_cub) {
+                const size_t words = (size_t)rs_scratch_words(E);
+                if (words > rs_scratch.n) rs_scratch.alloc(words * 2, st);
+                bool flip;
+                if (keys32)
+                    flip = radix_sort_pairs<int32_t, uint32_t>(ctx, k32, vals.p, k32b, vals2.p, E, end_bit,
+                                                               rs_scratch.p, st);
+                else
+                    flip = radix_sort_pairs<int32_t, uint64_t>(ctx, keys.p, vals.p, keys2.p, vals2.p, E, end_bit,
+                                                               rs_scratch.p, st);
+                sorted_keys = flip ? static_cast<const void *>(keys2.p) : static_cast<const void *>(keys.p);
+                sorted_vals = flip ? vals2.p : vals.p;
+            } else {
+                size_t bytes = 0;
+                if (keys32)
+                    CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k32, k32b, vals.p, vals2.p, E, 0, end_bit, st));
+                else
+                    CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, E, 0,
+                                                              end_bit, st));
+                if (bytes > drv.cub_tmp.n) drv.cub_tmp.alloc(bytes * 2, st);
+                if (keys32)
+                    CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, k32, k32b, vals.p, vals2.p, E, 0,
+                                                              end_bit, st));
+                else
+                    CPSJ_CUDA(cub::DeviceRadixSort::SortPairs(drv.cub_tmp.p, bytes, keys.p, keys2.p, vals.p, vals2.p, E,
+                                                              0, end_bit, st));
+                ctx->lib_calls++;
+                sorted_keys = keys2.p;
+                sorted_vals = vals2.p;
+            }
             // kscan / mscan = exclusive scans of the entry-level group marks
             // (kept-group heads, members of kept groups), marks computed
             // inside the scan from the sorted keys
             for (DevBuf<int64_t> *b : {&kscan, &mscan}) b->ensure(E + 1, st);
-            drv.scan_multi({nullptr, nullptr}, {kscan.p, mscan.p}, E + 1,
-                           keys32 ? static_cast<const void *>(k32b) : static_cast<const void *>(keys2.p),
-                           keys32 ? 1 : 0);
+            drv.scan_multi({nullptr, nullptr}, {kscan.p, mscan.p}, E + 1, sorted_keys, keys32 ? 1 : 0);
+            split_vals = sorted_vals;
         }
         // ---- (C) one read: point candidates, children totals
         {
@@ -2997,7 +3027,7 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
             nx.S.ensure(nx.N, st);
             nx.members.ensure(nx.M, st);
             k_children_e<<<blocks_for(E), TPB, 0, st>>>(E, kscan.p, mscan.p, n_int, e_off.p, ilist.p, lv.seed.p,
-                                                        lv.S.p, child_off, nx.off.p, nx.seed.p, nx.S.p, vals2.p,
+                                                        lv.S.p, child_off, nx.off.p, nx.seed.p, nx.S.p, split_vals,
                                                         nx.members.p);
             CPSJ_LAUNCH_CHECK();
             k_child_sizes<<<blocks_for(nx.N), TPB, 0, st>>>(nx.N, nx.M, nx.off.p, nx.S.p, nx.cnt.p, ctr.p);
@@ -3039,6 +3069,9 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
                         (long long)segs[4], (long long)ents[4], (long long)segs[5], (long long)ents[5]);
             }
         }
+        // the side stream's leaf kernels read this level's node arrays and
+        // work lists, which the next level overwrites
+        if (leaf_forked && em.defer) CPSJ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         std::swap(lv, nx);  // the old level's arrays become the next level's storage
         nx.N = nx.M = 0;
     }

@@ -1,6 +1,7 @@
-// Hand-written stable LSD radix sort of (u64 key, value) pairs on the B200
-// (no CUB): used by K6 (the result dedup, cpsjoin.py:308-319) and by the
-// first-seen dense remap of the embedding (embed.py:108-114,129-132).
+// Hand-written stable LSD radix sort of (u32 or u64 key, value) pairs on the
+// B200 (no CUB): used by K6 (the result dedup, cpsjoin.py:308-319), by the
+// first-seen dense remap of the embedding (embed.py:108-114,129-132) and by
+// the split's stable group-by (K3, cpsjoin.py:236-244).
 //
 // Per 8-bit digit pass, three launches over tiles of RS_TILE items:
 //   k_rs_hist     per-tile digit counts, digit-major: cnt[d * T + tile]
@@ -36,7 +37,8 @@ __device__ __forceinline__ int64_t rs_item(int64_t tile, int w, int r, int lane)
     return tile * RS_TILE + (int64_t)w * 32 * RS_ROUNDS + (int64_t)r * 32 + lane;
 }
 
-__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t *__restrict__ keys, int64_t n, int shift,
+template <typename K = uint64_t>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ keys, int64_t n, int shift,
                                                         int64_t T, uint32_t *__restrict__ cnt) {
     __shared__ uint32_t h[256];
     for (int d = threadIdx.x; d < 256; d += RS_THREADS) h[d] = 0;
@@ -95,12 +97,12 @@ __global__ void __launch_bounds__(1024) k_rs_colscan(uint32_t *__restrict__ cnt,
     if (threadIdx.x == 0) total[blockIdx.x] = carry;
 }
 
-template <typename V>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t *__restrict__ keys,
+template <typename V, typename K = uint64_t>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__ keys,
                                                            const V *__restrict__ vals, int64_t n, int shift, int64_t T,
                                                            const uint32_t *__restrict__ cnt,
                                                            const uint32_t *__restrict__ total,
-                                                           uint64_t *__restrict__ keys_out, V *__restrict__ vals_out) {
+                                                           K *__restrict__ keys_out, V *__restrict__ vals_out) {
     __shared__ uint32_t wc[RS_WARPS][256];  // per-warp digit counters, then per-warp digit prefixes
     __shared__ uint32_t base[256];          // this tile's first slot per digit
     __shared__ uint32_t wtot[8];
@@ -108,13 +110,13 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t *__res
     const int64_t tile = blockIdx.x;
     for (int e = threadIdx.x; e < RS_WARPS * 256; e += RS_THREADS) (&wc[0][0])[e] = 0;
     __syncthreads();
-    uint64_t k[RS_ROUNDS];
+    K k[RS_ROUNDS];
     uint32_t rk[RS_ROUNDS];
 #pragma unroll
     for (int r = 0; r < RS_ROUNDS; ++r) {
         const int64_t i = rs_item(tile, w, r, lane);
         const bool valid = i < n;
-        k[r] = valid ? keys[i] : 0ull;
+        k[r] = valid ? keys[i] : (K)0;
         const int d = valid ? (int)((k[r] >> shift) & 255u) : 256 + lane;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const uint32_t below = (uint32_t)__popc(peers & ((1u << lane) - 1));
@@ -176,18 +178,18 @@ inline int64_t rs_scratch_words(int64_t n) {
     return 256 * T + 256;
 }
 
-template <typename V>
-bool radix_sort_pairs(cpsj_ctx *ctx, uint64_t *k0, V *v0, uint64_t *k1, V *v1, int64_t n, int bits,
-                      uint32_t *scratch, cudaStream_t st) {
+template <typename V, typename K = uint64_t>
+bool radix_sort_pairs(cpsj_ctx *ctx, K *k0, V *v0, K *k1, V *v1, int64_t n, int bits, uint32_t *scratch,
+                      cudaStream_t st) {
     require(n < ((int64_t)1 << 32), "radix sort of >= 2^32 items");
     if (n <= 1 || bits <= 0) return false;
     const int64_t T = (n + RS_TILE - 1) / RS_TILE;
     uint32_t *cnt = scratch, *total = scratch + 256 * T;
     bool flip = false;
     for (int shift = 0; shift < bits; shift += 8) {
-        k_rs_hist<<<(unsigned)T, RS_THREADS, 0, st>>>(k0, n, shift, T, cnt);
+        k_rs_hist<K><<<(unsigned)T, RS_THREADS, 0, st>>>(k0, n, shift, T, cnt);
         k_rs_colscan<<<256, 1024, 0, st>>>(cnt, T, total);
-        k_rs_scatter<V><<<(unsigned)T, RS_THREADS, 0, st>>>(k0, v0, n, shift, T, cnt, total, k1, v1);
+        k_rs_scatter<V, K><<<(unsigned)T, RS_THREADS, 0, st>>>(k0, v0, n, shift, T, cnt, total, k1, v1);
         CPSJ_LAUNCH_CHECK();
         ctx->launches += 3;
         std::swap(k0, k1);

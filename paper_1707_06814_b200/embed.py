@@ -402,7 +402,7 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
     d_tok = torch.empty(len(tok), dtype=torch.int32, device=dev)
     d_vals = torch.empty((n, t), dtype=torch.int32, device=dev)
     d_sk = torch.empty((n, sketch[0]), dtype=torch.int64, device=dev) if sketch is not None else None
-    bounds = _chunk_bounds(n, chunks)
+    bounds = _chunk_bounds(n, chunks, nnz=int(off[-1]), t=t, ell=(sketch[0] if sketch is not None else 0))
     chunks = len(bounds) - 1
     d_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
     events = []
@@ -455,32 +455,54 @@ def _embed_pipelined(params: EmbeddingParams, ds: Dataset, sketch, chunks: int) 
     return emb
 
 
-# Chunk schedule of the pipelined embed: the first copy is exposed, so it is
-# small; every later chunk must arrive while K1 hashes the previous one.  The
-# H2D rate (pinned, ~44 GB/s of CSR on the B200 box) against K1 (values +
-# sketch, ~30 GB/s of CSR on config 2) allows a growth factor of about 1.5,
-# and every chunk costs ~0.25 ms (K1 launch overhead, and K1 runs slower
-# while a copy is in flight), so the schedule trades the exposed first copy
-# against the chunk count (simulated optimum on config 2 for 7.4-8.9 ms of
-# H2D: 1/32 growing by 1.8, 6 chunks).
-_FIRST_CHUNK = 1.0 / 32
-_CHUNK_GROWTH = 1.8
+# Chunk schedule of the pipelined embed.  The first copy is exposed, every
+# later chunk must arrive while K1 hashes the chunks before it, and every
+# chunk costs a fixed overhead (length order + two K1 launches and their
+# tails).  With cumulative fractions S_c, copy time T_copy and K1 time T_k1
+# for the whole input, chunk c + 1 has arrived when chunk c is done iff
+#   T_copy S_{c+1} <= T_copy S_0 + T_k1 S_c,
+# so S_{c+1} = S_0 + rho S_c with rho = T_k1 / T_copy (taken with a 10%
+# margin) is the fastest-growing stall-free schedule; S_0 is the candidate
+# that minimises  S_0 T_copy + chunks x overhead.  Rates measured on the B200
+# boxes: ~50 GB/s pinned H2D; K1 values 4.1e12 and sketches 5.5e12 hash
+# evaluations/s on Zipf sets (tools/k1_probe.py).  A copy-bound input
+# (rho < 1.3) keeps a geometric growth of 1.3 instead.
+_H2D_BYTES_PER_S = 50e9
+_K1_VALUES_EVALS_PER_S = 4.1e12
+_K1_SKETCH_EVALS_PER_S = 5.5e12
+_CHUNK_OVERHEAD_S = 0.15e-3
+_FIRST_CHUNKS = (1.0 / 64, 1.0 / 32, 1.0 / 16, 1.0 / 8, 1.0 / 4)
+_MIN_GROWTH = 1.3
 
 
-def _chunk_bounds(n: int, chunks: int | None) -> np.ndarray:
+def _chunk_fractions(t_copy: float, t_k1: float) -> list:
+    rho = 0.9 * t_k1 / max(t_copy, 1e-12)
+    best = None
+    for s0 in _FIRST_CHUNKS:
+        S = [s0]
+        while S[-1] < 1.0 - 1e-9 and len(S) < 64:
+            S.append(max(s0 + rho * S[-1], _MIN_GROWTH * S[-1]))
+        S = [x / S[-1] for x in S]  # scaled to end at 1 (the recurrence is linear, so it still holds)
+        S[-1] = 1.0
+        cost = S[0] * t_copy + len(S) * _CHUNK_OVERHEAD_S
+        if best is None or cost < best[0]:
+            best = (cost, S)
+    return best[1]
+
+
+def _chunk_bounds(n: int, chunks: int | None, nnz: int | None = None, t: int = 128, ell: int = 8) -> np.ndarray:
     """Set-aligned chunk boundaries: an explicit count uses doubling chunks
-    (1/2^(c-1), ..., 1/4, 1/2); None uses the growth schedule above."""
+    (1/2^(c-1), ..., 1/4, 1/2); None uses the rate-based schedule above
+    (nnz = tokens of the input, t / 64 ell = values / sketch functions)."""
     if chunks is not None:
         frac = np.array([0.0] + [2.0 ** -(chunks - 1)] + [2.0 ** -(chunks - k) for k in range(1, chunks)])
+        cum = np.cumsum(frac)
     else:
-        f, acc, fr = _FIRST_CHUNK, 0.0, [0.0]
-        while acc + f < 1.0 - 1e-9:
-            fr.append(f)
-            acc += f
-            f *= _CHUNK_GROWTH
-        fr.append(1.0 - acc)
-        frac = np.array(fr)
-    bounds = np.minimum(np.round(np.cumsum(frac) * n), n).astype(np.int64)
+        nnz = 100 * n if nnz is None else nnz
+        t_copy = (4.0 * nnz + 8.0 * n) / _H2D_BYTES_PER_S
+        t_k1 = nnz * (t / _K1_VALUES_EVALS_PER_S + 64.0 * ell / _K1_SKETCH_EVALS_PER_S)
+        cum = np.array([0.0] + _chunk_fractions(t_copy, t_k1))
+    bounds = np.minimum(np.round(cum * n), n).astype(np.int64)
     bounds[-1] = n
     return bounds
 

@@ -187,13 +187,15 @@ def test_join_matches_reference_golden(name):
 
 @pytest.mark.parametrize("env", [{"CPSJ_NO_SUBTREE": "1"}, {"CPSJ_K7_TINY_SCRATCH": "1"},
                                  {"CPSJ_NO_SMALL_LEAF": "1", "CPSJ_NO_LEAF_OVERLAP": "1"},
-                                 {"CPSJ_TINY_CAND_CAP": "1"}, {"CPSJ_NO_BLOCK_LEAF": "1"}])
+                                 {"CPSJ_TINY_CAND_CAP": "1"}, {"CPSJ_NO_BLOCK_LEAF": "1"},
+                                 {"CPSJ_DEVICE_LEVELS": "1"}, {"CPSJ_DEVICE_LEVELS": "1", "CPSJ_NO_SUBTREE": "1"}])
 @pytest.mark.parametrize("name", ["planted_880", "dense_cluster", "c1_sample"])
 def test_join_alternate_paths_match_reference_golden(name, env, monkeypatch):
     """The same trees through the level kernels only (no K7 handoff), through
     K7 with scratch small enough to overflow and retry, through the
-    pair-packed small-leaf kernel on the main stream, and with a candidate
-    buffer small enough that the call re-runs: identical results."""
+    pair-packed small-leaf kernel on the main stream, with a candidate
+    buffer small enough that the call re-runs, and through the opt-in
+    device-driven level engine (csrc/dle.cuh): identical results."""
     from paper_1707_06814_b200 import Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
     for k, v in env.items():
         monkeypatch.setenv(k, v)
