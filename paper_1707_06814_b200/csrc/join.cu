@@ -111,7 +111,7 @@ __global__ void k_plan(int64_t N, const int32_t *__restrict__ cnt, int32_t limit
     unsigned long long pre = 0;
     // with class lists, leaves of 33..LB_MAX_PLAN members go to the block
     // kernel instead of the tile kernel (needs limit <= LB_MAX_PLAN;
-    // block_max = 0 turns it off: CPSJ_NO_BLOCK_LEAF, A/B)
+    // block_max = 0, the default, turns it off: CPSJ_BLOCK_LEAF, A/B)
     const bool block_leaves = slists != nullptr && limit <= block_max;
     if (slists != nullptr) {
         // small leaves straight into their class lists (warp-aggregated
@@ -1727,10 +1727,14 @@ struct Driver {
     }
 };
 
-// A/B switch: CPSJ_NO_BLOCK_LEAF=1 sends every leaf > 32 members to the tile kernel
+// Leaves > 32 members go to the tile kernel; CPSJ_BLOCK_LEAF=1 (A/B) sends
+// those of <= LB_MAX_PLAN members to the CTA-per-leaf kernel instead.  Off
+// by default on measurement: k_leaf_block stages a leaf's sketches once but
+// its launches are slower than the tile kernel's (c2: 520 vs 392 us of
+// device time per join; join wall time equal on c2, 2-4% slower on c1/c5).
 inline int32_t block_leaf_max() {
-    const char *e = getenv("CPSJ_NO_BLOCK_LEAF");
-    return (e != nullptr && e[0] == '1') ? 0 : LB_MAX_PLAN;
+    const char *e = getenv("CPSJ_BLOCK_LEAF");
+    return (e != nullptr && e[0] == '1') ? LB_MAX_PLAN : 0;
 }
 
 struct LeafWork {
@@ -2434,7 +2438,8 @@ int self_join_dle(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan, c
     for (int depth = 0; depth + 1 < DLE_MAX_LEVELS && depth <= plan->depth_cap + 1; ++depth) {
         DLevel *Lp = L(depth), *Nx = L(depth + 1);
         std::unique_ptr<ProfScope> prof(new ProfScope(ctx, PROF_PLAN, st));
-        dle::k_dle_plan<<<G, TPB, 0, st>>>(Lp, plan->limit, block_leaf_max(), subtree_on ? ST_MAX_SUBM : 0, depth,
+        // (the engine has no tile kernel: every leaf > 32 members is a block leaf)
+        dle::k_dle_plan<<<G, TPB, 0, st>>>(Lp, plan->limit, LB_MAX_PLAN, subtree_on ? ST_MAX_SUBM : 0, depth,
                                           defer_depth, defer_level_m, sticky.p, ctr.p);
         dscan(depth, 2, {DL_OFF(internal), DL_OFF(imem)}, {DL_OFF(iscan), DL_OFF(im_off)}, DL_OFF(N), 1, 0,
               /*hook=alloc_internal*/ 1, &ctr.p->visits);
@@ -2692,8 +2697,12 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
     DevBuf<int32_t> vals, vals2;
     DevBuf<int64_t> head, hscan, gstart, keep, ksize, kscan, mscan;
     DevBuf<uint32_t> rs_scratch;
-    const char *cub_env = getenv("CPSJ_SPLIT_CUB");  // A/B switch: CUB onesweep for the split's group-by
-    const bool split_cub = cub_env != nullptr && cub_env[0] == '1';
+    // the split's stable group-by: CUB's onesweep radix sort by default;
+    // CPSJ_SPLIT_OWN_SORT=1 (A/B) uses the hand-written LSD sort of radix.cuh
+    // (three launches per digit pass; measured slower: c2 join 3.76 vs 3.60 ms,
+    // c5 x0.2 8.47 vs 7.51 ms)
+    const char *own_env = getenv("CPSJ_SPLIT_OWN_SORT");
+    const bool split_cub = !(own_env != nullptr && own_env[0] == '1');
 
     // Three host synchronisations per level: (A) leaf/internal totals,
     // (B) candidate count + flag/entry totals, (C) child totals.  Every
@@ -2967,8 +2976,7 @@ bool self_join_once(cpsj_ctx *ctx, const cpsj_inputs *in, const cpsj_plan *plan,
                                                                       in->d_values, vbits, keys.p, vals.p,
                                                                       &ctr.p->verr);
             CPSJ_LAUNCH_CHECK();
-            // stable sort by (segment, value): the hand-written LSD radix
-            // sort (radix.cuh); CPSJ_SPLIT_CUB=1 (A/B) uses CUB's onesweep
+            // stable sort by (segment, value)
             const void *sorted_keys = nullptr;
             const int32_t *sorted_vals = nullptr;
             if (!split_cub) {

@@ -849,19 +849,25 @@ template <int L, bool PFX>
 __global__ void __launch_bounds__(K1S_THREADS, 1) k_sketch_s16(
     const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
     const int32_t *__restrict__ order, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
-    const uint32_t *__restrict__ bitmask, const uint4 *__restrict__ simg, int F, const K1Out out) {
+    const uint32_t *__restrict__ bitmask, const uint4 *__restrict__ simg, int F, const K1Out out, int split) {
     extern __shared__ __align__(128) uint4 tab4[];  // [L][256][16] x uint4, then the mbarrier
     uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + L * 256 * 16);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tab4);
     const uint32_t lane_base = smem0 + ((uint32_t)(lane & 15) << 4);
     const int nchunks = (F + 127) >> 7;
-    const int64_t p_first = (int64_t)blockIdx.x * K1S_WARPS + warp, p_step = (int64_t)gridDim.x * K1S_WARPS;
+    // split: the grid is nchunks groups of CTAs and group g hashes function
+    // chunk g over all sets (one table load per CTA and no barrier between
+    // chunks); else every CTA loops over the chunks
+    const int c_first = split ? (int)(blockIdx.x % (unsigned)nchunks) : 0, c_last = split ? c_first + 1 : nchunks;
+    const int64_t slot = split ? (int64_t)(blockIdx.x / (unsigned)nchunks) : (int64_t)blockIdx.x;
+    const int64_t slots = split ? (int64_t)(gridDim.x / (unsigned)nchunks) : (int64_t)gridDim.x;
+    const int64_t p_first = slot * K1S_WARPS + warp, p_step = slots * K1S_WARPS;
     const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(mbar);
     if (threadIdx.x == 0) mbar_init(mbar_a, 1);
     __syncthreads();
     uint32_t phase = 0;
-    for (int c = 0; c < nchunks; ++c) {
+    for (int c = c_first; c < c_last; ++c) {
         __syncthreads();  // every warp is done with the previous chunk's tables
         if (threadIdx.x == 0) {
             const uint32_t tab_bytes = (uint32_t)L * 65536u;
@@ -1349,9 +1355,19 @@ static void launch_sketch_s16(cpsj_ctx *ctx, const cpsj_family *fam, const uint3
         order = own.p;
     }
     const int64_t want = ((n + 1) / 2 + K1S_WARPS - 1) / K1S_WARPS;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
+    // one function chunk per CTA group when the SMs divide evenly among the
+    // chunks (ell = 2, 4, 8 on 148 SMs); CPSJ_K1_NO_SPLIT=1 (A/B) keeps every
+    // CTA looping over the chunks
+    const int nchunks = (fam->F + 127) / 128;
+    const char *ns = getenv("CPSJ_K1_NO_SPLIT");
+    int split = 0;
+    if (nchunks > 1 && ctx->sm_count % nchunks == 0 && !(ns && ns[0] == '1')) {
+        split = 1;
+        grid = (int)std::min<int64_t>(want, (int64_t)ctx->sm_count / nchunks) * nchunks;
+    }
     kern<<<grid, K1S_THREADS, smem, stream>>>(tok, off, n, order, fam->d_hi, fam->d_lo, fam->d_bitmask,
-                                              reinterpret_cast<const uint4 *>(fam->d_simg[L - 1]), fam->F, out);
+                                              reinterpret_cast<const uint4 *>(fam->d_simg[L - 1]), fam->F, out, split);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
 }

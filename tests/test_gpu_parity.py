@@ -187,7 +187,7 @@ def test_join_matches_reference_golden(name):
 
 @pytest.mark.parametrize("env", [{"CPSJ_NO_SUBTREE": "1"}, {"CPSJ_K7_TINY_SCRATCH": "1"},
                                  {"CPSJ_NO_SMALL_LEAF": "1", "CPSJ_NO_LEAF_OVERLAP": "1"},
-                                 {"CPSJ_TINY_CAND_CAP": "1"}, {"CPSJ_NO_BLOCK_LEAF": "1"},
+                                 {"CPSJ_TINY_CAND_CAP": "1"}, {"CPSJ_BLOCK_LEAF": "1"}, {"CPSJ_SPLIT_OWN_SORT": "1"},
                                  {"CPSJ_DEVICE_LEVELS": "1"}, {"CPSJ_DEVICE_LEVELS": "1", "CPSJ_NO_SUBTREE": "1"}])
 @pytest.mark.parametrize("name", ["planted_880", "dense_cluster", "c1_sample"])
 def test_join_alternate_paths_match_reference_golden(name, env, monkeypatch):
