@@ -255,9 +255,9 @@ def int_peak(op_prefix: str, default: float):
 def ncu_traffic(cfg: int, launch: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
     dominant kernel from the committed ncu --set full capture, if it was
-    taken on this config (profiles/ncu_traffic_r01.json)."""
+    taken on this config (profiles/ncu_traffic_r02.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")) as f:
             d = json.load(f)
         return float(d["dram_bytes_per_launch"][launch]) if int(d["config"]) == cfg else None
     except (OSError, KeyError, ValueError):
@@ -647,6 +647,19 @@ def run_ours(args, rank: int, world: int):
     # evaluation against the measured 126 B/clk/SM conflict-free LDS rate
     # (profiles/int_peaks_r01.json: LDS.64 15.76 lanes x 8 B per clk per SM)
     lookup_peak = 148 * f_clk * 126.0 / (2 * L)
+    # with cached upper-byte entries (sorted tokens) a token needs T0 always,
+    # T1 when tok >> 8 differs from its predecessor in the set, T2 when
+    # tok >> 16 does: the minimum lookups per evaluation of this data
+    tk = w.tokens
+    first = np.zeros(len(tk), dtype=bool)
+    first[w.offsets[:-1]] = True
+    ch1 = np.ones(len(tk), dtype=bool)
+    ch1[1:] = (tk[1:] >> 8) != (tk[:-1] >> 8)
+    ch2 = np.ones(len(tk), dtype=bool)
+    ch2[1:] = (tk[1:] >> 16) != (tk[:-1] >> 16)
+    lookups_min = 1.0 + (float((ch1 | first).mean()) if L > 1 else 0.0) + (float((ch2 | first).mean()) if L > 2 else 0.0)
+    lookup_peak_cached = 148 * f_clk * 126.0 / (2 * lookups_min)
+    del first, ch1, ch2
     k4_ms = prof["k4_leaf"][0] + prof["point"][0]
     pre = res.counters.pre_candidates
     pairs_per_s = pre / (k4_ms / 1e3) if k4_ms > 0 else None
@@ -741,16 +754,26 @@ def run_ours(args, rank: int, world: int):
                                                      "recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
                      "frac": achieved / float(peaks["hbm_gbs"]), "traffic": ncu_traffic(args.config, "sketch"),
-                     "kernel": "k_sketch_s16<L> sketch launch (K1, 64*ell functions)",
+                     "kernel": "k_sketch_s16<L, PFX> sketch launch (K1, 64*ell functions)",
                      "algorithmic_bytes": sk_bytes, "avg_launch_ms": k1_sk_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
                      "note": "the dominant kernel is bound by shared-memory table lookups, not HBM: "
                              "roofline_smem.frac is its bound; HBM bytes are the CSR read + sketch write "
                              "(traffic = the token stream re-read once per 128-function chunk)"},
         "roofline_smem": {"bound": "shared-memory lookups (16-bit entries, 126 B/clk/SM measured LDS rate)",
-                          "achieved_evals_per_s": evals / (k1_sk_ms / 1e3), "peak_evals_per_s": lookup_peak,
-                          "frac": evals / (k1_sk_ms / 1e3) / lookup_peak, "key_bytes": L,
-                          "values_launch_ms": k1_val_ms},
+                          "achieved_evals_per_s": evals / (k1_sk_ms / 1e3),
+                          "peak_evals_per_s": lookup_peak_cached,
+                          "frac": evals / (k1_sk_ms / 1e3) / lookup_peak_cached,
+                          "lookups_per_eval_min": lookups_min,
+                          "peak_evals_per_s_all_key_bytes": lookup_peak,
+                          "frac_all_key_bytes": evals / (k1_sk_ms / 1e3) / lookup_peak, "key_bytes": L,
+                          "values_launch_ms": k1_val_ms,
+                          "note": "peak = 148 SMs x sm_max_mhz x 126 B/clk / (2 B x lookups per evaluation); "
+                                  "lookups_per_eval_min counts T0 per token plus T1/T2 only where a sorted set's "
+                                  "upper key bytes change (the kernel's cached-entry path); frac_all_key_bytes is "
+                                  "round 1's denominator (every key byte looked up for every token) and can "
+                                  "exceed 1.  ncu of the same launch (profiles/ncu_k1_s16_r02_c2.csv): shared "
+                                  "wavefronts 87% of peak incl. the token shuffles, ALU pipe 74%, issue 73%"},
         "roofline_int": {"kernel": "k_leaf_tiles + k_point (K4 BruteForce)", "pairs_per_s": pairs_per_s,
                          "peak_pairs_per_s": popc_peak,
                          "frac": (pairs_per_s / popc_peak) if pairs_per_s else None,
