@@ -17,5 +17,9 @@ python tools/k1_once.py 2 1.0 > $O/plain_k1.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:"k_sketch_s16|k_values_h8" -c 2 -f -o $O/ncu_k1_r02 python tools/k1_once.py 2 1.0 > $O/ncu_k1.log 2>&1
 echo "ncu k1 rc=$?"
 python tools/join_once.py 2 1.0 2 > $O/plain_join.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:"k_leaf_tiles|k_leaf_small|k_build_keys|Onesweep|k_flags|k_verify|k_children_e|k_survivors|k_subtree|k_rs_scatter" -c 40 -f -o $O/ncu_join_r02 python tools/join_once.py 2 1.0 2 > $O/ncu_join.log 2>&1
+ncu --set full --clock-control none -k regex:"k_leaf_tiles|k_leaf_small|k_build_keys|Onesweep|k_flags|k_verify|k_children_e|k_survivors|k_subtree|k_rs_scatter" -c 40 -f -o $O/ncu_join_r02 python tools/join_once.py 2 1.0 2 > $O/ncu_join.log 2>&1
 echo "ncu join rc=$?"
+# gpurun brings back at most 64 MiB: summaries here, the big report stays behind
+python tools/ncu_summary.py $O/ncu_join_r02.ncu-rep $O/ncu_join_r02_c2.csv && rm -f $O/ncu_join_r02.ncu-rep
+python tools/ncu_summary.py $O/ncu_k1_r02.ncu-rep $O/ncu_k1_r02_c2.csv
+du -sh gpurun_out

@@ -25,7 +25,7 @@ h = torch.cuda.current_stream().cuda_stream
 
 
 def run(n, env):
-    for k in ("CPSJ_K1_NO_ORDER", "CPSJ_K1_NO_FUSE", "CPSJ_K1_COOP_COPY"):
+    for k in ("CPSJ_K1_NO_ORDER", "CPSJ_K1_FUSE", "CPSJ_K1_NO_SPLIT"):
         os.environ.pop(k, None)
     os.environ.update(env)
     ts = []
@@ -46,6 +46,6 @@ t_end = time.time() + 3
 while time.time() < t_end:
     run(100000, {})
 for n in [1000, 10000, 31250, 100000, 300000, 1000000]:
-    print(f"n={n:8d}: fused {run(n, {}):.3f} ms  no-order {run(n, {'CPSJ_K1_NO_ORDER': '1'}):.3f} ms  "
-          f"two launches {run(n, {'CPSJ_K1_NO_FUSE': '1'}):.3f} ms "
+    print(f"n={n:8d}: default {run(n, {}):.3f} ms  no-order {run(n, {'CPSJ_K1_NO_ORDER': '1'}):.3f} ms  "
+          f"fused launch {run(n, {'CPSJ_K1_FUSE': '1'}):.3f} ms  no-split {run(n, {'CPSJ_K1_NO_SPLIT': '1'}):.3f} ms "
           f"  per-set {13.1e-3 * n / 1000:.3f}")
