@@ -88,8 +88,8 @@ CPSJ_API int cpsj_minhash_sketch(cpsj_ctx *ctx, const cpsj_family *fam,
 
 /*
  * K1 for the embed path: the embedding family's values AND the sketch
- * family's sketches of the same n_sets CSR sets in one launch (one
- * length-ordered pass per 128-function chunk of either family).
+ * family's sketches of the same n_sets CSR sets in one call (one length
+ * order shared by the values launch and the sketch launch).
  * Replaces embed_dataset (embed.py:117-139) followed by
  * EmbeddedDataset.sketches (embed.py:90-98 -> build_sketch_matrix,
  * hashing.py:197-211); outputs as cpsj_minhash_sketch's (both required).

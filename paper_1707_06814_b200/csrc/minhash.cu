@@ -495,6 +495,11 @@ constexpr int K1H_THREADS = K1H_WARPS * 32;
 #define K1S_WARPS 32
 #endif
 constexpr int K1S_THREADS = K1S_WARPS * 32;
+// warps of the values-only kernel (A/B: -DK1V_WARPS=32 runs it at 64 registers)
+#ifndef K1V_WARPS
+#define K1V_WARPS 24
+#endif
+constexpr int K1V_THREADS = K1V_WARPS * 32;
 // sketch_chunk_bits: a 16-token batch (both halves of the warp, 32 slots)
 // uses the cached upper entries when at most this many of its tokens change
 // key byte 1
@@ -939,7 +944,7 @@ __device__ __forceinline__ uint32_t imad16(uint32_t x, uint32_t add) {
 }
 
 template <int L>
-__global__ void __launch_bounds__(K1H_THREADS, 1) k_values_h8(
+__global__ void __launch_bounds__(K1V_THREADS, 1) k_values_h8(
     const uint32_t *__restrict__ tokens, const int64_t *__restrict__ offsets, int64_t n,
     const int32_t *__restrict__ order, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
     const uint4 *__restrict__ vimg, int F, const K1Out out) {
@@ -952,7 +957,7 @@ __global__ void __launch_bounds__(K1H_THREADS, 1) k_values_h8(
     const uint32_t lane_base = smem0 + ((uint32_t)l << 4);
     const int nchunks = (F + 127) >> 7;
     const int64_t npairs = (n + 1) >> 1;
-    const int64_t p_first = (int64_t)blockIdx.x * K1H_WARPS + warp, p_step = (int64_t)gridDim.x * K1H_WARPS;
+    const int64_t p_first = (int64_t)blockIdx.x * K1V_WARPS + warp, p_step = (int64_t)gridDim.x * K1V_WARPS;
     const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(mbar);
     if (threadIdx.x == 0) mbar_init(mbar_a, 1);
     __syncthreads();
@@ -1332,9 +1337,9 @@ static void launch_values_h8(cpsj_ctx *ctx, const cpsj_family *fam, const uint32
         own = length_order(ctx, off, n, stream);
         order = own.p;
     }
-    const int64_t want = ((n + 1) / 2 + K1H_WARPS - 1) / K1H_WARPS;
+    const int64_t want = ((n + 1) / 2 + K1V_WARPS - 1) / K1V_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
-    k_values_h8<L><<<grid, K1H_THREADS, smem, stream>>>(tok, off, n, order, fam->d_hi, fam->d_lo,
+    k_values_h8<L><<<grid, K1V_THREADS, smem, stream>>>(tok, off, n, order, fam->d_hi, fam->d_lo,
                                                         reinterpret_cast<const uint4 *>(fam->d_vimg[L - 1]), fam->F,
                                                         out);
     CPSJ_LAUNCH_CHECK();

@@ -283,3 +283,21 @@ def test_reference_shaped_embedded_dataset_matches_reference():
     assert np.array_equal(ours.sizes, ref.sizes) and ours.sizes.dtype == ref.sizes.dtype
     assert np.array_equal(ours.values, ref.values) and ours.values.dtype == ref.values.dtype
     assert np.array_equal(ours.sketches(8, 5), ref.sketches(8, 5))
+
+
+@pytest.mark.parametrize("t_copy,t_k1", [(8.2e-3, 11.2e-3), (1.4e-3, 3.4e-3), (12e-3, 30e-3), (8e-3, 4e-3),
+                                         (1e-6, 1e-6)])
+def test_pipelined_chunk_schedule_is_stall_free(t_copy, t_k1):
+    """embed._chunk_fractions: cumulative fractions rise to exactly 1, and
+    when K1 is slower than the copy (rho >= growth floor) chunk c + 1 has
+    arrived by the time chunk c is hashed: T_copy S_{c+1} <= T_copy S_0 + T_k1 S_c."""
+    from paper_1707_06814_b200.embed import _MIN_GROWTH, _chunk_bounds, _chunk_fractions
+    S = _chunk_fractions(t_copy, t_k1)
+    assert S[-1] == 1.0 and all(b > a for a, b in zip(S, S[1:])) and 0 < S[0] <= 0.25 and len(S) <= 64
+    if 0.9 * t_k1 / t_copy >= _MIN_GROWTH:
+        for c in range(len(S) - 1):
+            assert t_copy * S[c + 1] <= t_copy * S[0] + t_k1 * S[c] + 1e-12
+    b = _chunk_bounds(100_000, None, nnz=10_000_000, t=128, ell=8)
+    assert b[0] == 0 and b[-1] == 100_000 and np.all(np.diff(b) >= 0)
+    b = _chunk_bounds(100_000, 4)
+    assert list(b) == [0, 12500, 25000, 50000, 100000]
