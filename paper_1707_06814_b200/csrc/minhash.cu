@@ -495,9 +495,10 @@ constexpr int K1H_THREADS = K1H_WARPS * 32;
 #define K1S_WARPS 32
 #endif
 constexpr int K1S_THREADS = K1S_WARPS * 32;
-// warps of the values-only kernel (A/B: -DK1V_WARPS=32 runs it at 64 registers)
+// warps of the values-only kernel: 32 at 64 registers (spills stay outside the token
+// loop; c2 3.08 -> 3.06 ms, c3 0.86 -> 0.80 ms against 24 warps at 80 registers)
 #ifndef K1V_WARPS
-#define K1V_WARPS 24
+#define K1V_WARPS 32
 #endif
 constexpr int K1V_THREADS = K1V_WARPS * 32;
 // sketch_chunk_bits: a 16-token batch (both halves of the warp, 32 slots)
@@ -1362,12 +1363,17 @@ static void launch_sketch_s16(cpsj_ctx *ctx, const cpsj_family *fam, const uint3
     const int64_t want = ((n + 1) / 2 + K1S_WARPS - 1) / K1S_WARPS;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
     // one function chunk per CTA group when the SMs divide evenly among the
-    // chunks (ell = 2, 4, 8 on 148 SMs); CPSJ_K1_NO_SPLIT=1 (A/B) keeps every
+    // chunks (ell = 2, 4, 8 on 148 SMs), and always for a launch with few
+    // sets per warp (a chunk of the pipelined embed, long sets): the groups
+    // put nchunks times as many warps to work, which outweighs the
+    // sm_count % nchunks idle SMs.  CPSJ_K1_NO_SPLIT=1 (A/B) keeps every
     // CTA looping over the chunks
     const int nchunks = (fam->F + 127) / 128;
     const char *ns = getenv("CPSJ_K1_NO_SPLIT");
     int split = 0;
-    if (nchunks > 1 && ctx->sm_count % nchunks == 0 && !(ns && ns[0] == '1')) {
+    const int64_t pairs_per_warp = ((n + 1) / 2) / ((int64_t)ctx->sm_count * K1S_WARPS);
+    if (nchunks > 1 && nchunks <= ctx->sm_count && (ctx->sm_count % nchunks == 0 || pairs_per_warp < 16) &&
+        !(ns && ns[0] == '1')) {
         split = 1;
         grid = (int)std::min<int64_t>(want, (int64_t)ctx->sm_count / nchunks) * nchunks;
     }

@@ -471,14 +471,22 @@ _H2D_BYTES_PER_S = 50e9
 _K1_VALUES_EVALS_PER_S = 4.1e12
 _K1_SKETCH_EVALS_PER_S = 5.5e12
 _CHUNK_OVERHEAD_S = 0.15e-3
-_FIRST_CHUNKS = (1.0 / 64, 1.0 / 32, 1.0 / 16, 1.0 / 8, 1.0 / 4)
+_FIRST_CHUNKS = (1.0 / 64, 1.0 / 32, 1.0 / 16, 1.0 / 8, 1.0 / 4, 1.0 / 2)
 _MIN_GROWTH = 1.3
+_MIN_CHUNK_SETS = 20_000
 
 
-def _chunk_fractions(t_copy: float, t_k1: float) -> list:
+def _chunk_fractions(t_copy: float, t_k1: float, n: int = 0) -> list:
     rho = 0.9 * t_k1 / max(t_copy, 1e-12)
     best = None
-    for s0 in _FIRST_CHUNKS:
+    # a K1 launch needs about two set pairs per warp (148 SMs x 32 warps x 2
+    # sets x 2) to keep every warp busy -- long sets (c4: 300 tokens, 1024
+    # sketch functions) otherwise run a small chunk at a fraction of the
+    # kernel's rate: no first chunk smaller than _MIN_CHUNK_SETS
+    s_min = min(1.0, _MIN_CHUNK_SETS / n) if n > 0 else 0.0
+    for s0 in _FIRST_CHUNKS + (1.0,):
+        if s0 < s_min and s0 < 1.0:
+            continue
         S = [s0]
         while S[-1] < 1.0 - 1e-9 and len(S) < 64:
             S.append(max(s0 + rho * S[-1], _MIN_GROWTH * S[-1]))
@@ -501,7 +509,7 @@ def _chunk_bounds(n: int, chunks: int | None, nnz: int | None = None, t: int = 1
         nnz = 100 * n if nnz is None else nnz
         t_copy = (4.0 * nnz + 8.0 * n) / _H2D_BYTES_PER_S
         t_k1 = nnz * (t / _K1_VALUES_EVALS_PER_S + 64.0 * ell / _K1_SKETCH_EVALS_PER_S)
-        cum = np.array([0.0] + _chunk_fractions(t_copy, t_k1))
+        cum = np.array([0.0] + _chunk_fractions(t_copy, t_k1, n))
     bounds = np.minimum(np.round(cum * n), n).astype(np.int64)
     bounds[-1] = n
     return bounds

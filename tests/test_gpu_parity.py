@@ -530,17 +530,17 @@ def test_pipelined_embed_with_sketch_hint_matches_oracle(chunks):
     assert np.array_equal(res.a, ref.a) and np.array_equal(res.similarity, ref.sims)
 
 
-@pytest.mark.parametrize("cfg,scale", [(2, 0.07), (3, 0.1)])
+@pytest.mark.parametrize("cfg,scale", [(2, 0.07), (3, 0.4)])
 def test_default_pipelined_embed_matches_oracle(cfg, scale):
-    """The DEFAULT chunk schedule (chunks=None: first chunk 1/32 growing by
-    1.8, used by embed_dataset for n >= 65,536 and by the bench's e2e leg)
-    gives the oracle's values, sketches and join bit for bit."""
+    """The DEFAULT chunk schedule (chunks=None: the rate-based schedule of
+    embed._chunk_fractions, used by embed_dataset for n >= 65,536 and by the
+    bench's e2e leg) gives the oracle's values, sketches and join bit for bit."""
     from oracle import oracle as O
     from paper_1707_06814_b200 import CPSJoinParams, Dataset, EmbeddingParams, cpsjoin_self_arrays, embed_dataset
     from paper_1707_06814_b200.embed import _PIPELINE_MIN_SETS, _chunk_bounds
     from paper_1707_06814_b200.workloads import generate
     w = generate(cfg, scale=scale)
-    assert w.n >= _PIPELINE_MIN_SETS and len(_chunk_bounds(w.n, None)) > 3
+    assert w.n >= _PIPELINE_MIN_SETS and len(_chunk_bounds(w.n, None, nnz=len(w.tokens), t=128, ell=8)) > 2
     ds = Dataset.from_csr(w.tokens, w.offsets, w.d)
     emb = embed_dataset(EmbeddingParams(t=128, seed=7), ds, sketch=(8, 7))
     values, sk, ref = O.full_pipeline(w.tokens, w.offsets, w.sizes, lam=0.5, emb_seed=7, seed=7, repetitions=2)
