@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional multi-rank run through host-staged collectives (not a bench number)")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-workload oracle comparison")
+    ap.add_argument("--full-parity", action="store_true",
+                    help="when the timed CPU baseline ran on a scaled sample, run the oracle once more (untimed) on "
+                         "the whole workload so that parity.device_vs_oracle is always present")
     return ap.parse_args()
 
 
@@ -717,6 +720,13 @@ def run_ours(args, rank: int, world: int):
         cpu = {"value": cw.n / cdt, "unit": "sets/s", "cores": threads, "kind": "port",
                "sample": f"{cfg.name} x{cscale:g}: {cw.n} sets, embed+sketch+join R={R}"
                          + (f" (recall {crec:.3f})" if crec is not None else "") + f", {cdt:.2f} s"}
+        if cw is not w and args.full_parity and not args.no_parity:
+            # the timed CPU sample was a scaled workload: the oracle once more,
+            # untimed, on the whole workload for the bit-exact comparison
+            farm = CpuArm(w, cfg, threads)
+            farm.lam = lam
+            _, cout = farm.pipeline(R)
+            cw = w
         if cw is w and not args.no_parity:
             ocnt = [cout.pre_candidates, cout.candidates, cout.results, cout.max_depth, cout.peak_live_members]
             parity["device_vs_oracle"] = parity_check(res, cout.keys, cout.sims, ocnt)

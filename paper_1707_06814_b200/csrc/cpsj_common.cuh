@@ -205,8 +205,9 @@ struct cpsj_family {
     // and the [128][33] bit-mask block; copied to shared memory with TMA
     void *d_img16[3] = {nullptr, nullptr, nullptr};
     // and the sketch kernel's [L][256][16]{8 functions} (h15 << 1 | bit) images
-    void *d_simg[3] = {nullptr, nullptr, nullptr};
-    void *d_vimg[3] = {nullptr, nullptr, nullptr};  // same layout, top-16-bit entries (values kernel)
+    // slots 0-2: key widths 1-3; slot 3: the wide-second-table layout (minhash.cu: LW)
+    void *d_simg[4] = {nullptr, nullptr, nullptr, nullptr};
+    void *d_vimg[4] = {nullptr, nullptr, nullptr, nullptr};  // same layout, top-16-bit entries (values kernel)
     uint32_t *d_bmimg = nullptr;
 };
 

@@ -472,10 +472,24 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     return v;
 }
 
+// Template value LW ("wide second table"): universes below 2^17 tokens have
+// at most two values of key byte 2, so T1 and T2 are folded into ONE table of
+// 512 rows indexed by (tok >> 8) & 0x1FF (T12[(b2 << 8) | b1] = T1[b1] ^
+// T2[b2], exact: XOR tabulation is linear in the tables) -- two lookups per
+// evaluation instead of three in the same 3 x 64 KiB of shared memory.
+constexpr int LW = 5;
+__host__ __device__ constexpr int img_index(int L) { return L == LW ? 3 : L - 1; }  // cpsj_family::d_vimg / d_simg slot
+__host__ __device__ constexpr int tab_blocks(int L) { return L == LW ? 3 : L; }  // 64 KiB blocks per chunk
+
 // XOR of the L entries of token `tok`: [k][byte][l16] rows of 256 bytes
 template <int L>
 __device__ __forceinline__ uint4 key_oct(uint32_t tok, uint32_t lane_base) {
     uint4 h = lds128(lane_base + __byte_perm(tok, 0u, 0x4404));
+    if (L == LW) {
+        const uint4 v = lds128(lane_base + 65536u + (tok & 0x1FF00u));
+        h.x ^= v.x; h.y ^= v.y; h.z ^= v.z; h.w ^= v.w;
+        return h;
+    }
     if (L > 1) {
         const uint4 v = lds128(lane_base + 65536u + (tok & 0xFF00u));
         h.x ^= v.x; h.y ^= v.y; h.z ^= v.z; h.w ^= v.w;
@@ -561,6 +575,37 @@ __global__ void k_build_simg(const uint32_t *__restrict__ hi, const uint32_t *__
                         (v16[6] << 16) | v16[7]);
 }
 
+// the LW image of a chunk: 256 rows of T0, then 512 rows of T12 (see LW)
+__global__ void k_build_simg_wide(const uint32_t *__restrict__ hi, const uint32_t *__restrict__ bitmask, int F,
+                                  int64_t total, uint4 *__restrict__ img) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int64_t per_chunk = (int64_t)768 * 16;
+    const int c = (int)(e / per_chunk);
+    const int r = (int)(e - (int64_t)c * per_chunk);
+    const int row = r >> 4, ln = r & 15;
+    uint32_t v16[8];
+    for (int q = 0; q < 8; ++q) {
+        const int fn = (c << 7) + ln + 16 * q;
+        uint32_t v = 0, bit = 0;
+        if (fn < F) {
+            const size_t base = (size_t)fn * 1024;
+            const uint32_t *bm = bitmask != nullptr ? bitmask + (size_t)fn * 32 : nullptr;
+            if (row < 256) {
+                v = hi[base + row];
+                if (bm) bit = bm[row >> 5] >> (row & 31);
+            } else {
+                const int b1 = (row - 256) & 255, b2 = (row - 256) >> 8;
+                v = hi[base + 256 + b1] ^ hi[base + 512 + b2] ^ hi[base + 768];
+                if (bm) bit = (bm[8 + (b1 >> 5)] >> (b1 & 31)) ^ (bm[16 + (b2 >> 5)] >> (b2 & 31)) ^ bm[24];
+            }
+        }
+        v16[q] = bitmask != nullptr ? ((bit & 1u) << 15) | (v >> 17) : v >> 16;
+    }
+    img[e] = make_uint4((v16[0] << 16) | v16[1], (v16[2] << 16) | v16[3], (v16[4] << 16) | v16[5],
+                        (v16[6] << 16) | v16[7]);
+}
+
 __device__ __forceinline__ uint32_t vmin16x2(uint32_t a, uint32_t b) {
     uint32_t r;
     asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -608,8 +653,9 @@ __device__ __noinline__ uint32_t half_resolve15(const uint32_t *__restrict__ hi,
     for (int i = l; i < len; i += 16) {
         const uint32_t tk = __ldg(tokens + beg + i);
         uint32_t e = lds32(col + __byte_perm(tk, 0u, 0x4404));
-        if (L > 1) e ^= lds32(col + 65536u + (tk & 0xFF00u));
-        if (L > 2) e ^= lds32(col + 131072u + __byte_perm(tk, 0u, 0x4424));
+        if (L == LW) e ^= lds32(col + 65536u + (tk & 0x1FF00u));
+        if (L > 1 && L != LW) e ^= lds32(col + 65536u + (tk & 0xFF00u));
+        if (L == 3) e ^= lds32(col + 131072u + __byte_perm(tk, 0u, 0x4424));
         if (((e >> sh) & 0x7FFFu) == m15) {
             const uint32_t b0 = tk & 255, b1 = (tk >> 8) & 255, b2 = (tk >> 16) & 255, b3 = tk >> 24;
             const uint32_t h = __ldg(hi + base + b0) ^ __ldg(hi + base + 256 + b1) ^ __ldg(hi + base + 512 + b2) ^
@@ -690,7 +736,7 @@ __device__ __forceinline__ uint32_t sketch_chunk_bits(
             cached = __popc(b1) <= K1_PFX_MAX_RELOADS;
             if (cached) {
                 c1 = b1 >> (lane & 16);
-                if (L > 2) c2 = __ballot_sync(0xffffffffu, x > 0xFFFFu) >> (lane & 16);
+                if (L == 3) c2 = __ballot_sync(0xffffffffu, x > 0xFFFFu) >> (lane & 16);
                 prev_last = __shfl_sync(0xffffffffu, mine, 15, 16);
                 misses = 0;
             } else {
@@ -713,11 +759,11 @@ __device__ __forceinline__ uint32_t sketch_chunk_bits(
                         const uint32_t tk = __shfl_sync(0xffffffffu, mine, lane_g + jj, 16);
                         const uint4 e = lds128(lane_base + __byte_perm(tk, 0u, 0x4404));
                         if ((c1g >> jj) & 1u) {
-                            if (L > 2 && ((c2g >> jj) & 1u)) {
+                            if (L == 3 && ((c2g >> jj) & 1u)) {
                                 const uint4 v2 = lds128(lane_base + 131072u + __byte_perm(tk, 0u, 0x4424));
                                 P2[0] = v2.x; P2[1] = v2.y; P2[2] = v2.z; P2[3] = v2.w;
                             }
-                            const uint4 v = lds128(lane_base + 65536u + (tk & 0xFF00u));
+                            const uint4 v = lds128(lane_base + 65536u + (tk & (L == LW ? 0x1FF00u : 0xFF00u)));
                             P[0] = v.x ^ P2[0]; P[1] = v.y ^ P2[1]; P[2] = v.z ^ P2[2]; P[3] = v.w ^ P2[3];
                         }
                         k[u][0] = e.x ^ P[0]; k[u][1] = e.y ^ P[1]; k[u][2] = e.z ^ P[2]; k[u][3] = e.w ^ P[3];
@@ -857,7 +903,7 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k_sketch_s16(
     const int32_t *__restrict__ order, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
     const uint32_t *__restrict__ bitmask, const uint4 *__restrict__ simg, int F, const K1Out out, int split) {
     extern __shared__ __align__(128) uint4 tab4[];  // [L][256][16] x uint4, then the mbarrier
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + L * 256 * 16);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + tab_blocks(L) * 256 * 16);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tab4);
     const uint32_t lane_base = smem0 + ((uint32_t)(lane & 15) << 4);
@@ -876,7 +922,7 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k_sketch_s16(
     for (int c = c_first; c < c_last; ++c) {
         __syncthreads();  // every warp is done with the previous chunk's tables
         if (threadIdx.x == 0) {
-            const uint32_t tab_bytes = (uint32_t)L * 65536u;
+            const uint32_t tab_bytes = (uint32_t)tab_blocks(L) * 65536u;
             fence_proxy_async_smem();
             mbar_expect_tx(mbar_a, tab_bytes);
             const char *src = reinterpret_cast<const char *>(simg) + (size_t)c * tab_bytes;
@@ -912,8 +958,9 @@ __device__ __noinline__ uint32_t half_resolve16(const uint32_t *__restrict__ hi,
     for (int i = l; i < len; i += 16) {
         const uint32_t tk = __ldg(tokens + beg + i);
         uint32_t e = lds32(col + __byte_perm(tk, 0u, 0x4404));
-        if (L > 1) e ^= lds32(col + 65536u + (tk & 0xFF00u));
-        if (L > 2) e ^= lds32(col + 131072u + __byte_perm(tk, 0u, 0x4424));
+        if (L == LW) e ^= lds32(col + 65536u + (tk & 0x1FF00u));
+        if (L > 1 && L != LW) e ^= lds32(col + 65536u + (tk & 0xFF00u));
+        if (L == 3) e ^= lds32(col + 131072u + __byte_perm(tk, 0u, 0x4424));
         if (((e >> sh) & 0xFFFFu) == m16) {
             const uint32_t b0 = tk & 255, b1 = (tk >> 8) & 255, b2 = (tk >> 16) & 255, b3 = tk >> 24;
             const uint32_t h = __ldg(hi + base + b0) ^ __ldg(hi + base + 256 + b1) ^ __ldg(hi + base + 512 + b2) ^
@@ -950,7 +997,7 @@ __global__ void __launch_bounds__(K1V_THREADS, 1) k_values_h8(
     const int32_t *__restrict__ order, const uint32_t *__restrict__ hi, const uint32_t *__restrict__ lo,
     const uint4 *__restrict__ vimg, int F, const K1Out out) {
     extern __shared__ __align__(128) uint4 tab4[];  // [L][256][16] x uint4, then the mbarrier
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + L * 256 * 16);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(tab4 + tab_blocks(L) * 256 * 16);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int h = lane >> 4, l = lane & 15;
     const unsigned hmask = 0xFFFFu << (16 * h);
@@ -966,7 +1013,7 @@ __global__ void __launch_bounds__(K1V_THREADS, 1) k_values_h8(
     for (int c = 0; c < nchunks; ++c) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            const uint32_t tab_bytes = (uint32_t)L * 65536u;
+            const uint32_t tab_bytes = (uint32_t)tab_blocks(L) * 65536u;
             fence_proxy_async_smem();
             mbar_expect_tx(mbar_a, tab_bytes);
             const char *src = reinterpret_cast<const char *>(vimg) + (size_t)c * tab_bytes;
@@ -1330,7 +1377,7 @@ static void launch_embed_h8(cpsj_ctx *ctx, const cpsj_family *efam, const cpsj_f
 template <int L>
 static void launch_values_h8(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
                              int64_t n, const K1Out &out, cudaStream_t stream, const int32_t *order = nullptr) {
-    const int smem = L * 256 * 16 * 16 + 16;
+    const int smem = tab_blocks(L) * 256 * 16 * 16 + 16;
     CPSJ_CUDA(cudaFuncSetAttribute(k_values_h8<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     ProfScope prof(ctx, PROF_K1, stream);
     DevBuf<int32_t> own;
@@ -1341,7 +1388,7 @@ static void launch_values_h8(cpsj_ctx *ctx, const cpsj_family *fam, const uint32
     const int64_t want = ((n + 1) / 2 + K1V_WARPS - 1) / K1V_WARPS;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count));
     k_values_h8<L><<<grid, K1V_THREADS, smem, stream>>>(tok, off, n, order, fam->d_hi, fam->d_lo,
-                                                        reinterpret_cast<const uint4 *>(fam->d_vimg[L - 1]), fam->F,
+                                                        reinterpret_cast<const uint4 *>(fam->d_vimg[img_index(L)]), fam->F,
                                                         out);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
@@ -1350,7 +1397,7 @@ static void launch_values_h8(cpsj_ctx *ctx, const cpsj_family *fam, const uint32
 template <int L>
 static void launch_sketch_s16(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t *tok, const int64_t *off,
                               int64_t n, const K1Out &out, cudaStream_t stream, const int32_t *order = nullptr) {
-    const int smem = L * 256 * 16 * 16 + 16;
+    const int smem = tab_blocks(L) * 256 * 16 * 16 + 16;
     const bool pfx = k1_prefix_cache();
     auto kern = pfx ? k_sketch_s16<L, true> : k_sketch_s16<L, false>;
     CPSJ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1378,7 +1425,7 @@ static void launch_sketch_s16(cpsj_ctx *ctx, const cpsj_family *fam, const uint3
         grid = (int)std::min<int64_t>(want, (int64_t)ctx->sm_count / nchunks) * nchunks;
     }
     kern<<<grid, K1S_THREADS, smem, stream>>>(tok, off, n, order, fam->d_hi, fam->d_lo, fam->d_bitmask,
-                                              reinterpret_cast<const uint4 *>(fam->d_simg[L - 1]), fam->F, out, split);
+                                              reinterpret_cast<const uint4 *>(fam->d_simg[img_index(L)]), fam->F, out, split);
     CPSJ_LAUNCH_CHECK();
     ctx->launches++;
 }
@@ -1460,7 +1507,15 @@ void minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t 
         return;
     }
     const char *s16 = getenv("CPSJ_K1_NO_S16");  // A/B switch: sketches by the position-keyed kernels
+    // universes below 2^17 tokens: the folded T1/T2 table (LW), two lookups
+    // per evaluation; CPSJ_K1_NO_WIDE=1 (A/B) keeps three
+    const char *nw = getenv("CPSJ_K1_NO_WIDE");
+    const bool wide = L == 3 && max_token < (1u << 17) && !(nw && nw[0] == '1');
     if (want_sketch && !want_values && L < 4 && fam->d_simg[L - 1] != nullptr && !(s16 && s16[0] == '1')) {
+        if (wide && fam->d_simg[3] != nullptr) {
+            launch_sketch_s16<LW>(ctx, fam, d_tokens, d_offsets, n, out, stream);
+            return;
+        }
         switch (L) {
             case 1: launch_sketch_s16<1>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
             case 2: launch_sketch_s16<2>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
@@ -1470,6 +1525,10 @@ void minhash_sketch_multi(cpsj_ctx *ctx, const cpsj_family *fam, const uint32_t 
     }
     const char *h8 = getenv("CPSJ_K1_NO_H8");  // A/B switch: values by the full-warp kernel
     if (want_values && !want_sketch && L < 4 && fam->d_vimg[L - 1] != nullptr && !(h8 && h8[0] == '1')) {
+        if (wide && fam->d_vimg[3] != nullptr) {
+            launch_values_h8<LW>(ctx, fam, d_tokens, d_offsets, n, out, stream);
+            return;
+        }
         switch (L) {
             case 1: launch_values_h8<1>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
             case 2: launch_values_h8<2>(ctx, fam, d_tokens, d_offsets, n, out, stream); break;
@@ -1516,6 +1575,13 @@ void minhash_embed(cpsj_ctx *ctx, const cpsj_family *efam, const cpsj_family *sf
             return;
         }
         DevBuf<int32_t> order = length_order(ctx, d_offsets, n, stream);
+        const char *nw = getenv("CPSJ_K1_NO_WIDE");
+        if (L == 3 && max_token < (1u << 17) && !(nw && nw[0] == '1') && efam->d_vimg[3] != nullptr &&
+            sfam->d_simg[3] != nullptr) {
+            launch_values_h8<LW>(ctx, efam, d_tokens, d_offsets, n, vout, stream, order.p);
+            launch_sketch_s16<LW>(ctx, sfam, d_tokens, d_offsets, n, sout, stream, order.p);
+            return;
+        }
         switch (L) {
             case 1:
                 launch_values_h8<1>(ctx, efam, d_tokens, d_offsets, n, vout, stream, order.p);
@@ -1586,6 +1652,21 @@ void prepare_family(cpsj_ctx *ctx, cpsj_family *fam, const uint64_t *h_mh, const
             CPSJ_CUDA(cudaMalloc(&fam->d_simg[L - 1], elems8 * sizeof(uint4)));
             k_build_simg<<<(unsigned)((elems8 + 255) / 256), 256, 0, stream>>>(
                 fam->d_hi, fam->d_bitmask, fam->F, L, elems8, reinterpret_cast<uint4 *>(fam->d_simg[L - 1]));
+            CPSJ_LAUNCH_CHECK();
+            ctx->launches++;
+        }
+    }
+    {
+        const int64_t elemsw = (int64_t)nchunks * 768 * 16;
+        CPSJ_CUDA(cudaMalloc(&fam->d_vimg[3], elemsw * sizeof(uint4)));
+        k_build_simg_wide<<<(unsigned)((elemsw + 255) / 256), 256, 0, stream>>>(
+            fam->d_hi, nullptr, fam->F, elemsw, reinterpret_cast<uint4 *>(fam->d_vimg[3]));
+        CPSJ_LAUNCH_CHECK();
+        ctx->launches++;
+        if (fam->d_bitmask != nullptr) {
+            CPSJ_CUDA(cudaMalloc(&fam->d_simg[3], elemsw * sizeof(uint4)));
+            k_build_simg_wide<<<(unsigned)((elemsw + 255) / 256), 256, 0, stream>>>(
+                fam->d_hi, fam->d_bitmask, fam->F, elemsw, reinterpret_cast<uint4 *>(fam->d_simg[3]));
             CPSJ_LAUNCH_CHECK();
             ctx->launches++;
         }

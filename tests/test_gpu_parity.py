@@ -63,12 +63,13 @@ def test_sketch_kat():
     assert np.array_equal(build_sketch_matrix(fam, z["tokens"], z["offsets"]), z["sketch"])
 
 
-@pytest.mark.parametrize("L", [1, 2, 3, 4])
+@pytest.mark.parametrize("L", [1, 2, 3, 4, 5])
 def test_minhash_every_key_width_matches_oracle(L):
+    # L = 5: a 17-bit universe, the folded T1/T2 table layout (minhash.cu: LW)
     from oracle import oracle as O
     from paper_1707_06814_b200.hashing import minhash_segments_many
     rng = np.random.default_rng(L)
-    hi = (1 << (8 * L)) - 1
+    hi = (1 << 17) - 1 if L == 5 else (1 << (8 * L)) - 1
     rows = [np.unique(rng.integers(0, hi + 1, size=int(rng.integers(1, 300)), dtype=np.uint64)) for _ in range(400)]
     tok = np.concatenate(rows).astype(np.uint32)
     off = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
@@ -93,6 +94,33 @@ def test_minhash_high_word_ties_resolved_on_full_hash():
     assert np.array_equal(got, O.minhash(tok, off, tables))
 
 
+@pytest.mark.parametrize("env", [{}, {"CPSJ_K1_NO_PFX": "1"}, {"CPSJ_K1_FUSE": "1"}, {"CPSJ_K1_NO_SPLIT": "1"},
+                                 {"CPSJ_K1_NO_WIDE": "1"}, {"CPSJ_K1_NO_ORDER": "1"}])
+@pytest.mark.parametrize("cfg,scale,ell", [(2, 0.01, 8), (3, 0.02, 8), (4, 0.004, 16), (1, 0.3, 4)])
+def test_k1_alternate_paths_match_oracle(cfg, scale, ell, env, monkeypatch):
+    """Every K1 A/B switch (cached upper-byte entries off, the fused launch,
+    every CTA looping over the chunks, three lookups on a 17-bit universe, no
+    length order) gives the oracle's values and sketches: Zipf sets over 2^20
+    tokens, uniform sets over 2^17 (the folded-table layout), long sets with
+    1024 sketch functions, a 2-byte universe."""
+    from oracle import oracle as O
+    from paper_1707_06814_b200 import Dataset, EmbeddingParams, embed_dataset
+    from paper_1707_06814_b200.workloads import generate
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = generate(cfg, scale=scale)
+    ds = Dataset.from_csr(w.tokens, w.offsets, w.d)
+    emb = embed_dataset(EmbeddingParams(t=128, seed=7), ds, sketch=(ell, 9))
+    values = O.minhash(w.tokens, w.offsets, O.embedding_tables(128, 7))
+    mh, bt = O.sketch_tables(ell, 9)
+    sk = O.sketch(w.tokens, w.offsets, mh, bt)
+    assert np.array_equal(emb.values, values)
+    assert np.array_equal(emb.sketches(ell, 9), sk)
+    emb2 = embed_dataset(EmbeddingParams(t=128, seed=7), ds)  # separate values and sketch launches
+    assert np.array_equal(emb2.values, values)
+    assert np.array_equal(emb2.sketches(ell, 9), sk)
+
+
 def _sketch_gpu(mh, bt, tok, off, max_token):
     import torch
 
@@ -109,7 +137,7 @@ def _sketch_gpu(mh, bt, tok, off, max_token):
     return out.cpu().numpy().view(np.uint64)
 
 
-@pytest.mark.parametrize("L", [1, 2, 3, 4])
+@pytest.mark.parametrize("L", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("n_sets", [5, 3000])
 def test_sketch_15bit_ties_and_bit_disagreement(L, n_sets):
     # the sketch kernel compares (top 15 hash bits, sketch bit) keys; tables
@@ -118,7 +146,7 @@ def test_sketch_15bit_ties_and_bit_disagreement(L, n_sets):
     # full 64-bit ties (smallest token), empty and single-token sets
     from oracle import oracle as O
     rng = np.random.default_rng(100 + L)
-    hi = (1 << (8 * L)) - 1
+    hi = (1 << 17) - 1 if L == 5 else (1 << (8 * L)) - 1  # L = 5: the folded T1/T2 layout (LW)
     lens = rng.integers(0, 400, size=n_sets)
     lens[:3] = [0, 1, 2]
     rows = [np.unique(rng.integers(0, hi + 1, size=int(k), dtype=np.uint64)) for k in lens]
