@@ -330,8 +330,11 @@ __global__ void __launch_bounds__(TPB) k_leaf_small(SmallLeaves sl, const int64_
 // loop over the 32 row members; popcount(xor) <= accept passes the sketch
 // filter (matches >= k*), then the size filter; survivors are appended to
 // the candidate list with one atomic per warp (ballot + prefix).
+#ifndef CPSJ_LEAF_TILES_MINB
+#define CPSJ_LEAF_TILES_MINB 1
+#endif
 template <int ELL>
-__global__ void __launch_bounds__(TPB) k_leaf_tiles(
+__global__ void __launch_bounds__(TPB, CPSJ_LEAF_TILES_MINB) k_leaf_tiles(
     int64_t total_tiles, const int64_t *__restrict__ tile_off, int64_t N,
     const int64_t *__restrict__ nd_off, const int32_t *__restrict__ nd_cnt,
     const int32_t *__restrict__ members, const uint64_t *__restrict__ sketch, int ell_rt,
