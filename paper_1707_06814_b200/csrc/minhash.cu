@@ -985,6 +985,14 @@ __device__ __noinline__ uint32_t half_resolve16(const uint32_t *__restrict__ hi,
     return bt;
 }
 
+#ifndef VAL_G_FMA
+#define VAL_G_FMA 0
+#endif
+__device__ __forceinline__ uint32_t imad_reg(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;  // a * b + c on the FMA pipe
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
 __device__ __forceinline__ uint32_t imad16(uint32_t x, uint32_t add) {
     uint32_t r;  // x * 2^16 + add on the FMA pipe
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(65536u), "r"(add));
@@ -1004,6 +1012,9 @@ __global__ void __launch_bounds__(K1V_THREADS, 1) k_values_h8(
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(tab4);
     const uint32_t lane_base = smem0 + ((uint32_t)l << 4);
     const int nchunks = (F + 127) >> 7;
+#if VAL_G_FMA
+    const uint32_t one = (uint32_t)(F > 0);  // 1, opaque to the compiler
+#endif
     const int64_t npairs = (n + 1) >> 1;
     const int64_t p_first = (int64_t)blockIdx.x * K1V_WARPS + warp, p_step = (int64_t)gridDim.x * K1V_WARPS;
     const uint32_t mbar_a = (uint32_t)__cvta_generic_to_shared(mbar);
@@ -1064,8 +1075,17 @@ __global__ void __launch_bounds__(K1V_THREADS, 1) k_values_h8(
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
                             const uint32_t ma = xa[r] & 0xFFFF0000u, mb = xb[r] & 0xFFFF0000u;
+#if VAL_G_FMA
+                            // last-key of the high function from its first-key on the FMA
+                            // pipe: (h << 16 | p) + (q - p) = h << 16 | q (multiplier 1 in a
+                            // register the compiler cannot fold, so the add stays an IMAD)
+                            const uint32_t fa = ma | pa, fb = mb | pb;
+                            fk[2 * r] = __vimin3_u32(fk[2 * r], fa, fb);
+                            gk[2 * r] = __vimin3_u32(gk[2 * r], imad_reg(fa, one, qa - pa), imad_reg(fb, one, qb - pb));
+#else
                             fk[2 * r] = __vimin3_u32(fk[2 * r], ma | pa, mb | pb);
                             gk[2 * r] = __vimin3_u32(gk[2 * r], ma | qa, mb | qb);
+#endif
                             fk[2 * r + 1] = __vimin3_u32(fk[2 * r + 1], imad16(xa[r], pa), imad16(xb[r], pb));
                             gk[2 * r + 1] = __vimin3_u32(gk[2 * r + 1], imad16(xa[r], qa), imad16(xb[r], qb));
                         }
