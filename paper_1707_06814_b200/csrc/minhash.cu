@@ -795,8 +795,10 @@ __device__ __forceinline__ uint32_t sketch_chunk_bits(
         mine = mine_next;
     }
     // register j: function l + 32j in the high half (bit 2j), l + 32j + 16 in
-    // the low half (bit 2j + 1)
-    uint32_t bits = 0;
+    // the low half (bit 2j + 1).  Ties are rare (~0.15% of the functions), so
+    // the lanes first collect their tied slots in a mask and the half votes
+    // once; only a half with a tie walks the slots.
+    uint32_t bits = 0, tmask = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
@@ -808,16 +810,28 @@ __device__ __forceinline__ uint32_t sketch_chunk_bits(
             const uint32_t bit = u == sg ? u >> 15 : (h1 < u ? 1u : 0u);
             bits |= bit << q;
             const int f = (c << 7) + l + 32 * j + 16 * hl;
-            const bool tie = len > 1 && f < F && (u ^ sg) == 0x8000u;
-            unsigned tied = __ballot_sync(hmask, tie);
-            while (tied) {
-                const int src = __ffs(tied) - 1;
-                tied &= tied - 1;
-                const int fs = __shfl_sync(hmask, f, src);
-                const uint32_t m15 = __shfl_sync(hmask, u, src);
-                const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
-                const uint32_t tw = half_resolve15<L>(hi, lo, fs, m15, col, sh, tokens, beg, len, l, hmask);
-                if (lane == src) bits = (bits & ~(1u << q)) | (sketch_bit_g(bitmask, fs, tw) << q);
+            if (f < F && (u ^ sg) == 0x8000u) tmask |= 1u << q;
+        }
+    }
+    if (len <= 1) tmask = 0;
+    if (__ballot_sync(hmask, tmask != 0)) {  // uniform within the half
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int hl = 0; hl < 2; ++hl) {
+                const int sh = hl == 0 ? 16 : 0, q = 2 * j + hl;
+                const uint32_t u = (mU[j] >> sh) & 0xFFFFu;
+                const int f = (c << 7) + l + 32 * j + 16 * hl;
+                unsigned tied = __ballot_sync(hmask, (tmask >> q) & 1u);
+                while (tied) {
+                    const int src = __ffs(tied) - 1;
+                    tied &= tied - 1;
+                    const int fs = __shfl_sync(hmask, f, src);
+                    const uint32_t m15 = __shfl_sync(hmask, u, src);
+                    const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * j;
+                    const uint32_t tw = half_resolve15<L>(hi, lo, fs, m15, col, sh, tokens, beg, len, l, hmask);
+                    if (lane == src) bits = (bits & ~(1u << q)) | (sketch_bit_g(bitmask, fs, tw) << q);
+                }
             }
         }
     }
