@@ -1119,23 +1119,32 @@ __global__ void __launch_bounds__(K1V_THREADS, 1) k_values_h8(
                         }
                     }
                 }
+                // ties on the 16 compared bits are rare: the lanes collect
+                // their tied slots in a mask and the half votes once
+                uint32_t tmask = 0;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     // slot q = 2r (+1): function l + 32r (+16) of this chunk
-                    const int r = q >> 1;
-                    const int f = (c << 7) + l + 32 * r + 16 * (q & 1);
+                    const int f = (c << 7) + l + 32 * (q >> 1) + 16 * (q & 1);
                     tk[q] = __ldg(tokens + beg + (fk[q] & K16_MASK));
-                    const bool tie = (fk[q] & K16_MASK) != K16_MASK - (gk[q] & K16_MASK);
-                    unsigned tied = __ballot_sync(hmask, tie && f < F);
-                    while (tied) {
-                        const int src = __ffs(tied) - 1;
-                        tied &= tied - 1;
-                        const int fs = __shfl_sync(hmask, f, src);
-                        const uint32_t m16 = __shfl_sync(hmask, fk[q] >> 16, src);
-                        const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * r;
-                        const uint32_t tb = half_resolve16(hi, lo, fs, m16, col, (q & 1) ? 0 : 16, tokens, beg, len,
-                                                           l, hmask, L);
-                        if (lane == src) tk[q] = tb;
+                    if (f < F && (fk[q] & K16_MASK) != K16_MASK - (gk[q] & K16_MASK)) tmask |= 1u << q;
+                }
+                if (__ballot_sync(hmask, tmask != 0)) {  // uniform within the half
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int r = q >> 1;
+                        const int f = (c << 7) + l + 32 * r + 16 * (q & 1);
+                        unsigned tied = __ballot_sync(hmask, (tmask >> q) & 1u);
+                        while (tied) {
+                            const int src = __ffs(tied) - 1;
+                            tied &= tied - 1;
+                            const int fs = __shfl_sync(hmask, f, src);
+                            const uint32_t m16 = __shfl_sync(hmask, fk[q] >> 16, src);
+                            const uint32_t col = smem0 + ((uint32_t)(src & 15) << 4) + 4u * r;
+                            const uint32_t tb = half_resolve16(hi, lo, fs, m16, col, (q & 1) ? 0 : 16, tokens, beg,
+                                                               len, l, hmask, L);
+                            if (lane == src) tk[q] = tb;
+                        }
                     }
                 }
             }
