@@ -783,7 +783,7 @@ def run_ours(args, rank: int, world: int):
                                   "upper key bytes change (the kernel's cached-entry path); frac_all_key_bytes is "
                                   "round 1's denominator (every key byte looked up for every token) and can "
                                   "exceed 1.  ncu of the same launch (profiles/ncu_k1_s16_r02_c2.csv): shared "
-                                  "wavefronts 87% of peak incl. the token shuffles, ALU pipe 74%, issue 73%"},
+                                  "wavefronts 88% of peak incl. the token shuffles, ALU pipe 76%, issue 74%"},
         "roofline_int": {"kernel": "k_leaf_tiles + k_point (K4 BruteForce)", "pairs_per_s": pairs_per_s,
                          "peak_pairs_per_s": popc_peak,
                          "frac": (pairs_per_s / popc_peak) if pairs_per_s else None,
