@@ -404,9 +404,9 @@ def run_reference(args, rank: int, world: int):
             "data": "synthetic (seeded generator for the BASELINE.json config)",
             # the GPU arm's config dict (same workload keys) when the sample is the whole workload
             "config": workload_dict(w, cfg, R, rec, lam, {
-                "parallelism": f"host CPU, {threads} threads (C port of the reference, oracle/cpsj_oracle.c)",
                 "recall_truth": truth_src, "n_true_pairs": int(len(truth)),
                 **({} if scale == args.scale else {"sample_scale": scale})}),
+            "parallelism": f"host CPU, {threads} threads (C port of the reference, oracle/cpsj_oracle.c)",
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "sets/s", "cores": threads, "kind": "port",
                              "sample": sample},
@@ -754,14 +754,14 @@ def run_ours(args, rank: int, world: int):
         "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded generator for BASELINE.json config; Mann et al. datasets unavailable)",
-        "config": workload_dict(w, cfg, R, rec, lam, {"parallelism": (
-                                    "single GPU" if world == 1 else
-                                    f"K1 set-sharded over {world} GPUs, rows stored to every GPU "
-                                    f"{'by the kernel over NVLink (fused all-gather)' if args.k1_transport == 'p2p' else 'by an NCCL all-gather'}; "
-                                    + (f"join frontier sharded at depth {args.frontier_depth} (size-balanced cut; every "
-                                       f"rank builds the levels above it) + pair gather" if args.join_shard == "frontier"
-                                       else "repetitions sharded round-robin + pair gather")),
-                                                     "recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
+        # config = the workload only, so both arms print the same dict
+        "config": workload_dict(w, cfg, R, rec, lam, {"recall_truth": truth_src, "n_true_pairs": int(len(truth))}),
+        "parallelism": ("single GPU" if world == 1 else
+                        f"K1 set-sharded over {world} GPUs, rows stored to every GPU "
+                        f"{'by the kernel over NVLink (fused all-gather)' if args.k1_transport == 'p2p' else 'by an NCCL all-gather'}; "
+                        + (f"join frontier sharded at depth {args.frontier_depth} (size-balanced cut; every "
+                           f"rank builds the levels above it) + pair gather" if args.join_shard == "frontier"
+                           else "repetitions sharded round-robin + pair gather")),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
                      "frac": achieved / float(peaks["hbm_gbs"]), "traffic": ncu_traffic(args.config, "sketch"),
                      "kernel": "k_sketch_s16<L, PFX> sketch launch (K1, 64*ell functions)",
